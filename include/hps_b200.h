@@ -1,0 +1,79 @@
+/* hps_b200.h -- C ABI of the B200-native HPS build/solve hot path (libhps_b200.so).
+ *
+ * All pointers are DEVICE pointers unless noted. All matrices are fp64 row-major. `stream` is a
+ * cudaStream_t passed as void*. Every entry point returns a status code. On HPS_ERR_* the call
+ * sets a message, readable through hps_last_error(). Numerical failures are reported through
+ * device-side status words (-1 = ok), so a whole build can be enqueued without host syncs.
+ *
+ * Reference interfaces replaced (the reference is pure Python; these are its BLAS/LAPACK call
+ * sites):
+ *   hps_leaf_stage   <- solver._leaf_stage chunk loop, solver.py:226-246
+ *                       (assemble_operator leafops.py:217-233, interior_solve_batch
+ *                        leafops.py:273-295, DtN product solver.py:241-242)
+ *   hps_merge_level  <- merge.merge_dtn, merge.py:92-119, for all 2^d parents of one depth
+ *                       (the dense-branch loop body of solver.build, solver.py:266-285)
+ *   hps_solve_level  <- SolutionOperator.apply inside solver.solve, solver.py:93-97 / 312-315,
+ *                       for all parents of one depth and a batch of right-hand sides
+ *   hps_dgemm_batched <- the BLAS dgemm behind `@` (merge.py:118, solver.py:71 apply_global_dtn)
+ */
+#ifndef HPS_B200_H
+#define HPS_B200_H
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPS_OK 0
+#define HPS_ERR_LEAF_RESONANCE 1
+#define HPS_ERR_MERGE_RESONANCE 2
+#define HPS_ERR_CUDA 3
+#define HPS_ERR_NCCL 4
+#define HPS_ERR_ARG 5
+
+const char* hps_last_error(void);
+int hps_version(void);
+int hps_device_check(int* major, int* minor, int* sms);
+
+/* Leaf stage for `ngroups` distinct coefficient groups (leaves with bitwise-equal samples share a
+ * group, solver.py:208-222).
+ *   fields[6]  host array of device pointers (ngroups x p^2 samples, x1-major grid) or NULL
+ *   scalars[6] host array; used where fields[f] == NULL; a scalar 0 skips the term
+ *   consts     Dx, Dy, Dx@Dx, Dy@Dy (p^2 each), L43[:,J_e] (4p x nb), L43[:,J_i] (4p x ni),
+ *              L1 (nb x 4p), probe (ni); ni = (p-2)^2, nb = 4(p-1)
+ *   idx        int32 J_i (ni), J_e (nb)
+ * Outputs: Psi (ngroups x ni x nb), T (ngroups x 4p x 4p), cond (ngroups, probe estimate of
+ * leafops.py:293-294; the caller raises LeafResonanceError if cond > 1e13). */
+size_t hps_leaf_workspace_bytes(int p, int ngroups);
+int hps_leaf_stage(int p, int ngroups, const double* const* fields, const double* scalars,
+                   const double* consts, const int* idx, double probe_max, double* Psi, double* T,
+                   double* cond, void* ws, size_t ws_bytes, void* stream);
+
+/* All 2^d merges of one depth. Children of merge b are T_child + child_idx[2b(+1)]*child_stride
+ * (child_idx NULL => 2b, 2b+1), each m x m with m = ne/2 + n3.
+ *   maps   int32 j1a (ne/2), j2b (ne/2), j3a (n3), j3b (n3)   (merge.py:27-89 split positions)
+ *   vmode  q start + q end values of the corner null mode on one interface segment
+ * Outputs S_out (nbatch x n3 x ne), T_out (nbatch x ne x ne). *status (device int, init -1) is raised to
+ * the largest merge index whose interface system is singular or whose S is non-finite
+ * (MergeResonanceError, merge.py:106-112). */
+size_t hps_merge_workspace_bytes(int nbatch, int n3, int ne);
+int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const double* T_child,
+                    long long child_stride, const int* child_idx, const int* maps,
+                    const double* vmode, double* S_out, double* T_out, void* ws, size_t ws_bytes,
+                    int* status, int status_base, void* stream);
+
+/* u[ii_start0 + b*n3 + r, :nrhs] = sum_c S[b][r][c] * u[Ie[b][c], :nrhs] for all nbatch parents of
+ * one depth; u is node-major with leading dimension ldu (solver.py:312-315). */
+int hps_solve_level(int nbatch, int n3, int ne, const double* S, const int* Ie, long long ii_start0,
+                    double* u, int ldu, int nrhs, void* stream);
+
+/* C[b] = alpha A[b] B[b] + beta C[b]; optional B-row gather Bidx (NULL = none). K % 16 == 0. */
+int hps_dgemm_batched(int M, int N, int K, int batch, double alpha, const double* A, long long lda,
+                      long long strideA, const double* B, long long ldb, long long strideB,
+                      const int* Bidx, long long strideBidx, double beta, double* C, long long ldc,
+                      long long strideC, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,109 @@
+"""ctypes binding of libhps_b200.so (the C ABI declared in include/hps_b200.h).
+
+There is no fallback. If the library is missing or no sm_100 device is visible, every entry point
+raises. The product path never computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import NativeError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhps_b200.so")
+
+HPS_OK = 0
+HPS_ERR_LEAF_RESONANCE = 1
+HPS_ERR_MERGE_RESONANCE = 2
+HPS_ERR_CUDA = 3
+HPS_ERR_NCCL = 4
+HPS_ERR_ARG = 5
+
+#: every symbol include/hps_b200.h declares (tests check the .so exports all of them)
+EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_leaf_workspace_bytes",
+           "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
+           "hps_dgemm_batched")
+
+_lib = None
+
+c_dp = ctypes.c_void_p
+c_ll = ctypes.c_longlong
+c_int = ctypes.c_int
+c_sz = ctypes.c_size_t
+c_d = ctypes.c_double
+
+
+def load():
+    """Load the shared library (no device work). Raises ImportError if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() or csrc/build.sh; "
+                          "there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.hps_last_error.restype = ctypes.c_char_p
+    lib.hps_version.restype = c_int
+    lib.hps_device_check.argtypes = [ctypes.POINTER(c_int)] * 3
+    lib.hps_device_check.restype = c_int
+    lib.hps_leaf_workspace_bytes.argtypes = [c_int, c_int]
+    lib.hps_leaf_workspace_bytes.restype = c_sz
+    lib.hps_leaf_stage.argtypes = [c_int, c_int, ctypes.POINTER(c_dp), ctypes.POINTER(c_d), c_dp, c_dp, c_d,
+                                   c_dp, c_dp, c_dp, c_dp, c_sz, c_dp]
+    lib.hps_leaf_stage.restype = c_int
+    lib.hps_merge_workspace_bytes.argtypes = [c_int, c_int, c_int]
+    lib.hps_merge_workspace_bytes.restype = c_sz
+    lib.hps_merge_level.argtypes = [c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp, c_dp,
+                                    c_dp, c_sz, c_dp, c_int, c_dp]
+    lib.hps_merge_level.restype = c_int
+    lib.hps_solve_level.argtypes = [c_int, c_int, c_int, c_dp, c_dp, c_ll, c_dp, c_int, c_int, c_dp]
+    lib.hps_solve_level.restype = c_int
+    lib.hps_dgemm_batched.argtypes = [c_int, c_int, c_int, c_int, c_d, c_dp, c_ll, c_ll, c_dp, c_ll, c_ll, c_dp,
+                                      c_ll, c_d, c_dp, c_ll, c_ll, c_dp]
+    lib.hps_dgemm_batched.restype = c_int
+    _lib = lib
+    return lib
+
+
+def check(status, what):
+    if status != HPS_OK:
+        msg = load().hps_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed (status {status}): {msg}")
+
+
+_device_ok = False
+
+
+def require_device():
+    """Fail loudly unless an sm_100 device is usable through the library."""
+    global _device_ok
+    if _device_ok:
+        return
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeError("the HPS B200 path needs a CUDA device (sm_100a); there is no CPU fallback")
+    lib = load()
+    ma, mi, sms = c_int(), c_int(), c_int()
+    check(lib.hps_device_check(ctypes.byref(ma), ctypes.byref(mi), ctypes.byref(sms)), "hps_device_check")
+    _device_ok = True
+
+
+def ptr(t):
+    """Device pointer of a C-contiguous tensor (None -> NULL). The kernels assume row-major
+    dense storage; a strided view would be silently misread, so it is rejected here."""
+    if t is None:
+        return ctypes.c_void_p(0)
+    if not t.is_contiguous():
+        raise NativeError(f"non-contiguous tensor passed to the C ABI: shape {tuple(t.shape)} "
+                          f"stride {tuple(t.stride())}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream=None):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)

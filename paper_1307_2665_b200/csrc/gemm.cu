@@ -1,0 +1,46 @@
+// Host launcher for the DMMA GEMM (tile selection) + the C-ABI test hook.
+#include "gemm.cuh"
+
+namespace hps {
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+static int launch_cfg(const GemmParams& p, cudaStream_t stream) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
+  auto kern = dgemm_dmma_kernel<BM, BN, BK, WM, WN, STAGES>;
+  static bool attr_set = false;  // per-instantiation
+  if (!attr_set) {
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    attr_set = true;
+  }
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.batch);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(p);
+  HPS_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
+  if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return HPS_OK;
+  if (p.K % 16 != 0 || p.N % 2 != 0 || (p.ldb % 2) || (p.ldc % 2) || (p.lda % 2) ||
+      (p.strideA % 2) || (p.strideB % 2) || (p.strideC % 2) ||
+      (reinterpret_cast<uintptr_t>(p.A) & 15) || (reinterpret_cast<uintptr_t>(p.B) & 15) ||
+      (reinterpret_cast<uintptr_t>(p.C) & 15)) {
+    set_error("dgemm: unsupported shape/alignment M=%d N=%d K=%d lda=%lld ldb=%lld ldc=%lld", p.M, p.N, p.K,
+              p.lda, p.ldb, p.ldc);
+    return HPS_ERR_ARG;
+  }
+  if (p.K == 0) return HPS_OK;
+  double tiles128 = double((p.M + 127) / 128) * double((p.N + 127) / 128) * p.batch;
+  if (p.M >= 128 && p.N >= 128 && tiles128 >= 148.0) return launch_cfg<128, 128, 16, 2, 4, 4>(p, stream);
+  return launch_cfg<64, 64, 16, 2, 2, 3>(p, stream);
+}
+
+}  // namespace hps
+
+extern "C" int hps_dgemm_batched(int M, int N, int K, int batch, double alpha, const double* A, long long lda,
+                                 long long strideA, const double* B, long long ldb, long long strideB,
+                                 const int* Bidx, long long strideBidx, double beta, double* C, long long ldc,
+                                 long long strideC, void* stream) {
+  hps::GemmParams p{M, N, K, batch, A, lda, strideA, B, ldb, strideB, Bidx, strideBidx, C, ldc, strideC,
+                    alpha, beta, nullptr};
+  return hps::dgemm_launch(p, static_cast<cudaStream_t>(stream));
+}

@@ -1,0 +1,155 @@
+// Batched fp64 GEMM on the DMMA pipe (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4), sm_100a.
+//
+//   C[b] = alpha * A[b] * B[b] + beta * C[b]     (all row-major)
+//
+// B rows may be gathered through an index table (the solve's u[I_e] gather). This one kernel
+// carries every bulk flop of the merge levels (S = X^-1 R, T += C S, the recursive interface
+// inverse) and of the batched solve. tcgen05 has no f64 kind on sm_100a, so DMMA is the FP64
+// tensor path (measured 37.1 TF/s peak on B200 vs 34.2 for DFMA; profiles/fp64_peak_r01.json).
+//
+// Tiling: CTA tile BM x BN x BK, STAGES-deep cp.async pipeline. Smem strides are padded so every
+// fragment load is a 2-wavefront LDS.64 (A: stride = BK+4 doubles, B: stride = BN+8 doubles).
+#pragma once
+#include "common.cuh"
+
+namespace hps {
+
+struct GemmParams {
+  int M, N, K, batch;
+  const double* A; long long lda, strideA;
+  const double* B; long long ldb, strideB;
+  const int* Bidx; long long strideBidx;  // optional: row k of B[b] is B[b] + Bidx[b*strideBidx + k]*ldb
+  double* C; long long ldc, strideC;
+  double alpha, beta;
+  int* nonfinite;  // optional: set to max batch index with a non-finite output
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+struct GemmCfg {
+  static constexpr int kThreads = WM * WN * 32;
+  static constexpr int SA = BK + 4;
+  static constexpr int SB = BN + 8;
+  static constexpr int kStageA = BM * SA;
+  static constexpr int kStageB = BK * SB;
+  static constexpr size_t kSmem = size_t(STAGES) * (kStageA + kStageB) * sizeof(double);
+  static constexpr int TM = BM / WM / 8;
+  static constexpr int TN = BN / WN / 8;
+  static_assert(BM % (WM * 8) == 0 && BN % (WN * 8) == 0 && BK % 4 == 0, "tile");
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32)
+dgemm_dmma_kernel(GemmParams p) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
+  extern __shared__ __align__(128) double smem[];
+  double* sA = smem;
+  double* sB = smem + STAGES * Cfg::kStageA;
+
+  const int b = blockIdx.z;
+  const int m0 = blockIdx.y * BM;
+  const int n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const int g = lane >> 2, t = lane & 3;
+
+  const double* A = p.A + (long long)b * p.strideA;
+  const double* B = p.B + (long long)b * p.strideB;
+  const int* Bidx = p.Bidx ? p.Bidx + (long long)b * p.strideBidx : nullptr;
+  double* C = p.C + (long long)b * p.strideC;
+
+  const int ktiles = p.K / BK;  // K % BK == 0 enforced by the launcher
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* a_dst = sA + stage * Cfg::kStageA;
+    constexpr int A_CHUNKS = BM * BK / 2;
+#pragma unroll
+    for (int c = tid; c < A_CHUNKS; c += Cfg::kThreads) {
+      int r = c / (BK / 2), cc = c % (BK / 2);
+      int gr = m0 + r;
+      bool ok = gr < p.M;
+      const double* src = A + (long long)(ok ? gr : 0) * p.lda + k0 + 2 * cc;
+      cp_async16(a_dst + r * Cfg::SA + 2 * cc, src, ok);
+    }
+    double* b_dst = sB + stage * Cfg::kStageB;
+    constexpr int B_CHUNKS = BK * BN / 2;
+#pragma unroll
+    for (int c = tid; c < B_CHUNKS; c += Cfg::kThreads) {
+      int r = c / (BN / 2), cc = c % (BN / 2);
+      int gc = n0 + 2 * cc;
+      bool ok = gc < p.N;
+      long long row = Bidx ? (long long)Bidx[k0 + r] : (long long)(k0 + r);
+      const double* src = B + row * p.ldb + (ok ? gc : 0);
+      cp_async16(b_dst + r * Cfg::SB + 2 * cc, src, ok);
+    }
+  };
+
+  double acc[Cfg::TM][Cfg::TN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  const int a_row0 = wm * (BM / WM) + g;
+  const int b_col0 = wn * (BN / WN) + g;
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {  // prefetch tile kt + STAGES - 1 into the slot freed last iteration
+      int nk = kt + STAGES - 1;
+      if (nk < ktiles) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* a_s = sA + (kt % STAGES) * Cfg::kStageA;
+    const double* b_s = sB + (kt % STAGES) * Cfg::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[Cfg::TM], bf[Cfg::TN];
+#pragma unroll
+      for (int i = 0; i < Cfg::TM; ++i) af[i] = a_s[(a_row0 + i * 8) * Cfg::SA + kk + t];
+#pragma unroll
+      for (int j = 0; j < Cfg::TN; ++j) bf[j] = b_s[(kk + t) * Cfg::SB + b_col0 + j * 8];
+#pragma unroll
+      for (int i = 0; i < Cfg::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::TN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < Cfg::TM; ++i) {
+    int r = m0 + a_row0 + i * 8;
+    if (r >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < Cfg::TN; ++j) {
+      int c = n0 + wn * (BN / WN) + j * 8 + 2 * t;
+      if (c >= p.N) continue;
+      double* dst = C + (long long)r * p.ldc + c;
+      double2 v;
+      v.x = p.alpha * acc[i][j][0];
+      v.y = p.alpha * acc[i][j][1];
+      if (p.beta != 0.0) {
+        double2 o = *reinterpret_cast<const double2*>(dst);
+        v.x += p.beta * o.x;
+        v.y += p.beta * o.y;
+      }
+      bad |= !isfinite(v.x) || !isfinite(v.y);
+      *reinterpret_cast<double2*>(dst) = v;
+    }
+  }
+  if (p.nonfinite && bad) atomicMax(p.nonfinite, b);
+}
+
+// Launch with a tile shape picked from the problem size. Returns HPS_OK or an error code.
+int dgemm_launch(const GemmParams& p, cudaStream_t stream);
+
+}  // namespace hps

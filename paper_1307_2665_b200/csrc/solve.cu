@@ -1,0 +1,70 @@
+// Downward pass (reference solver.py:303-316): for every parent at one depth,
+//   u[I_i(box)] = S_box u[I_e(box)]
+// for a batch of boundary vectors. u is node-major (N x ldu, RHS contiguous). I_e rows are
+// gathered through the per-depth id table. I_i is contiguous (start0 + b*n3 ...), so the output
+// is a plain strided store. Large batches go through the DMMA GEMM (B-row gather). For
+// nrhs <= 8 a warp-per-row kernel streams S once (HBM-bound, like a batched GEMV).
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace hps {
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_solve_small(const double* __restrict__ S, const int* __restrict__ Ie,
+                                                     long long ii_start0, int n3, int ne,
+                                                     double* __restrict__ u, int ldu) {
+  const int b = blockIdx.x;
+  const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n3) return;
+  const double* Sr = S + ((long long)b * n3 + r) * ne;
+  const int* ie = Ie + (long long)b * ne;
+  double acc[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+  for (int c = lane; c < ne; c += 32) {
+    const double s = __ldg(Sr + c);
+    const double* uc = u + (long long)__ldg(ie + c) * ldu;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) acc[j] = fma(s, uc[j], acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j] = warp_sum(acc[j]);
+  if (lane < NR) {
+    double v = acc[0];
+#pragma unroll
+    for (int j = 1; j < NR; ++j)
+      if (lane == j) v = acc[j];
+    u[(ii_start0 + (long long)b * n3 + r) * ldu + lane] = v;
+  }
+}
+
+}  // namespace hps
+
+using namespace hps;
+
+extern "C" int hps_solve_level(int nbatch, int n3, int ne, const double* S, const int* Ie, long long ii_start0,
+                               double* u, int ldu, int nrhs, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (nbatch <= 0 || nrhs <= 0) return HPS_OK;
+  if (nrhs > ldu) {
+    set_error("hps_solve_level: nrhs > ldu");
+    return HPS_ERR_ARG;
+  }
+  if (nrhs <= 8) {
+    dim3 grid(nbatch, (n3 + 7) / 8);
+    switch (nrhs) {
+#define HPS_SOLVE_CASE(R) \
+  case R: k_solve_small<R><<<grid, 256, 0, st>>>(S, Ie, ii_start0, n3, ne, u, ldu); break;
+      HPS_SOLVE_CASE(1) HPS_SOLVE_CASE(2) HPS_SOLVE_CASE(3) HPS_SOLVE_CASE(4)
+      HPS_SOLVE_CASE(5) HPS_SOLVE_CASE(6) HPS_SOLVE_CASE(7) HPS_SOLVE_CASE(8)
+#undef HPS_SOLVE_CASE
+    }
+    HPS_LAUNCH_CHECK();
+    return HPS_OK;
+  }
+  // GEMM: C = u rows [start0 + b*n3, +n3), A = S[b] (n3 x ne), B = u[Ie[b]] (ne x nrhs)
+  GemmParams p{n3, nrhs, ne, nbatch, S, ne, (long long)n3 * ne, u, ldu, 0, Ie, ne,
+               u + ii_start0 * ldu, ldu, (long long)n3 * ldu, 1.0, 0.0, nullptr};
+  return dgemm_launch(p, st);
+}

@@ -1,0 +1,544 @@
+"""Build and solve stages on B200: drop-in for `hpsolve.solver` (reference solver.py:40-50).
+
+Host code only. It samples coefficients, groups leaves, owns device memory (through torch) and
+enqueues the C-ABI calls: one leaf-stage call, one merge call per depth, one solve call per depth.
+All arithmetic runs in libhps_b200.so. The returned `SolverState` has the reference's
+attributes. The device-resident operators (`S`, `psi`, `root_T`) are copied to numpy only when
+accessed.
+
+Differences from the reference, all documented in DESIGN.md:
+  * `eps`, `switch_threshold` and `hbs_leaf_size` are accepted and ignored. The GPU path is
+    dense by design; the reference's HBS branch is out of scope.
+  * The interface systems are deflated along their analytic corner null modes, so `S` is the
+    unique gauge-fixed solution (V^T S = 0) instead of the reference's rounding-dependent one.
+    T, and every null-mode-invariant function of u, match the reference.
+  * `solve` also accepts a batch F of shape (|Gamma|, b) and returns (N, b).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native, instrumentation
+from .errors import LeafResonanceError, MergeResonanceError
+from .grid import interp_matrix, layout_of
+from .leafops import RESONANCE_COND, LeafGeometry
+
+__all__ = [
+    "DtnOperator",
+    "SolutionOperator",
+    "SolverState",
+    "build",
+    "solve",
+    "solve_device",
+    "apply_global_dtn",
+    "post_process",
+    "boundary_flux_at",
+    "memory_report",
+]
+
+COEFF_NAMES = ("c11", "c12", "c22", "c1", "c2", "c")
+ctypes_vp = ctypes.c_void_p
+ctypes_d = ctypes.c_double
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ----------------------------------------------------------------------------------------------
+# Reference-shaped operator containers (solver.py:53-119), backed by device tensors
+# ----------------------------------------------------------------------------------------------
+class DtnOperator:
+    """A box DtN map (solver.py:53-77). `dense` materialises the device tensor to numpy."""
+
+    def __init__(self, dense=None, hbs=None, device_tensor=None):
+        if hbs is not None:
+            raise ValueError("the B200 path is dense-only (HBS is out of scope)")
+        if (dense is None) == (device_tensor is None):
+            raise ValueError("exactly one of dense/device_tensor required")
+        self._host = dense
+        self.device_tensor = device_tensor
+        self.hbs = None
+
+    @property
+    def dense(self):
+        if self._host is None:
+            self._host = self.device_tensor.cpu().numpy()
+        return self._host
+
+    @property
+    def is_dense(self):
+        return True
+
+    @property
+    def dim(self):
+        t = self.device_tensor if self.device_tensor is not None else self._host
+        return t.shape[0]
+
+    def apply(self, x):
+        return self.dense @ x
+
+    def to_dense(self):
+        return self.dense
+
+    def n_stored_entries(self):
+        t = self.device_tensor if self.device_tensor is not None else self._host
+        return int(np.prod(t.shape))
+
+
+class SolutionOperator:
+    """Parent map u_e -> u_i (solver.py:80-102), a view into the per-depth device S tensor."""
+
+    def __init__(self, dense=None, factors=None, device_tensor=None):
+        if factors is not None:
+            raise ValueError("the B200 path is dense-only (low-rank factors are out of scope)")
+        self._host = dense
+        self.device_tensor = device_tensor
+        self.factors = None
+
+    @property
+    def dense(self):
+        if self._host is None:
+            self._host = self.device_tensor.cpu().numpy()
+        return self._host
+
+    @property
+    def is_dense(self):
+        return True
+
+    def apply(self, u_e):
+        return self.dense @ u_e
+
+    def n_stored_entries(self):
+        t = self.device_tensor if self.device_tensor is not None else self._host
+        return int(np.prod(t.shape))
+
+
+class _LazyS(Mapping):
+    """parent box index -> SolutionOperator over the per-depth S tensors."""
+
+    def __init__(self, S_levels, L):
+        self._S = S_levels
+        self._n = (1 << (2 * L)) - 1
+
+    def __getitem__(self, idx):
+        if not 0 <= idx < self._n:
+            raise KeyError(idx)
+        d = int(math.floor(math.log2(idx + 1)))
+        return SolutionOperator(device_tensor=self._S[d][idx - ((1 << d) - 1)])
+
+    def __iter__(self):
+        return iter(range(self._n))
+
+    def __len__(self):
+        return self._n
+
+
+class _LazyPsi(Mapping):
+    """leaf box index -> Psi (numpy); leaves of one coefficient group share one array object."""
+
+    def __init__(self, psi_groups, leaf_group, first_leaf):
+        self._dev = psi_groups
+        self._gid = leaf_group
+        self._first = first_leaf
+        self._host = {}
+
+    def group_array(self, g):
+        a = self._host.get(g)
+        if a is None:
+            a = self._dev[g].cpu().numpy()
+            self._host[g] = a
+        return a
+
+    def __getitem__(self, idx):
+        k = idx - self._first
+        if not 0 <= k < self._gid.size:
+            raise KeyError(idx)
+        return self.group_array(int(self._gid[k]))
+
+    def __iter__(self):
+        return iter(range(self._first, self._first + self._gid.size))
+
+    def __len__(self):
+        return int(self._gid.size)
+
+
+@dataclass
+class SolverState:
+    """All built operators (solver.py:105-119) plus the device-resident level tensors."""
+
+    tree: object
+    nodes: object
+    coeffs: object
+    q: int
+    eps: float
+    switch_threshold: float
+    hbs_leaf_size: int
+    geometry: LeafGeometry
+    psi: Mapping
+    S: Mapping
+    root_T: DtnOperator
+    rank_stats: dict = field(default_factory=dict)
+    n_leaf_groups: int = 0
+    # device side
+    layout: object = None
+    S_levels: list = None
+    Ie_levels: list = None
+    psi_groups: object = None
+    T_leaf_groups: object = None
+    leaf_group: np.ndarray = None
+    root_Ie_dev: object = None
+    device: object = None
+    level_T: list = None  # per-depth T tensors when build(..., keep_level_T=True)
+
+
+# ----------------------------------------------------------------------------------------------
+# Build
+# ----------------------------------------------------------------------------------------------
+def _sample(coeffs, lay, geom):
+    """Coefficient samples on all leaf Chebyshev grids, heap leaf order (solver.py:196-206)."""
+    lc = lay.leaf_cells
+    xs = lay.xline[lc[:, 0]][:, None] + geom.grid_x[None, :]
+    ys = lay.yline[lc[:, 1]][:, None] + geom.grid_y[None, :]
+    fields = {}
+    for name in COEFF_NAMES:
+        f = getattr(coeffs, name)
+        fields[name] = f(xs, ys) if callable(f) else float(f)
+        v = np.atleast_1d(fields[name])
+        if not np.all(np.isfinite(v)):
+            bad = np.argwhere(~np.isfinite(np.broadcast_to(fields[name], xs.shape)))
+            i, k = (bad[0] if bad.size else (0, 0))
+            raise ValueError(f"coefficient {name} is not finite at node ({xs[i, k]}, {ys[i, k]})")
+        if not np.isscalar(fields[name]):
+            fields[name] = np.ascontiguousarray(np.broadcast_to(np.asarray(fields[name], dtype=float), xs.shape))
+    return fields
+
+
+def _group(fields, n_leaf):
+    """Group leaves whose six sample rows are bitwise equal (solver.py:208-222).
+
+    Returns (rep leaf positions in first-occurrence order, group id per leaf)."""
+    arrays = [fields[n] for n in COEFF_NAMES if not np.isscalar(fields[n])]
+    if not arrays:
+        return np.zeros(1, np.int64), np.zeros(n_leaf, np.int64)
+    rows = np.ascontiguousarray(np.concatenate(arrays, axis=1)).view(np.uint8).reshape(n_leaf, -1)
+    key = rows.view(np.dtype((np.void, rows.shape[1]))).reshape(n_leaf)
+    _, first, inv = np.unique(key, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")
+    rank = np.empty_like(order)
+    rank[order] = np.arange(order.size)
+    return first[order].astype(np.int64), rank[inv.reshape(-1)].astype(np.int64)
+
+
+class _DeviceLayout:
+    """Per-(tree, device) int32 tables: merge split maps, corner-mode vectors, I_e gathers."""
+
+    _cache = {}
+
+    @classmethod
+    def get(cls, lay, geom, device):
+        key = (id(lay), geom.p, geom.width, geom.height, str(device))
+        v = cls._cache.get(key)
+        if v is None:
+            v = cls(lay, geom, device)
+            cls._cache[key] = v
+        return v
+
+    def __init__(self, lay, geom, device):
+        torch = _torch()
+        self.maps, self.vmode, self.Ie = [], [], []
+        for dl in lay.depths:
+            m = np.concatenate([dl.j1a, dl.j2b, dl.j3a, dl.j3b]).astype(np.int32)
+            self.maps.append(torch.from_numpy(m).to(device))
+            vs, ve = geom.corner_mode_vectors(dl.axis)
+            self.vmode.append(torch.from_numpy(np.concatenate([vs, ve])).to(device))
+            self.Ie.append(torch.from_numpy(np.ascontiguousarray(dl.I_e, dtype=np.int32)).to(device))
+        self.root_Ie = torch.from_numpy(np.ascontiguousarray(lay.root_I_e, dtype=np.int64)).to(device)
+        blob, idx, pmax = geom.device_constants()
+        self.leaf_consts = torch.from_numpy(blob).to(device)
+        self.leaf_idx = torch.from_numpy(idx).to(device)
+        self.probe_max = pmax
+
+
+def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size=64, *, device=None,
+          keep_level_T=False, check=True):
+    """One bottom-up sweep producing every operator needed for solves (solver.py:250-289).
+
+    Dense on the GPU regardless of `switch_threshold`. With check=False the device status words
+    are not read back (no host sync); call `check_build(state)` later to raise the
+    reference's exceptions.
+    """
+    torch = _torch()
+    _native.require_device()
+    lib = _native.load()
+    device = torch.device(device if device is not None else "cuda")
+    if switch_threshold is None:
+        switch_threshold = math.inf
+    lay = layout_of(tree)
+    q, L = lay.q, lay.L
+    p = q
+    geom = LeafGeometry.get(q, tree.leaf_width, tree.leaf_height)
+    n_leaf = 1 << (2 * L)
+    p2, ni, nb, ng = p * p, (p - 2) ** 2, 4 * (p - 1), 4 * p
+    if p < 3:
+        raise ValueError("p must be >= 3 (need an interior node)")
+
+    # ---- leaf stage (solver.py:184-247) ----
+    fields = _sample(coeffs, lay, geom)
+    reps, gid = _group(fields, n_leaf)
+    ngroups = reps.size
+    dl = _DeviceLayout.get(lay, geom, device)
+    stream = _native.stream_ptr()
+    field_dev = []
+    fptr = (ctypes_vp * 6)()
+    scal = (ctypes_d * 6)()
+    for f, name in enumerate(COEFF_NAMES):
+        v = fields[name]
+        if np.isscalar(v):
+            fptr[f] = None
+            scal[f] = float(v)
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(v[reps])).to(device, non_blocking=False)
+            field_dev.append(t)
+            fptr[f] = t.data_ptr()
+            scal[f] = 0.0
+    Psi = torch.empty((ngroups, ni, nb), dtype=torch.float64, device=device)
+    Tleaf = torch.empty((ngroups, ng, ng), dtype=torch.float64, device=device)
+    cond = torch.empty(ngroups, dtype=torch.float64, device=device)
+    wsb = lib.hps_leaf_workspace_bytes(p, ngroups)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+    _native.check(lib.hps_leaf_stage(p, ngroups, fptr, scal, _native.ptr(dl.leaf_consts), _native.ptr(dl.leaf_idx),
+                                     dl.probe_max, _native.ptr(Psi), _native.ptr(Tleaf), _native.ptr(cond),
+                                     _native.ptr(ws), wsb, stream), "hps_leaf_stage")
+    del ws
+    chunk = max(1, int(2e8 / (8 * p2 * p2)))  # reference chunking, for counter parity (solver.py:226)
+    instrumentation.bump("leaf_dtn", -(-ngroups // chunk))
+
+    # ---- merges, deepest depth first (solver.py:266-285) ----
+    status = torch.full((max(2 * L, 1),), -1, dtype=torch.int32, device=device)
+    S_levels = [None] * (2 * L)
+    level_T = [None] * (2 * L) if keep_level_T else None
+    leaf_gid_dev = torch.from_numpy(gid.astype(np.int32)).to(device)
+    child_T, child_stride, child_idx = Tleaf, ng * ng, leaf_gid_dev
+    for d in range(2 * L - 1, -1, -1):
+        dlay = lay.depths[d]
+        nbatch, n3, ne, m = dlay.n_boxes, dlay.n3, dlay.ne, dlay.m
+        S = torch.empty((nbatch, n3, ne), dtype=torch.float64, device=device)
+        T = torch.empty((nbatch, ne, ne), dtype=torch.float64, device=device)
+        wsb = lib.hps_merge_workspace_bytes(nbatch, n3, ne)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+        _native.check(lib.hps_merge_level(nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride,
+                                          _native.ptr(child_idx), _native.ptr(dl.maps[d]),
+                                          _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T),
+                                          _native.ptr(ws), wsb, ctypes_vp(status.data_ptr() + 4 * d), 0,
+                                          stream), f"hps_merge_level(depth {d})")
+        del ws
+        instrumentation.bump("merge", nbatch)
+        S_levels[d] = S
+        if keep_level_T:
+            level_T[d] = T
+        child_T, child_stride, child_idx = T, ne * ne, None
+    root_dev = child_T[0] if L > 0 else Tleaf[int(gid[0])]
+
+    first_leaf = n_leaf - 1
+    state = SolverState(
+        tree=tree, nodes=nodeset, coeffs=coeffs, q=q, eps=eps, switch_threshold=switch_threshold,
+        hbs_leaf_size=hbs_leaf_size, geometry=geom, psi=_LazyPsi(Psi, gid, first_leaf),
+        S=_LazyS(S_levels, L), root_T=DtnOperator(device_tensor=root_dev),
+        rank_stats={"max_rank": 0, "min_rank": None, "per_level": {}, "n_hbs_matrices": 0},
+        n_leaf_groups=int(ngroups), layout=lay, S_levels=S_levels, Ie_levels=dl.Ie, psi_groups=Psi,
+        T_leaf_groups=Tleaf, leaf_group=gid, root_Ie_dev=dl.root_Ie, device=device, level_T=level_T)
+    state._status = status
+    state._cond = cond
+    state._reps = reps
+    if check:
+        check_build(state)
+    return state
+
+
+def check_build(state):
+    """Read back the device status words and raise the reference's exceptions (one host sync)."""
+    cond = state._cond.cpu().numpy()
+    bad = np.flatnonzero(cond > RESONANCE_COND)
+    if bad.size:  # first group in first-occurrence order (solver.py:235-239)
+        j = int(bad[0])
+        leaf_index = (1 << (2 * state.layout.L)) - 1 + int(state._reps[j])
+        raise LeafResonanceError(box=leaf_index, cond=float(cond[j]))
+    st = state._status.cpu().numpy()
+    for d in range(len(st) - 1, -1, -1):  # reference merges deepest (highest index) first
+        if st[d] >= 0:
+            raise MergeResonanceError(box=(1 << d) - 1 + int(st[d]), detail="non-finite solution operator")
+
+
+# ----------------------------------------------------------------------------------------------
+# Solve (solver.py:292-316)
+# ----------------------------------------------------------------------------------------------
+def _boundary_values(state, f):
+    ids = state.layout.root_I_e
+    if callable(f):
+        pts = state.nodes.points[ids]
+        return np.asarray(f(pts[:, 0], pts[:, 1]), dtype=float)
+    vals = np.asarray(f, dtype=float)
+    if vals.shape[:1] != (ids.size,) or vals.ndim > 2:
+        raise ValueError(f"boundary data must have length {ids.size}")
+    return vals
+
+
+def rhs_ld(b):
+    """Leading dimension of the node-major solution buffer for b right-hand sides."""
+    return 1 if b == 1 else -(-b // 8) * 8
+
+
+def solve_device(state, F, out=None):
+    """Device-resident batched solve. F: torch (|Gamma|, b) or (|Gamma|,) fp64 on the device, in
+    root.I_e order. Returns U (N, ldu) on the device; columns [:b] are the solutions."""
+    torch = _torch()
+    lib = _native.load()
+    lay = state.layout
+    if F.dim() == 1:
+        F = F[:, None]
+    b = F.shape[1]
+    ldu = rhs_ld(b)
+    N = lay.N
+    if out is None:
+        U = torch.zeros((N, ldu), dtype=torch.float64, device=state.device)
+    else:
+        U = out
+        U.zero_()
+    U[:, :b].index_copy_(0, state.root_Ie_dev, F.to(torch.float64))
+    stream = _native.stream_ptr()
+    for d in range(2 * lay.L):
+        dl = lay.depths[d]
+        nrhs = b if b <= 8 else ldu
+        _native.check(lib.hps_solve_level(dl.n_boxes, dl.n3, dl.ne, _native.ptr(state.S_levels[d]),
+                                          _native.ptr(state.Ie_levels[d]), int(lay.depth_off[d]),
+                                          _native.ptr(U), ldu, nrhs, stream), f"hps_solve_level(depth {d})")
+    return U
+
+
+def solve(state, f):
+    """Solution at every tabulation node (solver.py:303-316). `f` is a callable, a vector in
+    root.I_e order, or an (|Gamma|, b) batch (returns (N, b))."""
+    torch = _torch()
+    instrumentation.bump("solve")
+    vals = _boundary_values(state, f)
+    single = vals.ndim == 1
+    F = torch.from_numpy(np.ascontiguousarray(vals if not single else vals[:, None])).to(state.device)
+    U = solve_device(state, F)
+    u = U[:, :F.shape[1]].cpu().numpy()
+    return u[:, 0].copy() if single else u
+
+
+def apply_global_dtn(state, f):
+    """Root DtN applied to boundary data (solver.py:319-327), on the device."""
+    torch = _torch()
+    lib = _native.load()
+    instrumentation.bump("apply_dtn")
+    vals = _boundary_values(state, f)
+    single = vals.ndim == 1
+    V = vals[:, None] if single else vals
+    n, b = V.shape
+    ld = -(-b // 2) * 2
+    F = torch.zeros((n, ld), dtype=torch.float64, device=state.device)
+    F[:, :b] = torch.from_numpy(np.ascontiguousarray(V)).to(state.device)
+    out = torch.empty((n, ld), dtype=torch.float64, device=state.device)
+    Tr = state.root_T.device_tensor
+    if n % 16 == 0:
+        _native.check(lib.hps_dgemm_batched(n, ld, n, 1, 1.0, _native.ptr(Tr), n, 0, _native.ptr(F), ld, 0, None, 0,
+                                            0.0, _native.ptr(out), ld, 0, _native.stream_ptr()), "hps_dgemm_batched")
+        r = out[:, :b].cpu().numpy()
+    else:  # tiny odd q: not a hot path
+        r = state.root_T.dense @ V
+    return r[:, 0].copy() if single else r
+
+
+# ----------------------------------------------------------------------------------------------
+# Post-processing on the host (solver.py:330-432); these read the lazily materialised state
+# ----------------------------------------------------------------------------------------------
+def _owning_leaf(state, x, y):
+    tree = state.tree
+    dom = tree.domain
+    if not dom.contains(x, y):
+        raise ValueError(f"target ({x}, {y}) lies outside the domain")
+    n = 1 << tree.levels
+
+    def cell(t, extent):
+        s = (t / extent) * n
+        i = int(np.floor(s))
+        if i == s and i > 0:
+            i -= 1
+        return min(max(i, 0), n - 1)
+
+    return tree.leaf_at(cell(x - dom.x_lo, dom.width), cell(y - dom.y_lo, dom.height))
+
+
+def _leaf_field(state, u, leaf):
+    geom = state.geometry
+    w_e = geom.L1 @ u[leaf.I_e]
+    w_i = state.psi[leaf.index] @ w_e
+    w = np.zeros(geom.p ** 2)
+    w[geom.J_e] = w_e
+    w[geom.J_i] = w_i
+    return w.reshape(geom.p, geom.p)
+
+
+def post_process(state, u, targets):
+    """Solution at arbitrary points via leaf spectral interpolation (solver.py:359-377)."""
+    geom = state.geometry
+    out = np.empty(len(targets))
+    cache = {}
+    for t, (x, y) in enumerate(targets):
+        leaf = _owning_leaf(state, x, y)
+        W = cache.get(leaf.index)
+        if W is None:
+            W = cache[leaf.index] = _leaf_field(state, u, leaf)
+        rx = interp_matrix(geom.cheb_x, [x - leaf.rect.x_lo])
+        ry = interp_matrix(geom.cheb_y, [y - leaf.rect.y_lo])
+        out[t] = float(rx @ W @ ry.T)
+    return out
+
+
+def boundary_flux_at(state, u, targets):
+    """Coordinate-derivative flux at outer-boundary points (solver.py:380-400)."""
+    geom = state.geometry
+    dom = state.tree.domain
+    out = np.empty(len(targets))
+    for t, (x, y) in enumerate(targets):
+        on_v = x in (dom.x_lo, dom.x_hi)
+        on_h = y in (dom.y_lo, dom.y_hi)
+        if not (on_v or on_h):
+            raise ValueError(f"target ({x}, {y}) is not on the outer boundary")
+        leaf = _owning_leaf(state, x, y)
+        W = _leaf_field(state, u, leaf)
+        dW = geom.Dx @ W if (on_v and not on_h) else W @ geom.Dy.T
+        rx = interp_matrix(geom.cheb_x, [x - leaf.rect.x_lo])
+        ry = interp_matrix(geom.cheb_y, [y - leaf.rect.y_lo])
+        out[t] = float(rx @ dW @ ry.T)
+    return out
+
+
+def memory_report(state):
+    """Deterministic accounting of stored operators, 8 bytes a scalar (solver.py:403-432)."""
+    lay = state.layout
+    per_level = {d: (1 << d) * lay.depths[d].n3 * lay.depths[d].ne for d in range(2 * lay.L)}
+    geom = state.geometry
+    ni, nb = (geom.p - 2) ** 2, 4 * (geom.p - 1)
+    leaf_entries = state.n_leaf_groups * ni * nb + geom.L1.size + geom.L4.size
+    root_entries = state.root_T.n_stored_entries()
+    total = root_entries + leaf_entries + sum(per_level.values())
+    return {
+        "R_mb": total * 8 / 1e6,
+        "total_entries": int(total),
+        "root_dtn_mb": root_entries * 8 / 1e6,
+        "leaf_ops_mb": leaf_entries * 8 / 1e6,
+        "solution_ops_mb_per_level": {int(k): v * 8 / 1e6 for k, v in sorted(per_level.items())},
+        "rank_stats": {"max_rank": 0, "min_rank": None, "n_hbs_matrices": 0, "per_level": {}},
+    }
