@@ -92,96 +92,115 @@ __device__ __forceinline__ double vvt(int r, int c, int q, int nseg, const doubl
   return 0.0;
 }
 
-// In-place Gauss-Jordan inverse with partial pivoting, whole matrix in shared memory (n <= 128).
-// Optional deflation adds sigma V V^T first (sigma = max |diag|).
-__global__ void __launch_bounds__(256) k_inverse_small(double* X, long long lda, long long strideX, int n,
-                                                       int q, const double* __restrict__ vs,
-                                                       const double* __restrict__ ve, int deflate,
-                                                       int* status, int status_base) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ double red[32];
-  __shared__ int s_piv;
-  const int ld = n + 1;
-  double* A = sm;
-  int* perm = reinterpret_cast<int*>(A + n * ld);
+// Gauss-Jordan inverse with partial pivoting for n <= 16*NT (one CTA of 256 threads per matrix).
+// The matrix lives in REGISTERS: thread (ty, tx) of a 16x16 grid owns rows ty + 16a and columns
+// tx + 16b (a, b < NT), a cyclic distribution that stays balanced as pivots are consumed. Pivoting
+// is implicit. Row p_k is eliminated at step k, and no physical swap is made, so the in-place
+// result B satisfies inv(X)[k][p_j] = B[p_k][j]; the write-out applies that permutation. Per step:
+// pivot search over the unused rows (warp 0), then broadcast of the pivot row and column through
+// shared memory, then a register-resident rank-1 update.
+template <int NT>
+__global__ void __launch_bounds__(256) k_gj_inverse(const double* Xin, double* Xout,
+                                                    long long lda, long long strideX, int n,
+                                                    int* status, int status_base) {
+  constexpr int NMAX = 16 * NT;
+  __shared__ double colk[NMAX];
+  __shared__ double rowp[NMAX];
+  __shared__ int pivrow[NMAX];  // pivrow[k] = physical row eliminated at step k
+  __shared__ int rowstep[NMAX]; // inverse permutation
+  __shared__ int used[NMAX];
+  __shared__ int s_p;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int b = blockIdx.x;
-  double* Xb = X + (long long)b * strideX;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int idx = tid; idx < n * n; idx += nt) {
-    int r = idx / n, c = idx - r * n;
-    A[r * ld + c] = Xb[(long long)r * lda + c];
-  }
-  __syncthreads();
-  if (deflate) {
-    double dm = 0.0;
-    for (int i = tid; i < n; i += nt) dm = fmax(dm, fabs(A[i * ld + i]));
-    const double sigma = block_max(dm, red);
-    const int nseg = n / q;
-    for (int idx = tid; idx < n * n; idx += nt) {
-      int r = idx / n, c = idx - r * n;
-      if (abs(r / q - c / q) <= 1) A[r * ld + c] += sigma * vvt(r, c, q, nseg, vs, ve);
-    }
-    __syncthreads();
-  }
-  const int warp = tid >> 5, lane = tid & 31;
-  bool singular = false;
-  for (int k = 0; k < n; ++k) {
-    if (warp == 0) {
-      double best = -1.0;
-      int bi = k;
-      for (int i = k + lane; i < n; i += 32) {
-        double v = fabs(A[i * ld + k]);
-        if (v > best) { best = v; bi = i; }
-      }
+  const double* X = Xin + (long long)b * strideX;
+  double* Y = Xout + (long long)b * strideX;
+  double a[NT][NT];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-      }
-      if (lane == 0) { s_piv = bi; perm[k] = bi; }
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int r = ty + 16 * i, c = tx + 16 * j;
+      a[i][j] = (r < n && c < n) ? X[(long long)r * lda + c] : 0.0;
     }
-    __syncthreads();
-    const int p = s_piv;
-    if (p != k)
-      for (int c = tid; c < n; c += nt) {
-        double t0 = A[k * ld + c];
-        A[k * ld + c] = A[p * ld + c];
-        A[p * ld + c] = t0;
+  for (int i = tid; i < NMAX; i += 256) used[i] = (i < n) ? 0 : 1;
+  __syncthreads();
+  bool singular = false;
+  // k = 16*jb + kk: the column slot jb is a compile-time constant in every unrolled copy, so the
+  // register tile is never indexed dynamically (which would force it into local memory).
+#pragma unroll
+  for (int jb = 0; jb < NT; ++jb) {
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = 16 * jb + kk;
+      if (k >= n) break;
+      if (tx == kk) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) colk[ty + 16 * i] = a[i][jb];
       }
-    __syncthreads();
-    const double pv = A[k * ld + k];
-    singular |= (pv == 0.0);
-    const double inv = 1.0 / pv;
-    for (int c = tid; c < n; c += nt)
-      if (c != k) A[k * ld + c] *= inv;
-    __syncthreads();
-    for (int idx = tid; idx < n * n; idx += nt) {
-      int i = idx / n, c = idx - i * n;
-      if (i != k && c != k) A[i * ld + c] -= A[i * ld + k] * A[k * ld + c];
+      __syncthreads();
+      if (tid < 32) {
+        double best = -1.0;
+        int bi = 0;
+        for (int r = tid; r < n; r += 32) {
+          const double v = used[r] ? -1.0 : fabs(colk[r]);
+          if (v > best) { best = v; bi = r; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        }
+        if (tid == 0) { s_p = bi; pivrow[k] = bi; rowstep[bi] = k; used[bi] = 1; }
+      }
+      __syncthreads();
+      const int p = s_p;
+      const double piv = colk[p];
+      singular |= (piv == 0.0);
+      const double inv = 1.0 / piv;
+      if (ty == (p & 15)) {
+        const int ip = p >> 4;
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            if (i == ip) rowp[tx + 16 * j] = a[i][j] * inv;
+          }
+        }
+      }
+      __syncthreads();
+      double rp[NT], cf[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) rp[j] = rowp[tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < NT; ++i) cf[i] = colk[ty + 16 * i];
+      const bool own_col = (tx == kk);
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const bool prow = (ty + 16 * i) == p;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const bool kcol = own_col && (j == jb);
+          double v = fma(-cf[i], rp[j], a[i][j]);
+          v = kcol ? -cf[i] * inv : v;
+          v = prow ? (kcol ? inv : rp[j]) : v;
+          a[i][j] = v;
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    for (int i = tid; i < n; i += nt) A[i * ld + k] = (i == k) ? inv : -A[i * ld + k] * inv;
-    __syncthreads();
   }
-  for (int k = n - 1; k >= 0; --k) {
-    const int p = perm[k];
-    if (p != k)
-      for (int r = tid; r < n; r += nt) {
-        double t0 = A[r * ld + k];
-        A[r * ld + k] = A[r * ld + p];
-        A[r * ld + p] = t0;
-      }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < n * n; idx += nt) {
-    int r = idx / n, c = idx - r * n;
-    Xb[(long long)r * lda + c] = A[r * ld + c];
-  }
+  // inv(X)[rowstep[r]][pivrow[c]] = B[r][c]
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int r = ty + 16 * i, c = tx + 16 * j;
+      if (r < n && c < n) Y[(long long)rowstep[r] * lda + pivrow[c]] = a[i][j];
+    }
   if (singular && status && tid == 0) atomicMax(status, status_base + b);
 }
 
-// Deflation for n > 128 (before the recursive inverse): one CTA per (segment row, merge).
+// Deflation X += sigma V V^T, sigma = max |diag X|: one CTA per (segment row, merge).
 __global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs, const double* __restrict__ ve) {
   __shared__ double red[32];
   const int b = blockIdx.x, sr = blockIdx.y;
@@ -198,16 +217,21 @@ __global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs
   }
 }
 
-static int inverse_small(double* X, long long lda, long long strideX, int n, int batch, int q, const double* vs,
-                         const double* ve, int deflate, int* status, int status_base, cudaStream_t st) {
-  size_t smem = size_t(n) * (n + 1) * sizeof(double) + size_t(n) * sizeof(int) + 16;
-  static bool attr = false;
-  if (!attr) {
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(k_inverse_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(128 * 129 * 8 + 128 * 4 + 16)));
-    attr = true;
+// In-place batched inverse of n x n blocks (n <= 128), stride lda.
+static int inverse_small(double* X, long long lda, long long strideX, int n, int batch, int* status,
+                         int status_base, cudaStream_t st) {
+  if (n <= 16)
+    k_gj_inverse<1><<<batch, 256, 0, st>>>(X, X, lda, strideX, n, status, status_base);
+  else if (n <= 32)
+    k_gj_inverse<2><<<batch, 256, 0, st>>>(X, X, lda, strideX, n, status, status_base);
+  else if (n <= 64)
+    k_gj_inverse<4><<<batch, 256, 0, st>>>(X, X, lda, strideX, n, status, status_base);
+  else if (n <= 128)
+    k_gj_inverse<8><<<batch, 256, 0, st>>>(X, X, lda, strideX, n, status, status_base);
+  else {
+    set_error("inverse_small: n=%d > 128", n);
+    return HPS_ERR_ARG;
   }
-  k_inverse_small<<<batch, 256, smem, st>>>(X, lda, strideX, n, q, vs, ve, deflate, status, status_base);
   HPS_LAUNCH_CHECK();
   return HPS_OK;
 }
@@ -231,8 +255,7 @@ static int gemm(int M, int N, int K, int batch, double alpha, const double* A, l
 // Base blocks (<= 128) use pivoted Gauss-Jordan in shared memory.
 static int inverse_rec(double* A, long long lda, long long strideA, int n, int batch, double* tmp, int* status,
                        int status_base, cudaStream_t st) {
-  if (n <= 128)
-    return inverse_small(A, lda, strideA, n, batch, 16, nullptr, nullptr, 0, status, status_base, st);
+  if (n <= 128) return inverse_small(A, lda, strideA, n, batch, status, status_base, st);
   const int h = n / 2;
   double* A11 = A;
   double* A12 = A + h;
@@ -298,16 +321,11 @@ extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const d
   HPS_LAUNCH_CHECK();
   const double* vs = vmode;
   const double* ve = vmode + q;
-  const int deflate = n3 > q;
-  if (n3 <= 128) {
-    HPS_TRY(inverse_small(X, n3, (long long)n3 * n3, n3, nbatch, q, vs, ve, deflate, status, status_base, st));
-  } else {
-    if (deflate) {
-      k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vs, ve);
-      HPS_LAUNCH_CHECK();
-    }
-    HPS_TRY(inverse_rec(X, n3, (long long)n3 * n3, n3, nbatch, tmp, status, status_base, st));
+  if (n3 > q) {  // deflate the n3/q - 1 corner null modes
+    k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vs, ve);
+    HPS_LAUNCH_CHECK();
   }
+  HPS_TRY(inverse_rec(X, n3, (long long)n3 * n3, n3, nbatch, tmp, status, status_base, st));
   HPS_TRY(gemm(n3, ne, n3, nbatch, 1.0, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, 0.0, S_out, ne,
                (long long)n3 * ne, st, status));
   // nonfinite flag reports merge index; shift by status_base happens on the host side

@@ -269,12 +269,13 @@ class _DeviceLayout:
 
 
 def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size=64, *, device=None,
-          keep_level_T=False, check=True):
+          keep_level_T=False, check=True, timeline=None):
     """One bottom-up sweep producing every operator needed for solves (solver.py:250-289).
 
     Dense on the GPU regardless of `switch_threshold`. With check=False the device status words
     are not read back (no host sync); call `check_build(state)` later to raise the
-    reference's exceptions.
+    reference's exceptions. `timeline` (a list) receives (stage, start_event, end_event) CUDA
+    event pairs for a per-stage breakdown.
     """
     torch = _torch()
     _native.require_device()
@@ -315,9 +316,11 @@ def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size
     cond = torch.empty(ngroups, dtype=torch.float64, device=device)
     wsb = lib.hps_leaf_workspace_bytes(p, ngroups)
     ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+    mark = _marker(timeline, "leaf")
     _native.check(lib.hps_leaf_stage(p, ngroups, fptr, scal, _native.ptr(dl.leaf_consts), _native.ptr(dl.leaf_idx),
                                      dl.probe_max, _native.ptr(Psi), _native.ptr(Tleaf), _native.ptr(cond),
                                      _native.ptr(ws), wsb, stream), "hps_leaf_stage")
+    mark()
     del ws
     chunk = max(1, int(2e8 / (8 * p2 * p2)))  # reference chunking, for counter parity (solver.py:226)
     instrumentation.bump("leaf_dtn", -(-ngroups // chunk))
@@ -335,11 +338,13 @@ def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size
         T = torch.empty((nbatch, ne, ne), dtype=torch.float64, device=device)
         wsb = lib.hps_merge_workspace_bytes(nbatch, n3, ne)
         ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+        mark = _marker(timeline, f"merge_d{d}")
         _native.check(lib.hps_merge_level(nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride,
                                           _native.ptr(child_idx), _native.ptr(dl.maps[d]),
                                           _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T),
                                           _native.ptr(ws), wsb, ctypes_vp(status.data_ptr() + 4 * d), 0,
                                           stream), f"hps_merge_level(depth {d})")
+        mark()
         del ws
         instrumentation.bump("merge", nbatch)
         S_levels[d] = S
@@ -362,6 +367,21 @@ def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size
     if check:
         check_build(state)
     return state
+
+
+def _marker(timeline, name):
+    """Record a CUDA event now; the returned callable records the end event."""
+    if timeline is None:
+        return lambda: None
+    torch = _torch()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+
+    def end():
+        e1.record()
+        timeline.append((name, e0, e1))
+    return end
 
 
 def check_build(state):
