@@ -1,0 +1,339 @@
+"""Benchmark: HPS build + batched solve throughput (unknowns/s, fp64) on B200.
+
+Contract (driver-facing): `python bench.py --gpus N --steps K --warmup W [--impl reference]` prints
+ONE JSON line on rank 0. A "step" is one pass of the hot path: leaf stage -> every merge level ->
+one batched downward solve of b boundary vectors, on BASELINE.json configs[1] (config 2:
+variable-coefficient diffusion, 64x64 leaves, p = 16, b = 64). Other configs are available via
+--config for exploration; the default line is config 2.
+
+`value`    unknowns / (t_build + t_solve), inputs resident in HBM (coefficient samples of the
+           leaf groups, boundary batch), CUDA events per step, L2 flushed (256 MB write)
+           between steps outside the timed events.
+`e2e`      the same metric through the public API from pinned host memory: prepare() (sampling,
+           grouping, H2D) + build_device + check_build + H2D(F) + solve_device + D2H(u).
+`roofline` the dominant stage, measured live (CUDA events): achieved FP64 TFLOP/s vs the
+           measured cuBLAS DGEMM peak (profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has no
+           fp64 entry).
+`cpu_baseline` / --impl reference: the oracle port (numpy/scipy, LAPACK) of the reference
+           algorithm on this host, on a bounded sample: leaf stage on <=256 groups, one merge per
+           depth, one RHS solve sweep. Each is extrapolated to the full step exactly (every
+           depth is uniform).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+FP64_PEAK_FILE = os.path.join(HERE, "profiles", "fp64_peak_r01.json")
+FP64_PEAK_FALLBACK = 35.47  # TFLOP/s, cuBLAS DGEMM 8192^3 measured on this pool (round 1)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--levels", type=int, default=None, help="override L (exploration only)")
+    ap.add_argument("--batch", type=int, default=None, help="override solve batch b")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def fp64_peak():
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            d = json.load(f)
+        return float(d["fp64_tflops_burst"]), "measured cuBLAS DGEMM 8192^3 (profiles/fp64_peak_r01.json)"
+    except Exception:
+        return FP64_PEAK_FALLBACK, "measured cuBLAS DGEMM 8192^3, round 1 (constant in bench.py)"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=6)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------------------------
+# CPU reference port (oracle) on a bounded sample
+# ----------------------------------------------------------------------------------------------
+def cpu_reference_sample(cfg, L, b, q=16, max_groups=256):
+    """Seconds for one full step (build + b solves) of the oracle port, extrapolated from a
+    bounded sample. Returns (seconds, description)."""
+    from oracle import hps_oracle as O
+    from paper_1307_2665_b200 import problems
+    import scipy.linalg as sla
+
+    co = problems.coefficients(cfg)
+    coeffs = {n: getattr(co, n) for n in O.COEFF_NAMES}
+    tree = O.build_tree((0.0, 1.0, 0.0, 1.0), L, q)
+    geom = O.Geometry(q, tree.leaf_width, tree.leaf_height)
+    fields = O.sample_coefficients(coeffs, tree, geom)
+    reps, gid = O.group_leaves(fields, len(tree.leaves))
+    ng = len(reps)
+    k = min(ng, max_groups)
+    t0 = time.perf_counter()
+    Psi, Tg, cond = O.leaf_operators(geom, fields, reps[:k])
+    t_leaf = (time.perf_counter() - t0) * ng / k
+    # one merge per depth on congruent children (flop- and shape-identical to every merge there)
+    T_child = Tg[0]
+    t_merge = 0.0
+    S_depth = {}
+    for d in range(2 * L - 1, -1, -1):
+        box = (1 << d) - 1
+        a, c = tree.child_a[box], tree.child_b[box]
+        j1a, j2b, j3a, j3b = O.split_indices(tree.I_e[a], tree.I_e[c], tree.I_i[box])
+        t0 = time.perf_counter()
+        X = T_child[np.ix_(j3a, j3a)] - T_child[np.ix_(j3b, j3b)]
+        R = np.concatenate([-T_child[np.ix_(j3a, j1a)], T_child[np.ix_(j3b, j2b)]], axis=1)
+        lu = sla.lu_factor(X, check_finite=False)
+        S = sla.lu_solve(lu, R, check_finite=False)
+        n1 = j1a.size
+        T = np.zeros((n1 + j2b.size,) * 2)
+        T[:n1, :n1] = T_child[np.ix_(j1a, j1a)]
+        T[n1:, n1:] = T_child[np.ix_(j2b, j2b)]
+        T += np.concatenate([T_child[np.ix_(j1a, j3a)], T_child[np.ix_(j2b, j3b)]]) @ S
+        t_merge += (time.perf_counter() - t0) * (1 << d)
+        S_depth[d] = S
+        T_child = T
+    # one RHS sweep over every box (the reference solve is single-RHS, solver.py:298-299)
+    u = np.zeros(tree.points.shape[0])
+    u[tree.I_e[0]] = 1.0
+    t0 = time.perf_counter()
+    for bx in range(tree.n_boxes):
+        if tree.child_a[bx] < 0:
+            continue
+        d = int(np.floor(np.log2(bx + 1)))
+        u[tree.I_i[bx]] = S_depth[d] @ u[tree.I_e[bx]]
+    t_solve = (time.perf_counter() - t0) * b
+    desc = (f"oracle port (numpy/scipy LAPACK, {os.environ.get('OMP_NUM_THREADS', 'all')} BLAS threads): "
+            f"leaf stage on {k}/{ng} groups, 1 merge per depth x 2^d, 1-RHS sweep x {b}; "
+            f"extrapolated t_leaf={t_leaf:.2f}s t_merge={t_merge:.2f}s t_solve={t_solve:.2f}s")
+    return t_leaf + t_merge + t_solve, desc
+
+
+# ----------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    from paper_1307_2665_b200 import problems
+
+    cfg = args.config
+    c = problems.CONFIGS[cfg]
+    L = args.levels if args.levels is not None else c.L
+    b = args.batch if args.batch is not None else c.batch
+    q = 16
+    unknowns = (4 ** L) * q * q
+    workload = f"cfg{cfg}_{c.name}_L{L}_p{q}_b{b}"
+    metric = "HPS build and solve unknowns/s (fp64)"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cores = os.cpu_count()
+        os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+        times = []
+        desc = ""
+        for it in range(args.warmup + args.steps):
+            t, desc = cpu_reference_sample(cfg, L, b, q)
+            if it >= args.warmup:
+                times.append(t)
+        t = float(np.mean(times))
+        v = unknowns / t
+        print(json.dumps({
+            "impl": "reference", "metric": metric, "value": v, "unit": "unknowns/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "unknowns": unknowns, "batch": b},
+            "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": cores, "kind": "port", "sample": desc},
+            "e2e": {"value": v, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    from oracle import hps_oracle as O
+    import paper_1307_2665_b200 as P
+    from paper_1307_2665_b200 import _native, solver
+
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda")
+    lib = _native.load()
+    tree, nodes = P.build_tree(P.Rectangle(0.0, 1.0, 0.0, 1.0), L, q)
+    co = c.coefficients()
+    F_host = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=0, batch=b)
+    if F_host.ndim == 1:
+        F_host = F_host[:, None]
+    F_dev = torch.from_numpy(np.ascontiguousarray(F_host)).to(dev)
+    inp = solver.prepare(tree, nodes, co, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    # ---- device-resident timed steps ----
+    def step(timeline=None):
+        st = solver.build_device(inp, timeline=timeline)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        U = solver.solve_device(st, F_dev)
+        return st, U, e
+
+    for _ in range(args.warmup):
+        st, U, _ = step()
+    torch.cuda.synchronize()
+    solver.check_build(st)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    launches0 = lib.hps_launch_count()
+    t_build, t_solve, stages = [], [], {}
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        tl = []
+        e0 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st, U, e1 = step(tl)
+        e2.record()
+        e2.synchronize()
+        t_build.append(e0.elapsed_time(e1) / 1e3)
+        t_solve.append(e1.elapsed_time(e2) / 1e3)
+        for name, a, z in tl:
+            stages.setdefault(name, []).append(a.elapsed_time(z) / 1e3)
+    launches = lib.hps_launch_count() - launches0
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    tb, ts = float(np.mean(t_build)), float(np.mean(t_solve))
+    t_step = tb + ts
+    if world > 1:
+        tt = torch.tensor([t_step], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = unknowns / t_step * (world if world > 1 else 1)
+
+    # ---- roofline of the dominant stage ----
+    peak, peak_src = fp64_peak()
+    stage_flops = {"leaf": inp.ngroups * O.leaf_flops(q)}
+    for d in range(2 * L):
+        n3, ne = O.depth_sizes(L, q, d)
+        stage_flops[f"merge_d{d}"] = (2 ** d) * (2 / 3 * n3 ** 3 + 2 * n3 * n3 * ne + 2 * n3 * ne * ne)
+    stage_ms = {k: float(np.mean(v)) * 1e3 for k, v in stages.items()}
+    dom = max(stage_ms, key=stage_ms.get)
+    ach = stage_flops[dom] / (stage_ms[dom] / 1e3) / 1e12
+    kernels = {"leaf": "hps::k_leaf"}.get(dom, "hps_merge_level (gather, deflate, k_gj_inverse, dgemm_dmma)")
+    build_flops = sum(stage_flops.values())
+    solve_flops = O.solve_flops(L, q, b)
+    S_bytes = sum((2 ** d) * O.depth_sizes(L, q, d)[0] * O.depth_sizes(L, q, d)[1] * 8 for d in range(2 * L))
+    hpeak, hsrc = hbm_peak()
+    roofline = {
+        "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+        "kernel": dom, "kernels": kernels, "peak_source": peak_src,
+        "stage_ms": stage_ms, "build_tflops": build_flops / tb / 1e12, "build_frac": build_flops / tb / 1e12 / peak,
+        "solve": {"tflops": solve_flops / ts / 1e12, "frac_fp64": solve_flops / ts / 1e12 / peak,
+                  "gbs_S_stream": S_bytes / ts / 1e9, "frac_hbm": S_bytes / ts / 1e9 / hpeak, "hbm_peak_source": hsrc},
+    }
+
+    # ---- end-to-end through the public API, pinned host memory ----
+    pin_F = torch.from_numpy(np.ascontiguousarray(F_host)).pin_memory()
+    U_host = torch.empty((nodes.N, solver.rhs_ld(b)), dtype=torch.float64).pin_memory()
+    e2e_t = []
+    h2d = d2h = 0
+    for it in range(max(2, args.steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        inp2 = solver.prepare(tree, nodes, co, device=dev, pinned=True)
+        st2 = solver.build_device(inp2)
+        Fd = pin_F.to(dev, non_blocking=True)
+        U2 = solver.solve_device(st2, Fd)
+        U_host.copy_(U2, non_blocking=True)
+        solver.check_build(st2)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+        h2d = inp2.h2d_bytes() + pin_F.numel() * 8
+        d2h = U_host.numel() * 8 + 4 * 2 * L + 8 * inp2.ngroups
+    e2e = {"value": unknowns / float(np.median(e2e_t)), "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "seconds_per_step": float(np.median(e2e_t)),
+           "includes": "coefficient sampling + grouping (host), H2D from pinned memory, build, status check, "
+                       "batched solve, D2H of u (N x ldu)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+        t_ref, desc = cpu_reference_sample(cfg, L, b, q)
+        cpu = {"value": unknowns / t_ref, "unit": "unknowns/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": desc}
+    if rank == 0:
+        print(json.dumps({
+            "metric": metric, "value": value, "unit": "unknowns/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "unknowns": unknowns, "batch": b, "leaf_groups": inp.ngroups,
+                       "l2": "flushed (256 MB write) between timed steps, outside the step events",
+                       "build_ms": tb * 1e3, "solve_ms": ts * 1e3,
+                       "build_unknowns_per_s": unknowns / tb, "solve_unknowns_per_s": unknowns * b / ts},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "gpu_launches_per_step": int(launches // args.steps), "clocks": clk}))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

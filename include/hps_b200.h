@@ -34,6 +34,8 @@ extern "C" {
 const char* hps_last_error(void);
 int hps_version(void);
 int hps_device_check(int* major, int* minor, int* sms);
+/* Kernels launched by this library so far in this process (benchmark accounting). */
+long long hps_launch_count(void);
 
 /* Leaf stage for `ngroups` distinct coefficient groups (leaves with bitwise-equal samples share a
  * group, solver.py:208-222).

@@ -22,7 +22,7 @@ HPS_ERR_NCCL = 4
 HPS_ERR_ARG = 5
 
 #: every symbol include/hps_b200.h declares (tests check the .so exports all of them)
-EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_leaf_workspace_bytes",
+EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_launch_count", "hps_leaf_workspace_bytes",
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
            "hps_dgemm_batched")
 
@@ -46,6 +46,7 @@ def load():
     lib = ctypes.CDLL(LIB_PATH)
     lib.hps_last_error.restype = ctypes.c_char_p
     lib.hps_version.restype = c_int
+    lib.hps_launch_count.restype = c_ll
     lib.hps_device_check.argtypes = [ctypes.POINTER(c_int)] * 3
     lib.hps_device_check.restype = c_int
     lib.hps_leaf_workspace_bytes.argtypes = [c_int, c_int]

@@ -1,5 +1,6 @@
 // C-ABI plumbing: error string, version, capability probe. Entry points live beside their kernels
 // (leaf.cu, merge.cu, solve.cu, gemm.cu); all are declared in include/hps_b200.h.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -14,7 +15,12 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace hps
+
+// Number of kernels this library has launched in this process (bench.py's gpu_launches).
+extern "C" long long hps_launch_count(void) { return hps::g_launches.load(); }
 
 extern "C" const char* hps_last_error(void) { return hps::g_err; }
 

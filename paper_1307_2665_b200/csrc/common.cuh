@@ -14,6 +14,7 @@
 namespace hps {
 
 void set_error(const char* fmt, ...);
+void count_launch();  // every kernel launch of this library bumps a process-wide counter
 
 #define HPS_CUDA_CHECK(expr)                                                              \
   do {                                                                                    \
@@ -24,7 +25,11 @@ void set_error(const char* fmt, ...);
     }                                                                                     \
   } while (0)
 
-#define HPS_LAUNCH_CHECK() HPS_CUDA_CHECK(cudaGetLastError())
+#define HPS_LAUNCH_CHECK()            \
+  do {                                \
+    ::hps::count_launch();            \
+    HPS_CUDA_CHECK(cudaGetLastError()); \
+  } while (0)
 
 // DMMA: D(8x8) += A(8x4, row) * B(4x8, col), one f64 each for A/B per lane, two for C.
 // Lane layout (g = lane>>2, t = lane&3): a = A[g][t], b = B[t][g], c = C[g][2t..2t+1].

@@ -34,6 +34,9 @@ __all__ = [
     "SolutionOperator",
     "SolverState",
     "build",
+    "prepare",
+    "build_device",
+    "check_build",
     "solve",
     "solve_device",
     "apply_global_dtn",
@@ -268,49 +271,87 @@ class _DeviceLayout:
         self.probe_max = pmax
 
 
-def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size=64, *, device=None,
-          keep_level_T=False, check=True, timeline=None):
-    """One bottom-up sweep producing every operator needed for solves (solver.py:250-289).
+@dataclass
+class BuildInputs:
+    """Host-prepared, device-resident inputs of one build (coefficient samples of the group
+    representatives, leaf->group map, layout tables). `build_device` consumes it with no host
+    work besides kernel enqueues."""
 
-    Dense on the GPU regardless of `switch_threshold`. With check=False the device status words
-    are not read back (no host sync); call `check_build(state)` later to raise the
-    reference's exceptions. `timeline` (a list) receives (stage, start_event, end_event) CUDA
-    event pairs for a per-stage breakdown.
-    """
+    tree: object
+    nodeset: object
+    coeffs: object
+    layout: object
+    geom: LeafGeometry
+    dev_layout: object
+    reps: np.ndarray
+    gid: np.ndarray
+    gid_dev: object
+    fields_dev: list
+    scalars: tuple
+    device: object
+
+    @property
+    def ngroups(self):
+        return int(self.reps.size)
+
+    def h2d_bytes(self):
+        return int(sum(t.numel() * t.element_size() for t in self.fields_dev if t is not None)
+                   + self.gid_dev.numel() * 4)
+
+
+def prepare(tree, nodeset, coeffs, *, device=None, pinned=False):
+    """Sample the coefficients on every leaf grid, group bitwise-equal leaves and upload the group
+    representatives' samples (solver.py:184-222). Host work + H2D only."""
     torch = _torch()
     _native.require_device()
-    lib = _native.load()
     device = torch.device(device if device is not None else "cuda")
-    if switch_threshold is None:
-        switch_threshold = math.inf
     lay = layout_of(tree)
-    q, L = lay.q, lay.L
-    p = q
-    geom = LeafGeometry.get(q, tree.leaf_width, tree.leaf_height)
-    n_leaf = 1 << (2 * L)
-    p2, ni, nb, ng = p * p, (p - 2) ** 2, 4 * (p - 1), 4 * p
-    if p < 3:
+    q = lay.q
+    if q < 3:
         raise ValueError("p must be >= 3 (need an interior node)")
-
-    # ---- leaf stage (solver.py:184-247) ----
+    geom = LeafGeometry.get(q, tree.leaf_width, tree.leaf_height)
     fields = _sample(coeffs, lay, geom)
-    reps, gid = _group(fields, n_leaf)
-    ngroups = reps.size
+    reps, gid = _group(fields, 1 << (2 * lay.L))
     dl = _DeviceLayout.get(lay, geom, device)
-    stream = _native.stream_ptr()
-    field_dev = []
-    fptr = (ctypes_vp * 6)()
-    scal = (ctypes_d * 6)()
-    for f, name in enumerate(COEFF_NAMES):
+    fields_dev, scalars = [], []
+    for name in COEFF_NAMES:
         v = fields[name]
         if np.isscalar(v):
-            fptr[f] = None
-            scal[f] = float(v)
+            fields_dev.append(None)
+            scalars.append(float(v))
         else:
-            t = torch.from_numpy(np.ascontiguousarray(v[reps])).to(device, non_blocking=False)
-            field_dev.append(t)
-            fptr[f] = t.data_ptr()
-            scal[f] = 0.0
+            h = torch.from_numpy(np.ascontiguousarray(v[reps]))
+            if pinned:
+                h = h.pin_memory()
+            fields_dev.append(h.to(device, non_blocking=pinned))
+            scalars.append(0.0)
+    h = torch.from_numpy(gid.astype(np.int32))
+    if pinned:
+        h = h.pin_memory()
+    gid_dev = h.to(device, non_blocking=pinned)
+    return BuildInputs(tree, nodeset, coeffs, lay, geom, dl, reps, gid, gid_dev, fields_dev, tuple(scalars), device)
+
+
+def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_threshold=math.inf,
+                 hbs_leaf_size=64):
+    """Enqueue the leaf stage and every merge level on the current stream (no host sync)."""
+    torch = _torch()
+    lib = _native.load()
+    lay, geom, dl, device = inp.layout, inp.geom, inp.dev_layout, inp.device
+    q, L = lay.q, lay.L
+    p = q
+    n_leaf = 1 << (2 * L)
+    p2, ni, nb, ng = p * p, (p - 2) ** 2, 4 * (p - 1), 4 * p
+    ngroups = inp.ngroups
+    stream = _native.stream_ptr()
+
+    # ---- leaf stage (solver.py:184-247) ----
+    fptr = (ctypes_vp * 6)()
+    scal = (ctypes_d * 6)()
+    for f in range(6):
+        t = inp.fields_dev[f]
+        fptr[f] = None if t is None else _native.ptr(t).value
+        scal[f] = inp.scalars[f]
     Psi = torch.empty((ngroups, ni, nb), dtype=torch.float64, device=device)
     Tleaf = torch.empty((ngroups, ng, ng), dtype=torch.float64, device=device)
     cond = torch.empty(ngroups, dtype=torch.float64, device=device)
@@ -329,8 +370,7 @@ def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size
     status = torch.full((max(2 * L, 1),), -1, dtype=torch.int32, device=device)
     S_levels = [None] * (2 * L)
     level_T = [None] * (2 * L) if keep_level_T else None
-    leaf_gid_dev = torch.from_numpy(gid.astype(np.int32)).to(device)
-    child_T, child_stride, child_idx = Tleaf, ng * ng, leaf_gid_dev
+    child_T, child_stride, child_idx = Tleaf, ng * ng, inp.gid_dev
     for d in range(2 * L - 1, -1, -1):
         dlay = lay.depths[d]
         nbatch, n3, ne, m = dlay.n_boxes, dlay.n3, dlay.ne, dlay.m
@@ -351,19 +391,35 @@ def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size
         if keep_level_T:
             level_T[d] = T
         child_T, child_stride, child_idx = T, ne * ne, None
-    root_dev = child_T[0] if L > 0 else Tleaf[int(gid[0])]
+    root_dev = child_T[0] if L > 0 else Tleaf[int(inp.gid[0])]
 
-    first_leaf = n_leaf - 1
     state = SolverState(
-        tree=tree, nodes=nodeset, coeffs=coeffs, q=q, eps=eps, switch_threshold=switch_threshold,
-        hbs_leaf_size=hbs_leaf_size, geometry=geom, psi=_LazyPsi(Psi, gid, first_leaf),
+        tree=inp.tree, nodes=inp.nodeset, coeffs=inp.coeffs, q=q, eps=eps, switch_threshold=switch_threshold,
+        hbs_leaf_size=hbs_leaf_size, geometry=geom, psi=_LazyPsi(Psi, inp.gid, n_leaf - 1),
         S=_LazyS(S_levels, L), root_T=DtnOperator(device_tensor=root_dev),
         rank_stats={"max_rank": 0, "min_rank": None, "per_level": {}, "n_hbs_matrices": 0},
-        n_leaf_groups=int(ngroups), layout=lay, S_levels=S_levels, Ie_levels=dl.Ie, psi_groups=Psi,
-        T_leaf_groups=Tleaf, leaf_group=gid, root_Ie_dev=dl.root_Ie, device=device, level_T=level_T)
+        n_leaf_groups=ngroups, layout=lay, S_levels=S_levels, Ie_levels=dl.Ie, psi_groups=Psi,
+        T_leaf_groups=Tleaf, leaf_group=inp.gid, root_Ie_dev=dl.root_Ie, device=device, level_T=level_T)
     state._status = status
     state._cond = cond
-    state._reps = reps
+    state._reps = inp.reps
+    return state
+
+
+def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size=64, *, device=None,
+          keep_level_T=False, check=True, timeline=None):
+    """One bottom-up sweep producing every operator needed for solves (solver.py:250-289).
+
+    Dense on the GPU regardless of `switch_threshold` (the reference's HBS branch is out of
+    scope). With check=False the device status words are not read back (no host sync); call
+    `check_build(state)` later to raise the reference's exceptions. `timeline` (a list) receives
+    (stage, start_event, end_event) CUDA event pairs for a per-stage breakdown.
+    """
+    if switch_threshold is None:
+        switch_threshold = math.inf
+    inp = prepare(tree, nodeset, coeffs, device=device)
+    state = build_device(inp, keep_level_T=keep_level_T, timeline=timeline, eps=eps,
+                         switch_threshold=switch_threshold, hbs_leaf_size=hbs_leaf_size)
     if check:
         check_build(state)
     return state
