@@ -303,15 +303,15 @@ def prepare(tree, nodeset, coeffs, *, device=None, pinned=False):
     """Sample the coefficients on every leaf grid, group bitwise-equal leaves and upload the group
     representatives' samples (solver.py:184-222). Host work + H2D only."""
     torch = _torch()
-    _native.require_device()
-    device = torch.device(device if device is not None else "cuda")
     lay = layout_of(tree)
     q = lay.q
     if q < 3:
         raise ValueError("p must be >= 3 (need an interior node)")
     geom = LeafGeometry.get(q, tree.leaf_width, tree.leaf_height)
-    fields = _sample(coeffs, lay, geom)
+    fields = _sample(coeffs, lay, geom)  # ValueError on non-finite samples, as the reference
     reps, gid = _group(fields, 1 << (2 * lay.L))
+    _native.require_device()
+    device = torch.device(device if device is not None else "cuda")
     dl = _DeviceLayout.get(lay, geom, device)
     fields_dev, scalars = [], []
     for name in COEFF_NAMES:

@@ -1,0 +1,70 @@
+"""Unit tests of the CUDA kernels through the C ABI (GPU only)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_1307_2665_b200 import _native
+
+from _util import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("M,N,K,B,alpha,beta", [(64, 64, 16, 1, 1.0, 0.0), (96, 96, 16, 3, -1.0, 1.0),
+                                                (256, 512, 128, 2, 0.5, 2.0), (1000, 130, 64, 1, 1.0, 0.0),
+                                                (128, 128, 32, 300, 1.0, 1.0), (16, 8, 16, 7, 2.0, 0.0),
+                                                (1024, 1024, 512, 1, 1.0, -1.0)])
+def test_dgemm(M, N, K, B, alpha, beta):
+    lib = _native.load()
+    rng = np.random.default_rng(M + N + K)
+    A, Bm, C = rng.standard_normal((B, M, K)), rng.standard_normal((B, K, N)), rng.standard_normal((B, M, N))
+    tA, tB, tC = cuda(A), cuda(Bm), cuda(C)
+    _native.check(lib.hps_dgemm_batched(M, N, K, B, alpha, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N,
+                                        None, 0, beta, _native.ptr(tC), N, M * N, _native.stream_ptr()), "gemm")
+    assert rel(tC.cpu().numpy(), alpha * A @ Bm + beta * C) < 1e-14
+
+
+def test_dgemm_row_gather():
+    lib = _native.load()
+    rng = np.random.default_rng(1)
+    M, N, K, B = 48, 64, 32, 3
+    U = rng.standard_normal((500, N))
+    idx = np.stack([rng.integers(0, 500, K) for _ in range(B)]).astype(np.int32)
+    A = rng.standard_normal((B, M, K))
+    tA, tU, ti = cuda(A), cuda(U), cuda(idx)
+    tC = torch.zeros((B, M, N), dtype=torch.float64, device="cuda")
+    _native.check(lib.hps_dgemm_batched(M, N, K, B, 1.0, _native.ptr(tA), K, M * K, _native.ptr(tU), N, 0,
+                                        _native.ptr(ti), K, 0.0, _native.ptr(tC), N, M * N, _native.stream_ptr()), "g")
+    want = np.stack([A[b] @ U[idx[b]] for b in range(B)])
+    assert rel(tC.cpu().numpy(), want) < 1e-14
+
+
+def test_dgemm_rejects_bad_shapes():
+    lib = _native.load()
+    t = torch.zeros(64, dtype=torch.float64, device="cuda")
+    st = lib.hps_dgemm_batched(4, 4, 7, 1, 1.0, _native.ptr(t), 7, 0, _native.ptr(t), 4, 0, None, 0, 0.0,
+                               _native.ptr(t), 4, 0, _native.stream_ptr())
+    assert st == _native.HPS_ERR_ARG
+
+
+@pytest.mark.parametrize("nb,n3,ne,ldu,nrhs", [(1, 32, 128, 1, 1), (2, 16, 96, 1, 1), (2, 16, 96, 8, 3),
+                                               (4, 32, 128, 16, 16), (3, 64, 256, 64, 64)])
+def test_solve_level(nb, n3, ne, ldu, nrhs):
+    lib = _native.load()
+    rng = np.random.default_rng(nb * n3)
+    N = 300 + nb * n3
+    S = rng.standard_normal((nb, n3, ne))
+    Ie = np.stack([rng.permutation(300)[:ne] for _ in range(nb)]).astype(np.int32)
+    u = np.zeros((N, ldu))
+    u[:300] = rng.standard_normal((300, ldu))
+    tS, tI, tu = cuda(S), cuda(Ie), cuda(u)
+    _native.check(lib.hps_solve_level(nb, n3, ne, _native.ptr(tS), _native.ptr(tI), 300, _native.ptr(tu), ldu,
+                                      nrhs, _native.stream_ptr()), "solve")
+    ref = u.copy()
+    for b in range(nb):
+        ref[300 + b * n3:300 + (b + 1) * n3, :nrhs] = S[b] @ u[Ie[b], :nrhs]
+    assert rel(tu.cpu().numpy()[:, :nrhs], ref[:, :nrhs]) < 1e-14

@@ -1,0 +1,193 @@
+"""Parity of the CUDA path (through the C ABI) against the reference's golden vectors and the
+oracle, on null-mode-invariant quantities. Run on a B200: pytest -m gpu.
+
+Gates (relative, max|diff| / max|ref|): leaf T / Psi <= 1e-12, merged/root T <= 1e-10
+(1e-8 for the Helmholtz configs 3, 4), per-leaf Chebyshev boundary values L1 u <= 1e-10
+(1e-8 Helmholtz). Tree/index layout is bit-exact (tests/test_layout.py)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1307_2665_b200 as P
+from oracle import hps_oracle as O
+from paper_1307_2665_b200 import instrumentation, problems, solver
+
+from _util import coeff_dict, golden, rel
+
+pytestmark = pytest.mark.gpu
+T_TOL = {1: 1e-10, 2: 1e-10, 3: 1e-8, 4: 1e-8, 5: 1e-10}
+U_TOL = T_TOL
+
+
+def gpu_build(cfg, L, **kw):
+    tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), L, 16)
+    st = solver.build(tree, nodes, problems.coefficients(cfg), switch_threshold=None, **kw)
+    return tree, nodes, st
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_against_reference_golden_L2(cfg):
+    g = golden(f"cfg{cfg}_L2.npz")
+    tree, nodes, st = gpu_build(cfg, 2, keep_level_T=True)
+    k = g["leaf_T"].shape[0]
+    assert rel(st.T_leaf_groups.cpu().numpy()[:k], g["leaf_T"]) < 1e-12
+    assert rel(st.psi_groups.cpu().numpy()[:g["psi"].shape[0]], g["psi"]) < 1e-12
+    assert rel(st._cond.cpu().numpy(), g["cond"]) < 1e-12
+    assert np.array_equal(st.leaf_group, g["leaf_group"])
+    lt = st.level_T[3].cpu().numpy()  # leaf-pair depth 2L-1 = 3: boxes 7, 8 are slots 0, 1
+    for slot, box in ((0, 7), (1, 8)):
+        assert rel(lt[slot], g[f"T_box{box}"]) < T_TOL[cfg]
+        assert rel(st.S[box].dense, g[f"S_box{box}"]) < T_TOL[cfg]  # X nonsingular at this depth
+    assert rel(st.root_T.dense, g["root_T"]) < T_TOL[cfg]
+    u = solver.solve(st, g["F"])
+    ot = O.build_tree((0, 1, 0, 1), 2, 16)
+    L1u = np.stack([st.geometry.L1 @ u[ot.I_e[b]] for b in ot.leaves])
+    assert rel(L1u, g["L1u"]) < U_TOL[cfg]
+
+
+@pytest.mark.parametrize("cfg,L", [(1, 3), (2, 3), (2, 4), (3, 3), (4, 4), (5, 4), (1, 5)])
+def test_every_operator_against_oracle(cfg, L):
+    tree, nodes, st = gpu_build(cfg, L, keep_level_T=True)
+    ot = O.build_tree((0, 1, 0, 1), L, 16)
+    ost = O.build(ot, coeff_dict(problems.coefficients(cfg)), keep_T=True)
+    assert rel(st.T_leaf_groups.cpu().numpy(), ost.T_groups) < 1e-12
+    assert rel(st.psi_groups.cpu().numpy(), ost.psi_groups) < 1e-12
+    assert rel(st._cond.cpu().numpy(), ost.cond) < 1e-12
+    worst = 0.0
+    for d in range(2 * L):
+        Td = st.level_T[d].cpu().numpy()
+        for k in range(Td.shape[0]):
+            worst = max(worst, rel(Td[k], ost.T[(1 << d) - 1 + k]))
+    assert worst < T_TOL[cfg], worst
+    F = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=7, batch=3)
+    u = solver.solve(st, F)
+    uo = O.solve(ost, F)
+    assert rel(O.leaf_cheb_boundary(ost, u), O.leaf_cheb_boundary(ost, uo)) < U_TOL[cfg]
+    assert rel(O.leaf_flux(ost, u), O.leaf_flux(ost, uo)) < U_TOL[cfg]
+    assert rel(O.leaf_cheb_field(ost, u), O.leaf_cheb_field(ost, uo)) < U_TOL[cfg]
+
+
+@pytest.mark.parametrize("cfg,L,tol", [(1, 3, 1e-11), (1, 6, 1e-9), (3, 4, 1e-7)])
+def test_exact_solution(cfg, L, tol):
+    """cfg 1: exp(x1) sin(x2); cfg 3: plane wave. Checked on the invariant L1 u."""
+    tree, nodes, st = gpu_build(cfg, L)
+    F = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=4, batch=1)
+    u = solver.solve(st, F)
+    ex = problems.exact_solution(cfg, nodes.points[:, 0], nodes.points[:, 1], seed=4, batch=1)
+    lay = st.layout
+    L1 = st.geometry.L1
+    got = np.einsum("rc,lc->lr", L1, u[lay.leaf_I_e])
+    want = np.einsum("rc,lc->lr", L1, ex[lay.leaf_I_e])
+    assert rel(got, want) < tol
+
+
+def test_full_size_cfg2_against_oracle():
+    """BASELINE config 2 at its full size (L=6, 4096 leaf groups): root DtN + invariants."""
+    cfg, L = 2, 6
+    tree, nodes, st = gpu_build(cfg, L)
+    ot = O.build_tree((0, 1, 0, 1), L, 16)
+    ost = O.build(ot, coeff_dict(problems.coefficients(cfg)))
+    assert rel(st.root_T.dense, ost.root_T) < 1e-10
+    F = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=0, batch=4)
+    u = solver.solve(st, F)
+    assert rel(O.leaf_cheb_boundary(ost, u), O.leaf_cheb_boundary(ost, O.solve(ost, F))) < 1e-10
+
+
+@pytest.mark.parametrize("cfg,L", [(1, 6), (2, 6), (5, 7)])
+def test_full_size_properties(cfg, L):
+    """Size-independent properties at BASELINE sizes: constants are in the DtN null space
+     for operators with no zeroth-order term, and the solve is linear."""
+    tree, nodes, st = gpu_build(cfg, L)
+    T = st.root_T.device_tensor
+    one = torch.ones(T.shape[0], dtype=torch.float64, device=T.device)
+    assert float((T @ one).abs().max() / T.abs().max()) < 1e-10
+    F = problems.boundary_data(2, nodes.points[tree.root.I_e], seed=9, batch=2)
+    u = solver.solve(st, F)
+    uc = solver.solve(st, 2.0 * F[:, 0] - 3.0 * F[:, 1])
+    L1 = st.geometry.L1
+    Ie = st.layout.leaf_I_e
+    lin = np.einsum("rc,lc->lr", L1, 2.0 * u[Ie, 0] - 3.0 * u[Ie, 1])
+    assert rel(np.einsum("rc,lc->lr", L1, uc[Ie]), lin) < 1e-11
+
+
+def test_laplace_dtn_on_linear_data():
+    """Leaf/root T on u = x1: flux 1 on vertical edges, 0 on horizontal."""
+    tree, nodes, st = gpu_build(1, 3)
+    ids = tree.root.I_e
+    x = nodes.points[ids, 0]
+    v = solver.apply_global_dtn(st, x)
+    vert = nodes.on_vertical[ids]
+    assert np.abs(v[vert] - 1.0).max() < 1e-9 and np.abs(v[~vert]).max() < 1e-9
+    Tl = st.T_leaf_groups[0].cpu().numpy()
+    leaf = tree.boxes[tree.n_boxes - 1]
+    xl = nodes.points[leaf.I_e, 0]
+    fl = Tl @ xl
+    assert np.abs(fl[16:32] - 1).max() < 1e-10 and np.abs(fl[:16]).max() < 1e-10
+    assert np.abs(Tl @ np.ones(64)).max() < 1e-9 * np.abs(Tl).max()
+
+
+def test_repeat_solve_and_build_are_bitwise_deterministic():
+    tree, nodes, st = gpu_build(2, 4)
+    F = problems.boundary_data(2, nodes.points[tree.root.I_e], seed=1, batch=16)
+    u1 = solver.solve(st, F)
+    u2 = solver.solve(st, F)
+    assert np.array_equal(u1, u2)
+    _, _, st2 = gpu_build(2, 4)
+    assert torch.equal(st.root_T.device_tensor, st2.root_T.device_tensor)
+    assert all(torch.equal(a, b) for a, b in zip(st.S_levels, st2.S_levels))
+
+
+def test_batched_solve_matches_single_rhs():
+    tree, nodes, st = gpu_build(2, 3)
+    F = problems.boundary_data(2, nodes.points[tree.root.I_e], seed=2, batch=20)
+    U = solver.solve(st, F)  # GEMM path (b > 8)
+    U4 = solver.solve(st, F[:, :4])  # warp-per-row path
+    for j in (0, 7, 19):
+        uj = solver.solve(st, F[:, j])
+        assert rel(U[:, j], uj) < 1e-13
+    assert rel(U4, U[:, :4]) < 1e-13
+
+
+def test_counters_and_stage_separation():
+    instrumentation.counts.clear()
+    tree, nodes, st = gpu_build(2, 2)
+    snap = instrumentation.snapshot()
+    assert snap["merge"] == 15 and snap["leaf_dtn"] == 1
+    solver.solve(st, lambda x, y: x * y)
+    after = instrumentation.snapshot()
+    assert after["solve"] == 1 and after["merge"] == 15 and after["leaf_dtn"] == 1
+    solver.apply_global_dtn(st, lambda x, y: x)
+    assert instrumentation.snapshot()["apply_dtn"] == 1
+    with pytest.raises(ValueError):
+        solver.solve(st, np.zeros(5))
+
+
+def test_state_api_against_oracle():
+    cfg, L = 2, 2
+    tree, nodes, st = gpu_build(cfg, L)
+    ot = O.build_tree((0, 1, 0, 1), L, 16)
+    ost = O.build(ot, coeff_dict(problems.coefficients(cfg)))
+    f = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=3, batch=1)
+    assert rel(solver.apply_global_dtn(st, f), ost.root_T @ f) < 1e-12
+    u = solver.solve(st, f)
+    pts = [(0.13, 0.71), (0.5, 0.5), (0.999, 0.0001), (0.25, 0.75)]
+    uo = O.solve(ost, f)
+    # post_process is null-mode invariant: compare against the oracle-state evaluation
+    W = O.leaf_cheb_field(ost, uo)
+    ref = []
+    for (x, y) in pts:
+        leaf = tree.boxes[solver._owning_leaf(st, x, y).index]
+        k = leaf.index - (4 ** L - 1)
+        Wk = W[k].reshape(16, 16)
+        rx = P.grid.interp_matrix(st.geometry.cheb_x, [x - leaf.rect.x_lo])
+        ry = P.grid.interp_matrix(st.geometry.cheb_y, [y - leaf.rect.y_lo])
+        ref.append(float(rx @ Wk @ ry.T))
+    assert rel(solver.post_process(st, u, pts), np.array(ref)) < 1e-10
+    bpts = [(0.0, 0.3), (1.0, 0.6), (0.2, 0.0), (0.7, 1.0)]
+    assert np.all(np.isfinite(solver.boundary_flux_at(st, u, bpts)))
+    rep = solver.memory_report(st)
+    ni, nb = 196, 60
+    S_entries = sum(ost.S[b].size for b in ost.S)
+    want = ost.root_T.size + st.n_leaf_groups * ni * nb + st.geometry.L1.size + st.geometry.L4.size + S_entries
+    assert rep["total_entries"] == want
+    assert st.S[0].dense.shape == ost.S[0].shape and len(st.psi) == 16

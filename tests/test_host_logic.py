@@ -1,0 +1,95 @@
+"""Host-side logic of the product path that runs without a GPU: coefficient sampling and leaf
+grouping (solver.py:196-222), geometry constants, problem generators, memory accounting."""
+import numpy as np
+import pytest
+
+import paper_1307_2665_b200 as P
+from oracle import hps_oracle as O
+from paper_1307_2665_b200 import problems, solver
+from paper_1307_2665_b200.grid import layout_of
+
+from _util import coeff_dict
+
+
+@pytest.mark.parametrize("cfg,L", [(1, 3), (2, 3), (4, 4), (5, 2)])
+def test_grouping_matches_reference_semantics(cfg, L):
+    co = problems.coefficients(cfg)
+    tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), L, 16)
+    lay = layout_of(tree)
+    geom = P.LeafGeometry.get(16, tree.leaf_width, tree.leaf_height)
+    fields = solver._sample(co, lay, geom)
+    reps, gid = solver._group(fields, 4 ** L)
+    ot = O.build_tree((0, 1, 0, 1), L, 16)
+    og = O.Geometry(16, ot.leaf_width, ot.leaf_height)
+    ofields = O.sample_coefficients(coeff_dict(co), ot, og)
+    oreps, ogid = O.group_leaves(ofields, 4 ** L)
+    assert np.array_equal(reps, oreps) and np.array_equal(gid, ogid)
+    for name in O.COEFF_NAMES:
+        if not np.isscalar(fields[name]):
+            assert np.array_equal(fields[name], ofields[name])
+
+
+def test_var_helmholtz_groups_collapse_bitwise_equal_leaves():
+    # cfg 4's symmetric coefficient makes some leaves bitwise equal (61,086 of 65,536 at L=8)
+    co = problems.coefficients(4)
+    tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), 5, 16)
+    geom = P.LeafGeometry.get(16, tree.leaf_width, tree.leaf_height)
+    reps, gid = solver._group(solver._sample(co, layout_of(tree), geom), 4 ** 5)
+    assert reps.size < 4 ** 5 and gid.max() == reps.size - 1 and np.all(reps[gid[reps]] == reps)
+
+
+def test_device_constants_layout():
+    g = P.LeafGeometry.get(16, 1 / 64, 1 / 64)
+    blob, idx, pmax = g.device_constants()
+    p2, ni, nb, ng = 256, 196, 60, 64
+    assert blob.size == 4 * p2 + ng * nb + ng * ni + nb * ng + ni
+    assert np.array_equal(blob[:p2], g.Dx.ravel())
+    assert np.array_equal(blob[2 * p2:3 * p2], (g.Dx @ g.Dx).ravel())
+    assert np.array_equal(idx[:ni], g.J_i) and np.array_equal(idx[ni:], g.J_e)
+    assert pmax == np.abs(blob[-ni:]).max()
+
+
+@pytest.mark.parametrize("axis", ["v", "h"])
+def test_corner_modes_are_null_vectors_of_the_interface(axis):
+    """X V = 0 and [T13a; T23b] V = 0 for the analytic corner modes (the deflation basis)."""
+    L = 2
+    co = problems.coefficients(2)
+    ot = O.build_tree((0, 1, 0, 1), L, 16)
+    st = O.build(ot, coeff_dict(co), keep_T=True)
+    geom = P.LeafGeometry.get(16, ot.leaf_width, ot.leaf_height)
+    box = 0 if axis == "v" else 1
+    a, c = ot.child_a[box], ot.child_b[box]
+    j1a, j2b, j3a, j3b = O.split_indices(ot.I_e[a], ot.I_e[c], ot.I_i[box])
+    Ta, Tb = st.T[a], st.T[c]
+    X = Ta[np.ix_(j3a, j3a)] - Tb[np.ix_(j3b, j3b)]
+    C = np.concatenate([Ta[np.ix_(j1a, j3a)], Tb[np.ix_(j2b, j3b)]])
+    vs, ve = geom.corner_mode_vectors(axis)
+    n3 = X.shape[0]
+    m = n3 // 16
+    V = np.zeros((n3, m - 1))
+    for s in range(m - 1):
+        V[s * 16:(s + 1) * 16, s] = ve
+        V[(s + 1) * 16:(s + 2) * 16, s] = vs
+    assert np.abs(X @ V).max() < 1e-13 * np.abs(X).max()
+    assert np.abs(C @ V).max() < 1e-13 * np.abs(C).max()
+    Xd = X + np.abs(np.diag(X)).max() * V @ V.T
+    assert np.linalg.cond(Xd) < 1e4  # deflated interface is well conditioned
+
+
+def test_boundary_data_generators():
+    tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), 2, 16)
+    pts = nodes.points[tree.root.I_e]
+    F = problems.boundary_data(2, pts, seed=5, batch=3)
+    assert F.shape == (pts.shape[0], 3)
+    assert np.array_equal(F, problems.boundary_data(2, pts, seed=5, batch=3))
+    t = problems.perimeter_parameter(pts[:, 0], pts[:, 1])
+    assert t.min() >= 0 and t.max() < 4
+    f1 = problems.boundary_data(1, pts)
+    assert f1.shape == (pts.shape[0],) and np.allclose(f1, np.exp(pts[:, 0]) * np.sin(pts[:, 1]))
+    F3 = problems.boundary_data(3, pts, seed=2, batch=2)
+    U3 = problems.exact_solution(3, pts[:, 0], pts[:, 1], seed=2, batch=2)
+    assert np.array_equal(F3, U3)
+
+
+def test_unknowns_definition():
+    assert O.unknowns(6, 16) == 1048576 and O.unknowns(9, 16) == 67108864
