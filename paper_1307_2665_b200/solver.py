@@ -578,7 +578,7 @@ def post_process(state, u, targets):
             W = cache[leaf.index] = _leaf_field(state, u, leaf)
         rx = interp_matrix(geom.cheb_x, [x - leaf.rect.x_lo])
         ry = interp_matrix(geom.cheb_y, [y - leaf.rect.y_lo])
-        out[t] = float(rx @ W @ ry.T)
+        out[t] = float((rx @ W @ ry.T)[0, 0])
     return out
 
 
@@ -597,7 +597,7 @@ def boundary_flux_at(state, u, targets):
         dW = geom.Dx @ W if (on_v and not on_h) else W @ geom.Dy.T
         rx = interp_matrix(geom.cheb_x, [x - leaf.rect.x_lo])
         ry = interp_matrix(geom.cheb_y, [y - leaf.rect.y_lo])
-        out[t] = float(rx @ dW @ ry.T)
+        out[t] = float((rx @ dW @ ry.T)[0, 0])
     return out
 
 

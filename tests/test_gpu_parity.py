@@ -181,7 +181,7 @@ def test_state_api_against_oracle():
         Wk = W[k].reshape(16, 16)
         rx = P.grid.interp_matrix(st.geometry.cheb_x, [x - leaf.rect.x_lo])
         ry = P.grid.interp_matrix(st.geometry.cheb_y, [y - leaf.rect.y_lo])
-        ref.append(float(rx @ Wk @ ry.T))
+        ref.append(float((rx @ Wk @ ry.T)[0, 0]))
     assert rel(solver.post_process(st, u, pts), np.array(ref)) < 1e-10
     bpts = [(0.0, 0.3), (1.0, 0.6), (0.2, 0.0), (0.7, 1.0)]
     assert np.all(np.isfinite(solver.boundary_flux_at(st, u, bpts)))
