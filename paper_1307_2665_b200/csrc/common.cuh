@@ -53,6 +53,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Explicit shared-memory store. Copy loops over a register array written with plain stores get
+// turned into memcpy by LLVM, which forces the array into local memory; this keeps it in registers.
+__device__ __forceinline__ void sts64(double* p, double v) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(smem_u32(p)), "d"(v) : "memory");
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
