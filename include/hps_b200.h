@@ -69,6 +69,12 @@ int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const double* T_ch
 int hps_solve_level(int nbatch, int n3, int ne, const double* S, const int* Ie, long long ii_start0,
                     double* u, int ldu, int nrhs, void* stream);
 
+/* In-place inverse of `batch` n x n matrices (partial-pivoting Gauss-Jordan for n <= 128, recursive
+ * 2x2 block inverse on the DMMA GEMM above that; n % 32 == 0 when n > 128). *status as above. */
+size_t hps_inverse_workspace_bytes(int n, int batch);
+int hps_inverse_batched(int n, int batch, double* X, long long lda, long long strideX, void* ws,
+                        size_t ws_bytes, int* status, void* stream);
+
 /* C[b] = alpha A[b] B[b] + beta C[b]; optional B-row gather Bidx (NULL = none). K % 16 == 0. */
 int hps_dgemm_batched(int M, int N, int K, int batch, double alpha, const double* A, long long lda,
                       long long strideA, const double* B, long long ldb, long long strideB,

@@ -12,7 +12,7 @@ import os
 from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhps_b200.so")
+LIB_PATH = os.environ.get("HPS_LIB") or os.path.join(_HERE, "libhps_b200.so")
 
 HPS_OK = 0
 HPS_ERR_LEAF_RESONANCE = 1
@@ -24,7 +24,7 @@ HPS_ERR_ARG = 5
 #: every symbol include/hps_b200.h declares (tests check the .so exports all of them)
 EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_launch_count", "hps_leaf_workspace_bytes",
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
-           "hps_dgemm_batched")
+           "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched")
 
 _lib = None
 
@@ -64,6 +64,10 @@ def load():
     lib.hps_dgemm_batched.argtypes = [c_int, c_int, c_int, c_int, c_d, c_dp, c_ll, c_ll, c_dp, c_ll, c_ll, c_dp,
                                       c_ll, c_d, c_dp, c_ll, c_ll, c_dp]
     lib.hps_dgemm_batched.restype = c_int
+    lib.hps_inverse_workspace_bytes.argtypes = [c_int, c_int]
+    lib.hps_inverse_workspace_bytes.restype = c_sz
+    lib.hps_inverse_batched.argtypes = [c_int, c_int, c_dp, c_ll, c_ll, c_dp, c_sz, c_dp, c_dp]
+    lib.hps_inverse_batched.restype = c_int
     _lib = lib
     return lib
 

@@ -2,14 +2,14 @@
 # Build libhps_b200.so in-tree for sm_100a (the .so travels to the GPU box with the repo).
 set -euo pipefail
 here="$(cd "$(dirname "$0")" && pwd)"
-out="${here}/../libhps_b200.so"
+out="${HPS_OUT:-${here}/../libhps_b200.so}"
 NVCC="${NVCC:-nvcc}"
 FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
        -I"${here}" -I"${here}/../../include" --expt-relaxed-constexpr ${HPS_NVCC_EXTRA:-})
 objs=()
-mkdir -p "${here}/../build_obj"
+mkdir -p "${HPS_OBJ:-${here}/../build_obj}"
 for f in capi gemm merge solve leaf; do
-  o="${here}/../build_obj/${f}.o"
+  o="${HPS_OBJ:-${here}/../build_obj}/${f}.o"
   if [[ ! -f "$o" || "${here}/${f}.cu" -nt "$o" || "${here}/common.cuh" -nt "$o" || "${here}/gemm.cuh" -nt "$o" ]]; then
     "$NVCC" "${FLAGS[@]}" -c "${here}/${f}.cu" -o "$o" &
   fi

@@ -273,28 +273,35 @@ __global__ void __launch_bounds__(LEAF_THREADS) k_leaf(LeafArgs a) {
 // After 13 panels, row p_k of M holds x_k (Gauss-Jordan: no back substitution phase). The DtN
 // epilogue T = (L43e + L43i Psi) L1 also runs on DMMA.
 // ---------------------------------------------------------------------------------------------
+#ifdef HPS_LEAF_PROFILE
+__device__ long long g_leaf_prof[1024][8];
+#define PROF_T(var) long long var = clock64()
+#define PROF_ADD(slot, t0) do { if (threadIdx.x == 0) g_leaf_prof[blockIdx.x][slot] += clock64() - (t0); } while (0)
+#else
+#define PROF_T(var)
+#define PROF_ADD(slot, t0)
+#endif
 namespace l16 {
 constexpr int NI = 196, NB = 60, NG = 64, NCOLS = 257, LDM = 260, MROWS = 200;
 constexpr int SA = 20;   // A16 row stride (== 4 mod 16: conflict-free A fragments)
-constexpr int SB = 264;  // W row stride (== 8 mod 16: conflict-free B fragments)
+constexpr int SB = 264;  // W row stride (== 8 mod 16: conflict-free B fragments); >= 256 columns
 constexpr int ST1 = 68;  // T1 row stride
-constexpr int THREADS = 256;
-constexpr int SMEM_D = MROWS * SA + 16 * SB + 16 * 17 + 16;  // doubles
+constexpr int SMEM_D = MROWS * SA + 16 * SB + 16 * 17 + 32;  // doubles
 constexpr size_t SMEM = SMEM_D * sizeof(double) + sizeof(int) * (NI + NI + NB) + 64;
 }  // namespace l16
 
-__global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, 512 / THREADS) k_leaf16(LeafArgs a) {
   using namespace l16;
   extern __shared__ __align__(16) double sm[];
-  __shared__ double redv[8];
-  __shared__ int redi[8];
-  __shared__ int s_piv;
+  __shared__ double redv[32];
+  __shared__ int redi[32];
   __shared__ int s_sing;
   double* sA16 = sm;                 // MROWS x SA
   double* sW = sA16 + MROWS * SA;    // 16 x SB
   double* sLU = sW + 16 * SB;        // 16 x 17
-  double* sProw = sLU + 16 * 17;     // 16
-  int* sPiv = reinterpret_cast<int*>(sProw + 16);  // NI: pivot row of step k
+  double* sProw = sLU + 16 * 17;     // 2 x 16 (double-buffered pivot row)
+  int* sPiv = reinterpret_cast<int*>(sProw + 32);  // NI: pivot row of step k
   int* Ji = sPiv + NI;
   int* Je = Ji + NI;
   // assembly-phase aliases (inside sA16/sW)
@@ -324,6 +331,7 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
     }
     if (tid == 0) s_sing = 0;
     __syncthreads();
+    PROF_T(t_asm);
 
     // ---- assemble (same per-entry op sequence as leafops.py:217-233) ----
     double rowmax = 0.0;
@@ -366,12 +374,14 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
     for (int w = 0; w < THREADS / 32; ++w) anorm = fmax(anorm, redv[w]);
     __syncthreads();
 
+    PROF_ADD(0, t_asm);
     // ---- block Gauss-Jordan, 13 panels ----
     int mystep = -1;
     bool act = tid < NI;
     for (int kp = 0; kp < (NI + 15) / 16; ++kp) {
       const int k0 = kp * 16;
       const int kb = min(16, NI - k0);
+      PROF_T(t_pan);
       double orig[16], work[16];
       if (tid < NI) {
         const double2* row = reinterpret_cast<const double2*>(M + (long long)tid * LDM + k0);
@@ -400,35 +410,38 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
           }
           if (lane == 0) { redv[warp] = cand; redi[warp] = ci; }
           __syncthreads();
-          if (warp == 0) {
-            double v = lane < 8 ? redv[lane] : -2.0;
-            int vi = lane < 8 ? redi[lane] : 0x7fffffff;
+          {  // every warp reduces the per-warp candidates (identical result): no broadcast barrier
+            constexpr int NW = THREADS / 32;
+            double v = lane < NW ? redv[lane] : -2.0;
+            int vi = lane < NW ? redi[lane] : 0x7fffffff;
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) {
+            for (int o = NW / 2; o > 0; o >>= 1) {
               const double ov = __shfl_xor_sync(0xffffffffu, v, o);
               const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
               if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
             }
-            if (lane == 0) { s_piv = vi; sPiv[k0 + j] = vi; }
-          }
-          __syncthreads();
-          if (tid == s_piv) {
-            act = false;
-            mystep = k0 + j;
-            if (work[j] == 0.0) s_sing = 1;
+            vi = __shfl_sync(0xffffffffu, vi, 0);
+            if (tid == 0) sPiv[k0 + j] = vi;
+            if (tid == vi) {
+              act = false;
+              mystep = k0 + j;
+              if (work[j] == 0.0) s_sing = 1;
 #pragma unroll
-            for (int c = 0; c < 16; ++c) sts64(sProw + c, work[c]);
+              for (int c = 0; c < 16; ++c) sts64(sProw + (j & 1) * 16 + c, work[c]);
+            }
           }
           __syncthreads();
           if (act) {
-            const double pv = sProw[j];
-            const double l = work[j] / pv;
+            const double* pr = sProw + (j & 1) * 16;  // double-buffered: no barrier after the update
+            const double l = work[j] / pr[j];
             work[j] = l;
 #pragma unroll
-            for (int c = j + 1; c < 16; ++c) work[c] = fma(-l, sProw[c], work[c]);
+            for (int c = j + 1; c < 16; ++c) work[c] = fma(-l, pr[c], work[c]);
           }
         }
       }
+      PROF_ADD(1, t_pan);
+      PROF_T(t_w);
       const bool inP = mystep >= k0 && mystep < k0 + kb;
       if (inP) {
         const int r = mystep - k0;
@@ -443,7 +456,7 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
       // W = U11^{-1} L11^{-1} M[P, c0:]
       const int c0 = k0 + kb;
       const int nT = LDM - c0;
-      const int nTp = (nT + 31) & ~31;
+      const int nTp = (nT + 127) & ~127;  // W is padded with zero columns to whole 128-chunks
       for (int cc = tid; cc < nTp; cc += THREADS) {
         double y[16];
 #pragma unroll
@@ -470,37 +483,53 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
             if (r < kb) M[(long long)sPiv[k0 + r] * LDM + c0 + cc] = y[r];
       }
       __syncthreads();
-      // M[:, c0:] += (-orig) * W on DMMA; warp tile = 8 rows x 32 cols
-      const int nct = nTp / 32;
-      const int ntiles = (MROWS / 8) * nct;
-      for (int t = warp; t < ntiles; t += THREADS / 32) {
-        const int r0 = (t / nct) * 8, cb = (t % nct) * 32;
-        double acc[4][2];
-        double* Mr = M + (long long)(r0 + g) * LDM + c0 + cb;
+      // M[:, c0:] += (-orig) * W on DMMA. Warp = row tiles of 8 (A fragments kept in registers);
+      // columns in chunks of 128 = 16 DMMA tiles whose C loads are all issued before the first
+      // DMMA, so one L2 round trip covers 16 tiles.
+      PROF_ADD(2, t_w);
+      PROF_T(t_u);
+      const int nchunk = (nT + 127) >> 7;
+      for (int item = warp; item < (MROWS / 8) * nchunk; item += THREADS / 32) {
+        const int r0 = (item / nchunk) * 8;
+        const int cb = (item % nchunk) * 128;
+        double af[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int col = 8 * j + 2 * tq;
-          if (cb + col < nT) {
-            const double2 v = *reinterpret_cast<const double2*>(Mr + col);
-            acc[j][0] = v.x;
-            acc[j][1] = v.y;
-          } else {
-            acc[j][0] = acc[j][1] = 0.0;
+        for (int ks = 0; ks < 4; ++ks) af[ks] = sA16[(r0 + g) * SA + 4 * ks + tq];
+        double* Mr = M + (long long)(r0 + g) * LDM + c0;
+        {
+          double acc[16][2];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = cb + 8 * j + 2 * tq;
+            if (col < nT) {
+              const double2 v = *reinterpret_cast<const double2*>(Mr + col);
+              acc[j][0] = v.x;
+              acc[j][1] = v.y;
+            } else {
+              acc[j][0] = acc[j][1] = 0.0;
+            }
+          }
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            if (4 * ks < kb) {
+              const double* Wr = sW + (4 * ks + tq) * SB + cb + g;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) dmma_8x8x4(acc[j][0], acc[j][1], af[ks], Wr[8 * j]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = cb + 8 * j + 2 * tq;
+            if (col < nT) *reinterpret_cast<double2*>(Mr + col) = make_double2(acc[j][0], acc[j][1]);
           }
         }
-        for (int ks = 0; ks < kb; ks += 4) {
-          const double af = sA16[(r0 + g) * SA + ks + tq];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[j][0], acc[j][1], af, sW[(ks + tq) * SB + cb + 8 * j + g]);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int col = 8 * j + 2 * tq;
-          if (cb + col < nT) *reinterpret_cast<double2*>(Mr + col) = make_double2(acc[j][0], acc[j][1]);
-        }
       }
+      PROF_ADD(3, t_u);
+      PROF_T(t_ub);
       __syncthreads();
+      PROF_ADD(4, t_ub);
     }
+    PROF_T(t_ep);
 
     // ---- X rows in step order; probe condition estimate; Psi = -X[:, :NB] ----
     double* Psi = a.Psi + (long long)grp * NI * NB;
@@ -508,7 +537,7 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
     for (int e = tid; e < NI * (NB + 1); e += THREADS) {
       const int k = e / (NB + 1), c = e - k * (NB + 1);
       const double v = M[(long long)sPiv[k] * LDM + NI + c];
-      if (c < NB) Psi[k * NB + c] = -v;
+      if (c < NB) __stcs(Psi + k * NB + c, -v);
       else pm = fmax(pm, fabs(v));
     }
     pm = warp_max(pm);
@@ -522,7 +551,7 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
     }
     __syncthreads();
     // ---- T1 = L43e + L43i Psi (64 x 60), warp = 8 rows x 64 cols ----
-    {
+    if (warp < 8) {
       const int r0 = warp * 8;
       double acc[8][2];
 #pragma unroll
@@ -550,7 +579,7 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
     }
     __syncthreads();
     // ---- T = T1 L1 (64 x 64), K = 60 ----
-    {
+    if (warp < 8) {
       const int r0 = warp * 8;
       double acc[8][2];
 #pragma unroll
@@ -564,8 +593,9 @@ __global__ void __launch_bounds__(l16::THREADS, 2) k_leaf16(LeafArgs a) {
       double* T = a.T + (long long)grp * NG * NG;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        *reinterpret_cast<double2*>(T + (r0 + g) * NG + 8 * j + 2 * tq) = make_double2(acc[j][0], acc[j][1]);
+        __stcs(reinterpret_cast<double2*>(T + (r0 + g) * NG + 8 * j + 2 * tq), make_double2(acc[j][0], acc[j][1]));
     }
+    PROF_ADD(5, t_ep);
   }
 }
 
@@ -586,7 +616,27 @@ int leaf_grid(int ngroups) {
 
 using namespace hps;
 
-static int leaf16_grid(int ngroups) { return std::max(1, std::min(ngroups, 2 * leaf_grid(1 << 30))); }
+static int leaf16_threads() {
+  static int t = getenv("HPS_LEAF16_THREADS") ? atoi(getenv("HPS_LEAF16_THREADS")) : 256;
+  return t == 512 ? 512 : 256;
+}
+static int leaf16_grid(int ngroups) {
+  static int per_sm = getenv("HPS_LEAF_CTAS_PER_SM") ? atoi(getenv("HPS_LEAF_CTAS_PER_SM"))
+                                                     : (leaf16_threads() == 512 ? 1 : 2);
+  return std::max(1, std::min(ngroups, per_sm * leaf_grid(1 << 30)));
+}
+
+#ifdef HPS_LEAF_PROFILE
+extern "C" int hps_debug_leaf_profile(long long* out, int reset) {
+  if (reset) {
+    static long long z[1024][8] = {};
+    cudaMemcpyToSymbol(g_leaf_prof, z, sizeof(z));
+    return 0;
+  }
+  cudaMemcpyFromSymbol(out, g_leaf_prof, sizeof(long long) * 1024 * 8);
+  return 0;
+}
+#endif
 
 extern "C" size_t hps_leaf_workspace_bytes(int p, int ngroups) {
   if (p == 16) return sizeof(double) * (size_t)leaf16_grid(ngroups) * l16::MROWS * l16::LDM + 256;
@@ -624,10 +674,14 @@ extern "C" int hps_leaf_stage(int p, int ngroups, const double* const* fields, c
     a.scratch_stride = (long long)l16::MROWS * l16::LDM;
     static bool attr = false;
     if (!attr) {
-      HPS_CUDA_CHECK(cudaFuncSetAttribute(k_leaf16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l16::SMEM));
+      HPS_CUDA_CHECK(cudaFuncSetAttribute(k_leaf16<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l16::SMEM));
+      HPS_CUDA_CHECK(cudaFuncSetAttribute(k_leaf16<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l16::SMEM));
       attr = true;
     }
-    k_leaf16<<<leaf16_grid(ngroups), l16::THREADS, l16::SMEM, st>>>(a);
+    if (leaf16_threads() == 512)
+      k_leaf16<512><<<leaf16_grid(ngroups), 512, l16::SMEM, st>>>(a);
+    else
+      k_leaf16<256><<<leaf16_grid(ngroups), 256, l16::SMEM, st>>>(a);
     HPS_LAUNCH_CHECK();
     return HPS_OK;
   }

@@ -92,112 +92,130 @@ __device__ __forceinline__ double vvt(int r, int c, int q, int nseg, const doubl
   return 0.0;
 }
 
-// Gauss-Jordan inverse with partial pivoting for n <= 16*NT (one CTA of 256 threads per matrix).
-// The matrix lives in REGISTERS: thread (ty, tx) of a 16x16 grid owns rows ty + 16a and columns
-// tx + 16b (a, b < NT), a cyclic distribution that stays balanced as pivots are consumed. Pivoting
-// is implicit. Row p_k is eliminated at step k, and no physical swap is made, so the in-place
-// result B satisfies inv(X)[k][p_j] = B[p_k][j]; the write-out applies that permutation. Per step:
-// pivot search over the unused rows (warp 0), then broadcast of the pivot row and column through
-// shared memory, then a register-resident rank-1 update.
-template <int NT>
-__global__ void __launch_bounds__(256) k_gj_inverse(const double* Xin, double* Xout,
-                                                    long long lda, long long strideX, int n,
-                                                    int* status, int status_base) {
-  constexpr int NMAX = 16 * NT;
-  __shared__ double colk[NMAX];
-  __shared__ double rowp[NMAX];
-  __shared__ int pivrow[NMAX];  // pivrow[k] = physical row eliminated at step k
-  __shared__ int rowstep[NMAX]; // inverse permutation
-  __shared__ int used[NMAX];
-  __shared__ int s_p;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+// Gauss-Jordan inverse with partial pivoting for n <= 32*RPL (one CTA of W warps per matrix).
+// Layout: warp w owns columns [w*CPW, (w+1)*CPW); lane l owns rows l + 32*i (i < RPL). The whole
+// matrix lives in registers. One __syncthreads per pivot step:
+//   * column k (already updated) sits in a double-buffered shared vector; EVERY warp computes the
+//     same argmax over the unused rows from it, so no broadcast barrier is needed;
+//   * the pivot row reaches the lanes of each warp by shuffles, since it holds that warp's columns;
+//   * after its rank-1 update, the warp that owns column k+1 publishes it for the next step.
+// Pivoting is implicit (no row swaps): row p_k is eliminated at step k and the in-place result B
+// satisfies inv(X)[k][p_j] = B[p_k][j]; the write-out applies that permutation.
+template <int RPL, int CPW, int W>
+__global__ void __launch_bounds__(W * 32) k_gj_inverse(double* X, long long lda, long long strideX, int n,
+                                                      int* status, int status_base) {
+  constexpr int NMAX = 32 * RPL;
+  __shared__ double colbuf[2][NMAX];
+  __shared__ int pivrow[NMAX];
+  __shared__ int rowstep[NMAX];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x;
-  const double* X = Xin + (long long)b * strideX;
-  double* Y = Xout + (long long)b * strideX;
-  double a[NT][NT];
+  double* Xb = X + (long long)b * strideX;
+  const int cbase = warp * CPW;
+  double a[RPL][CPW];
+  bool used[RPL];
 #pragma unroll
-  for (int i = 0; i < NT; ++i)
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+    used[i] = r >= n;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int r = ty + 16 * i, c = tx + 16 * j;
-      a[i][j] = (r < n && c < n) ? X[(long long)r * lda + c] : 0.0;
+    for (int j = 0; j < CPW; ++j) {
+      const int c = cbase + j;
+      a[i][j] = (r < n && c < n) ? Xb[(long long)r * lda + c] : 0.0;
     }
-  for (int i = tid; i < NMAX; i += 256) used[i] = (i < n) ? 0 : 1;
+  }
+  // publish column 0
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) colbuf[0][lane + 32 * i] = a[i][0];
+  }
   __syncthreads();
   bool singular = false;
-  // k = 16*jb + kk: the column slot jb is a compile-time constant in every unrolled copy, so the
-  // register tile is never indexed dynamically (which would force it into local memory).
+  for (int k = 0; k < n; ++k) {
+    const double* ck = colbuf[k & 1];
+    // argmax |col k| over the unused rows. Non-negative doubles order like their bit patterns, so
+    // three 32-bit warp reductions (REDUX) give the exact argmax with ties to the smallest row.
+    double cv[RPL];
+    unsigned long long bestkey = 0ull;
+    int bi = 0x7fffffff;
 #pragma unroll
-  for (int jb = 0; jb < NT; ++jb) {
-    for (int kk = 0; kk < 16; ++kk) {
-      const int k = 16 * jb + kk;
-      if (k >= n) break;
-      if (tx == kk) {
-#pragma unroll
-        for (int i = 0; i < NT; ++i) colk[ty + 16 * i] = a[i][jb];
-      }
-      __syncthreads();
-      if (tid < 32) {
-        double best = -1.0;
-        int bi = 0;
-        for (int r = tid; r < n; r += 32) {
-          const double v = used[r] ? -1.0 : fabs(colk[r]);
-          if (v > best) { best = v; bi = r; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-        }
-        if (tid == 0) { s_p = bi; pivrow[k] = bi; rowstep[bi] = k; used[bi] = 1; }
-      }
-      __syncthreads();
-      const int p = s_p;
-      const double piv = colk[p];
-      singular |= (piv == 0.0);
-      const double inv = 1.0 / piv;
-      if (ty == (p & 15)) {
-        const int ip = p >> 4;
-#pragma unroll
-        for (int i = 0; i < NT; ++i) {
-#pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            if (i == ip) rowp[tx + 16 * j] = a[i][j] * inv;
-          }
-        }
-      }
-      __syncthreads();
-      double rp[NT], cf[NT];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) rp[j] = rowp[tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < NT; ++i) cf[i] = colk[ty + 16 * i];
-      const bool own_col = (tx == kk);
-#pragma unroll
-      for (int i = 0; i < NT; ++i) {
-        const bool prow = (ty + 16 * i) == p;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const bool kcol = own_col && (j == jb);
-          double v = fma(-cf[i], rp[j], a[i][j]);
-          v = kcol ? -cf[i] * inv : v;
-          v = prow ? (kcol ? inv : rp[j]) : v;
-          a[i][j] = v;
-        }
-      }
-      __syncthreads();
+    for (int i = 0; i < RPL; ++i) {
+      cv[i] = ck[lane + 32 * i];
+      const unsigned long long key = used[i] ? 0ull : (unsigned long long)__double_as_longlong(fabs(cv[i]));
+      const int idx = used[i] ? 0x7fffffff : lane + 32 * i;
+      if (key > bestkey || (key == bestkey && idx < bi)) { bestkey = key; bi = idx; }
     }
+    const unsigned hi = (unsigned)(bestkey >> 32), lo = (unsigned)bestkey;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    const int p = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)bi : 0xffffffffu);
+    const int pl = p & 31, pi = p >> 5;
+    const double piv = ck[p];
+    singular |= (piv == 0.0);
+    const double inv = 1.0 / piv;
+    if (threadIdx.x == 0) { pivrow[k] = p; rowstep[p] = k; }
+    // pivot row for this warp's columns (pi is warp-uniform: a uniform branch, no selects)
+    double rp[CPW];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i)
+      if (pi == i) {
+        if (lane == pl) used[i] = true;
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) rp[j] = __shfl_sync(0xffffffffu, a[i][j], pl) * inv;
+      }
+    // column k: the owning warp zeroes it and sets its "pivot row" entry to inv, so the common
+    // update below yields -f*inv in column k and inv at the pivot position.
+    const int kw = k / CPW;
+    if (warp == kw) {
+      const int kj = k - kw * CPW;
+#pragma unroll
+      for (int j = 0; j < CPW; ++j)
+        if (j == kj) {
+          rp[j] = inv;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) a[i][j] = 0.0;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const double f = cv[i];
+      if (pi == i) {  // the slot holding the pivot row (one lane) takes rp itself
+        const bool prow = (lane == pl);
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) {
+          const double v = fma(-f, rp[j], a[i][j]);
+          a[i][j] = prow ? rp[j] : v;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) a[i][j] = fma(-f, rp[j], a[i][j]);
+      }
+    }
+    // publish column k+1 (after this step's update) for the next step
+    if (k + 1 < n && warp == (k + 1) / CPW) {
+      const int j1 = (k + 1) - warp * CPW;
+#pragma unroll
+      for (int j = 0; j < CPW; ++j)
+        if (j == j1) {
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) sts64(&colbuf[(k + 1) & 1][lane + 32 * i], a[i][j]);
+        }
+    }
+    __syncthreads();
   }
   // inv(X)[rowstep[r]][pivrow[c]] = B[r][c]
 #pragma unroll
-  for (int i = 0; i < NT; ++i)
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+    if (r >= n) continue;
+    const long long orow = (long long)rowstep[r] * lda;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int r = ty + 16 * i, c = tx + 16 * j;
-      if (r < n && c < n) Y[(long long)rowstep[r] * lda + pivrow[c]] = a[i][j];
+    for (int j = 0; j < CPW; ++j) {
+      const int c = cbase + j;
+      if (c < n) Xb[orow + pivrow[c]] = a[i][j];
     }
-  if (singular && status && tid == 0) atomicMax(status, status_base + b);
+  }
+  if (singular && status && threadIdx.x == 0) atomicMax(status, status_base + b);
 }
 
 // Deflation X += sigma V V^T, sigma = max |diag X|: one CTA per (segment row, merge).
@@ -221,13 +239,13 @@ __global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs
 static int inverse_small(double* X, long long lda, long long strideX, int n, int batch, int* status,
                          int status_base, cudaStream_t st) {
   if (n <= 16)
-    k_gj_inverse<1><<<batch, 256, 0, st>>>(X, X, lda, strideX, n, status, status_base);
+    k_gj_inverse<1, 8, 2><<<batch, 64, 0, st>>>(X, lda, strideX, n, status, status_base);
   else if (n <= 32)
-    k_gj_inverse<2><<<batch, 256, 0, st>>>(X, X, lda, strideX, n, status, status_base);
+    k_gj_inverse<1, 8, 4><<<batch, 128, 0, st>>>(X, lda, strideX, n, status, status_base);
   else if (n <= 64)
-    k_gj_inverse<4><<<batch, 256, 0, st>>>(X, X, lda, strideX, n, status, status_base);
+    k_gj_inverse<2, 8, 8><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
   else if (n <= 128)
-    k_gj_inverse<8><<<batch, 256, 0, st>>>(X, X, lda, strideX, n, status, status_base);
+    k_gj_inverse<4, 16, 8><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
   else {
     set_error("inverse_small: n=%d > 128", n);
     return HPS_ERR_ARG;
@@ -332,4 +350,20 @@ extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const d
   HPS_TRY(gemm(ne, ne, n3, nbatch, 1.0, Cm, n3, (long long)ne * n3, S_out, ne, (long long)n3 * ne, 1.0, T_out, ne,
                (long long)ne * ne, st));
   return HPS_OK;
+}
+
+// Batched in-place inverse (n <= 128 uses the register Gauss-Jordan kernel directly, larger n the
+// recursive block inverse). Exposed for unit tests and micro-benchmarks.
+extern "C" size_t hps_inverse_workspace_bytes(int n, int batch) {
+  return inverse_rec_tmp_doubles(n, batch) * sizeof(double) + 256;
+}
+
+extern "C" int hps_inverse_batched(int n, int batch, double* X, long long lda, long long strideX, void* ws,
+                                   size_t ws_bytes, int* status, void* stream) {
+  if (ws_bytes < hps_inverse_workspace_bytes(n, batch) || (n > 128 && (n % 32))) {
+    set_error("hps_inverse_batched: bad arguments n=%d ws=%zu", n, ws_bytes);
+    return HPS_ERR_ARG;
+  }
+  return inverse_rec(X, lda, strideX, n, batch, static_cast<double*>(ws), status, 0,
+                     static_cast<cudaStream_t>(stream));
 }

@@ -228,17 +228,31 @@ def _sample(coeffs, lay, geom):
 def _group(fields, n_leaf):
     """Group leaves whose six sample rows are bitwise equal (solver.py:208-222).
 
-    Returns (rep leaf positions in first-occurrence order, group id per leaf)."""
-    arrays = [fields[n] for n in COEFF_NAMES if not np.isscalar(fields[n])]
+    Returns (rep leaf positions in first-occurrence order, group id per leaf). Exact: rows are
+    bucketed by a 64-bit hash of their bit patterns, then every row is compared bitwise with its
+    bucket's first row. A hash collision (never observed) falls back to exact byte-key sorting.
+    """
+    arrays = [np.ascontiguousarray(fields[n]).view(np.uint64).reshape(n_leaf, -1)
+              for n in COEFF_NAMES if not np.isscalar(fields[n])]
     if not arrays:
         return np.zeros(1, np.int64), np.zeros(n_leaf, np.int64)
-    rows = np.ascontiguousarray(np.concatenate(arrays, axis=1)).view(np.uint8).reshape(n_leaf, -1)
-    key = rows.view(np.dtype((np.void, rows.shape[1]))).reshape(n_leaf)
-    _, first, inv = np.unique(key, return_index=True, return_inverse=True)
+    rng = np.random.default_rng(0x5eed)
+    h = np.zeros(n_leaf, np.uint64)
+    with np.errstate(over="ignore"):
+        for a in arrays:  # wrapping 64-bit dot products of the bit patterns
+            h += a @ (rng.integers(1, 2 ** 63, size=a.shape[1], dtype=np.uint64) | np.uint64(1))
+    _, first, inv = np.unique(h, return_index=True, return_inverse=True)
+    inv = inv.reshape(-1)
+    rep_of = first[inv]
+    if not all(np.array_equal(a, a[rep_of]) for a in arrays):  # collision: exact fallback
+        rows = np.concatenate(arrays, axis=1)
+        key = rows.view(np.uint8).view(np.dtype((np.void, rows.shape[1] * 8))).reshape(n_leaf)
+        _, first, inv = np.unique(key, return_index=True, return_inverse=True)
+        inv = inv.reshape(-1)
     order = np.argsort(first, kind="stable")
     rank = np.empty_like(order)
     rank[order] = np.arange(order.size)
-    return first[order].astype(np.int64), rank[inv.reshape(-1)].astype(np.int64)
+    return first[order].astype(np.int64), rank[inv].astype(np.int64)
 
 
 class _DeviceLayout:
