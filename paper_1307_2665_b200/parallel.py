@@ -1,0 +1,399 @@
+"""Multi-GPU build and solve by quadtree subtrees. One process per GPU.
+
+With N = 2^s ranks, rank r owns the box at depth s, slot r (for N = 8: boxes 7..14, a 2 x 4
+split of the domain) and everything below it.
+
+* Build: each rank runs the leaf stage for its own leaves and every merge level below depth s,
+  with no communication. For the top s depths, the owner of a parent is the owner of its child a
+  (the left/bottom one). The owner of child b sends its DtN matrix with one point-to-point
+  `send`; the owner merges. The root DtN ends on rank 0. S of a top-depth box stays on its owner.
+* Solve: rank 0 holds the boundary batch. Top-down over the top depths, each owner applies its S
+  and sends the child-b boundary values u[I_e(child b)] to the owner of child b. Then every rank
+  runs its subtree solve independently. The output u stays sharded: rank r owns the
+  rows of its subtree (`DistState.owned_rows`). `gather_solution` assembles it on rank 0.
+
+The orchestration is backend-agnostic. `CudaBackend` drives libhps_b200.so on the rank's GPU,
+with NCCL as the transport. tests/test_distributed.py runs the same orchestration with a numpy
+backend over gloo, world_size 2 and 4, against the single-process oracle.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError
+from .grid import layout_of
+from .leafops import LeafGeometry
+
+__all__ = ["CudaBackend", "DistState", "prepare_distributed", "build_distributed", "solve_distributed",
+           "gather_solution", "subtree_plan", "TorchComm"]
+
+
+# ----------------------------------------------------------------------------------------------
+# Ownership plan (pure integer logic)
+# ----------------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class SubtreePlan:
+    L: int
+    world: int
+    s: int  # split depth
+
+    def owner(self, d, k):
+        """Rank owning box (depth d, slot k)."""
+        if d >= self.s:
+            return k >> (d - self.s)
+        return k << (self.s - d)
+
+    def local_slots(self, rank, d):
+        """[lo, hi) slots of depth d (d >= s) inside rank's subtree."""
+        w = 1 << (d - self.s)
+        return rank * w, (rank + 1) * w
+
+    def top_boxes(self, rank, d):
+        """Slots at a top depth d < s that `rank` owns (at most one)."""
+        k, rem = divmod(rank, 1 << (self.s - d))
+        return [k] if rem == 0 else []
+
+
+def subtree_plan(L, world):
+    s = int(round(math.log2(world))) if world > 0 else -1
+    if world < 1 or (1 << s) != world:
+        raise ConfigError(f"world size {world} is not a power of two")
+    if s > 2 * L:
+        raise ConfigError(f"world size {world} exceeds the number of leaves 4^{L}")
+    return SubtreePlan(L, world, s)
+
+
+# ----------------------------------------------------------------------------------------------
+# CUDA backend (one GPU per rank)
+# ----------------------------------------------------------------------------------------------
+class CudaBackend:
+    """Stage calls into libhps_b200.so for a subset of slots, on the current CUDA device."""
+
+    def __init__(self, tree, device=None):
+        import torch
+
+        from .solver import _DeviceLayout
+
+        _native.require_device()
+        self.torch = torch
+        self.lib = _native.load()
+        self.device = torch.device(device if device is not None else "cuda")
+        self.lay = layout_of(tree)
+        self.geom = LeafGeometry.get(self.lay.q, tree.leaf_width, tree.leaf_height)
+        self.dl = _DeviceLayout.get(self.lay, self.geom, self.device)
+
+    # -- tensors / transport --
+    def empty(self, shape):
+        return self.torch.empty(shape, dtype=self.torch.float64, device=self.device)
+
+    def from_numpy(self, a, dtype=None):
+        return self.torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    def upload(self, a):
+        return a if isinstance(a, self.torch.Tensor) else self.from_numpy(a)
+
+    def to_numpy(self, t):
+        return t.cpu().numpy()
+
+    # -- stages --
+    def leaf_stage(self, fields_local, scalars, ngroups):
+        lib, torch, q = self.lib, self.torch, self.lay.q
+        ni, nb, ng = (q - 2) ** 2, 4 * (q - 1), 4 * q
+        fptr = (ctypes.c_void_p * 6)()
+        scal = (ctypes.c_double * 6)()
+        keep = []
+        for f in range(6):
+            if fields_local[f] is None:
+                fptr[f] = None
+            else:
+                t = self.upload(fields_local[f])
+                keep.append(t)
+                fptr[f] = _native.ptr(t).value
+            scal[f] = scalars[f]
+        Psi = self.empty((ngroups, ni, nb))
+        T = self.empty((ngroups, ng, ng))
+        cond = self.empty((ngroups,))
+        wsb = lib.hps_leaf_workspace_bytes(q, ngroups)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        _native.check(lib.hps_leaf_stage(q, ngroups, fptr, scal, _native.ptr(self.dl.leaf_consts),
+                                         _native.ptr(self.dl.leaf_idx), self.dl.probe_max, _native.ptr(Psi),
+                                         _native.ptr(T), _native.ptr(cond), _native.ptr(ws), wsb,
+                                         _native.stream_ptr()), "hps_leaf_stage")
+        return Psi, T, cond
+
+    def merge_level(self, d, nbatch, child_T, child_idx, status):
+        lib, torch = self.lib, self.torch
+        dl = self.lay.depths[d]
+        S = self.empty((nbatch, dl.n3, dl.ne))
+        T = self.empty((nbatch, dl.ne, dl.ne))
+        wsb = lib.hps_merge_workspace_bytes(nbatch, dl.n3, dl.ne)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        idx = None if child_idx is None else self.torch.from_numpy(np.asarray(child_idx, np.int32)).to(self.device)
+        _native.check(lib.hps_merge_level(nbatch, dl.n3, dl.ne, dl.m, self.lay.q, _native.ptr(child_T),
+                                          dl.m * dl.m, _native.ptr(idx), _native.ptr(self.dl.maps[d]),
+                                          _native.ptr(self.dl.vmode[d]), _native.ptr(S), _native.ptr(T),
+                                          _native.ptr(ws), wsb, _native.ptr(status), 0, _native.stream_ptr()),
+                      f"hps_merge_level(depth {d})")
+        return S, T
+
+    def solve_level(self, d, slot0, nslots, S, u, nrhs):
+        dl = self.lay.depths[d]
+        ldu = u.shape[1]
+        Ie = self.dl.Ie[d][slot0:slot0 + nslots]
+        start = int(self.lay.depth_off[d]) + slot0 * dl.n3
+        _native.check(self.lib.hps_solve_level(nslots, dl.n3, dl.ne, _native.ptr(S), _native.ptr(Ie), start,
+                                               _native.ptr(u), ldu, nrhs, _native.stream_ptr()), "hps_solve_level")
+
+    def zeros(self, shape):
+        return self.torch.zeros(shape, dtype=self.torch.float64, device=self.device)
+
+    def stack2(self, a, b):
+        return self.torch.cat([a, b], dim=0).contiguous()
+
+    def status_word(self):
+        return self.torch.full((1,), -1, dtype=self.torch.int32, device=self.device)
+
+
+# ----------------------------------------------------------------------------------------------
+# Orchestration
+# ----------------------------------------------------------------------------------------------
+@dataclass
+class DistState:
+    plan: SubtreePlan
+    rank: int
+    layout: object
+    geom: object
+    backend: object
+    S_local: dict = field(default_factory=dict)   # depth -> S tensor for this rank's slots (d >= s)
+    S_top: dict = field(default_factory=dict)     # depth -> S of the single owned box (d < s)
+    subtree_T: object = None                       # DtN of this rank's depth-s box (before top merges)
+    root_T: object = None                          # rank 0 only
+    psi_groups: object = None
+    T_leaf_groups: object = None
+    leaf_group: np.ndarray = None                  # local leaf -> local group
+    cond: object = None
+    statuses: list = field(default_factory=list)
+
+    def owned_rows(self):
+        """Global node ids whose solution this rank computes (its subtree's I_i ranges)."""
+        lay, p = self.layout, self.plan
+        rows = []
+        for d in range(p.s, 2 * lay.L):
+            lo, hi = p.local_slots(self.rank, d)
+            n3 = lay.depths[d].n3
+            rows.append(np.arange(lay.depth_off[d] + lo * n3, lay.depth_off[d] + hi * n3))
+        for d in range(p.s):
+            for k in p.top_boxes(self.rank, d):
+                n3 = lay.depths[d].n3
+                rows.append(np.arange(lay.depth_off[d] + k * n3, lay.depth_off[d] + (k + 1) * n3))
+        return np.concatenate(rows) if rows else np.zeros(0, np.int64)
+
+
+def _sample_local(coeffs, lay, geom, leaf_lo, leaf_hi):
+    from .solver import COEFF_NAMES
+
+    lc = lay.leaf_cells[leaf_lo:leaf_hi]
+    xs = lay.xline[lc[:, 0]][:, None] + geom.grid_x[None, :]
+    ys = lay.yline[lc[:, 1]][:, None] + geom.grid_y[None, :]
+    fields = {}
+    for name in COEFF_NAMES:
+        f = getattr(coeffs, name)
+        v = f(xs, ys) if callable(f) else float(f)
+        if not np.all(np.isfinite(np.atleast_1d(v))):
+            bad = np.argwhere(~np.isfinite(np.broadcast_to(v, xs.shape)))
+            i, k = bad[0] if bad.size else (0, 0)
+            raise ValueError(f"coefficient {name} is not finite at node ({xs[i, k]}, {ys[i, k]})")
+        fields[name] = v if np.isscalar(v) else np.ascontiguousarray(np.broadcast_to(np.asarray(v, float), xs.shape))
+    return fields
+
+
+@dataclass
+class LocalInputs:
+    """This rank's sampled, grouped (and uploaded) leaf inputs."""
+
+    fields: list
+    scalars: list
+    reps: np.ndarray
+    gid: np.ndarray
+
+
+def prepare_distributed(tree, coeffs, rank, world, backend):
+    """Sample + group this rank's leaves and upload the group representatives (host work)."""
+    from .solver import COEFF_NAMES, _group
+
+    lay = layout_of(tree)
+    plan = subtree_plan(lay.L, world)
+    geom = LeafGeometry.get(lay.q, tree.leaf_width, tree.leaf_height)
+    lo, hi = plan.local_slots(rank, 2 * lay.L)
+    fields = _sample_local(coeffs, lay, geom, lo, hi)
+    reps, gid = _group(fields, hi - lo)
+    local_fields = [None if np.isscalar(fields[n]) else backend.upload(fields[n][reps]) for n in COEFF_NAMES]
+    scalars = [float(fields[n]) if np.isscalar(fields[n]) else 0.0 for n in COEFF_NAMES]
+    return LocalInputs(local_fields, scalars, reps, gid)
+
+
+def build_distributed(tree, coeffs, comm, backend, inputs=None):
+    """Subtree-parallel build. `comm` provides rank, world, send(tensor, dst), recv(tensor, src).
+    `inputs` (from prepare_distributed) skips the host sampling/grouping."""
+    lay = layout_of(tree)
+    L = lay.L
+    plan = subtree_plan(L, comm.world)
+    rank, s = comm.rank, plan.s
+    geom = LeafGeometry.get(lay.q, tree.leaf_width, tree.leaf_height)
+    st = DistState(plan=plan, rank=rank, layout=lay, geom=geom, backend=backend)
+    if inputs is None:
+        inputs = prepare_distributed(tree, coeffs, rank, comm.world, backend)
+    gid = inputs.gid
+    Psi, Tleaf, cond = backend.leaf_stage(inputs.fields, inputs.scalars, int(inputs.reps.size))
+    st.psi_groups, st.T_leaf_groups, st.leaf_group, st.cond = Psi, Tleaf, gid, cond
+
+    # ---- local merges, depths 2L-1 .. s ----
+    child_T, child_idx = Tleaf, gid
+    for d in range(2 * L - 1, s - 1, -1):
+        a, b = plan.local_slots(rank, d)
+        status = backend.status_word()
+        st.statuses.append((d, a, status))
+        S, T = backend.merge_level(d, b - a, child_T, child_idx, status)
+        st.S_local[d] = S
+        child_T, child_idx = T, None
+    if s == 2 * L:  # one leaf per rank
+        child_T = Tleaf[gid[0]:gid[0] + 1]
+    st.subtree_T = child_T  # (1, ne_s, ne_s)
+
+    # ---- top merges, depths s-1 .. 0: child b's owner sends its T to child a's owner ----
+    cur = child_T
+    for d in range(s - 1, -1, -1):
+        span = 1 << (s - d - 1)  # ranks per box at depth d+1
+        if rank % span:
+            continue  # this rank owns no box at depth d+1
+        kc = rank // span
+        if kc % 2 == 1:
+            comm.send(cur, plan.owner(d, kc // 2))
+            cur = None
+            continue
+        m = lay.depths[d].m
+        other = backend.empty((1, m, m))
+        comm.recv(other, plan.owner(d + 1, kc + 1))
+        status = backend.status_word()
+        st.statuses.append((d, kc // 2, status))
+        S, T = backend.merge_level(d, 1, backend.stack2(cur, other), None, status)
+        st.S_top[d] = S
+        cur = T
+    if rank == 0:
+        st.root_T = cur
+    return st
+
+
+def solve_distributed(st, F, comm):
+    """Subtree-parallel batched solve. F: (|Gamma|, b) on rank 0 (ignored elsewhere), in root.I_e
+    order. Returns this rank's u buffer (N x ldu); rows in st.owned_rows() plus the subtree's
+    boundary are valid."""
+    from .solver import rhs_ld
+
+    be, lay, plan, rank = st.backend, st.layout, st.plan, st.rank
+    L, s = lay.L, plan.s
+    b = int(F.shape[1]) if F is not None and len(F.shape) > 1 else 1
+    b = comm.bcast_int(b)
+    ldu = rhs_ld(b)
+    nrhs = b if b <= 8 else ldu
+    u = be.zeros((lay.N, ldu))
+    if rank == 0:
+        Fm = F if len(F.shape) > 1 else F[:, None]
+        be.scatter_rows(u, lay.root_I_e, Fm)
+    # top depths: owners apply S, then hand child-b boundary values to child b's owner
+    for d in range(s):
+        for k in plan.top_boxes(rank, d):
+            be.solve_level(d, k, 1, st.S_top[d], u, nrhs)
+            kb = 2 * k + 1
+            dst = plan.owner(d + 1, kb)
+            if dst != rank:
+                ids = lay.depths[d + 1].I_e[kb] if d + 1 < 2 * L else lay.leaf_I_e[kb]
+                comm.send(be.gather_rows(u, ids), dst)
+        # receive my subtree's (or my child-b box's) boundary values from the parent owner
+        if rank % (1 << (s - d - 1)) == 0 and (rank >> (s - d - 1)) % 2 == 1:
+            kb = rank >> (s - d - 1)
+            ids = lay.depths[d + 1].I_e[kb] if d + 1 < 2 * L else lay.leaf_I_e[kb]
+            buf = be.zeros((len(ids), ldu))
+            comm.recv(buf, plan.owner(d, kb // 2))
+            be.scatter_rows(u, ids, buf)
+    for d in range(s, 2 * L):
+        a, bb = plan.local_slots(rank, d)
+        be.solve_level(d, a, bb - a, st.S_local[d], u, nrhs)
+    return u
+
+
+def gather_solution(st, u, comm, b):
+    """Assemble the full (N, b) solution on rank 0 from the sharded buffers (others get None)."""
+    be = st.backend
+    rows = st.owned_rows()
+    mine = be.gather_rows(u, rows)
+    if comm.rank != 0:
+        comm.send_obj(rows, 0)
+        comm.send(mine, 0)
+        return None
+    out = be.zeros(u.shape)
+    be.scatter_rows(out, st.layout.root_I_e, be.gather_rows(u, st.layout.root_I_e))
+    be.scatter_rows(out, rows, mine)
+    for src in range(1, comm.world):
+        r = comm.recv_obj(src)
+        buf = be.zeros((len(r), u.shape[1]))
+        comm.recv(buf, src)
+        be.scatter_rows(out, r, buf)
+    return be.to_numpy(out)[:, :b]
+
+
+class TorchComm:
+    """torch.distributed transport (NCCL for device tensors, gloo for host tensors)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def send(self, t, dst):
+        self.dist.send(t.contiguous(), dst, group=self.group)
+
+    def recv(self, t, src):
+        self.dist.recv(t, src, group=self.group)
+
+    def bcast_int(self, v):
+        obj = [v]
+        self.dist.broadcast_object_list(obj, src=0, group=self.group)
+        return int(obj[0])
+
+    def send_obj(self, o, dst):
+        self.dist.send_object_list([o], dst, group=self.group)
+
+    def recv_obj(self, src):
+        obj = [None]
+        self.dist.recv_object_list(obj, src, group=self.group)
+        return obj[0]
+
+
+def _cuda_backend_extras():
+    """Row gather/scatter helpers on torch tensors (shared by the CUDA backend)."""
+
+    def gather_rows(self, u, ids):
+        idx = self.torch.as_tensor(np.asarray(ids, np.int64), device=u.device)
+        return u.index_select(0, idx).contiguous()
+
+    def scatter_rows(self, u, ids, vals):
+        idx = self.torch.as_tensor(np.asarray(ids, np.int64), device=u.device)
+        v = vals if hasattr(vals, "to") else self.torch.from_numpy(np.ascontiguousarray(vals))
+        v = v.to(u.device, self.torch.float64)
+        u[:, :v.shape[1]].index_copy_(0, idx, v)
+
+    CudaBackend.gather_rows = gather_rows
+    CudaBackend.scatter_rows = scatter_rows
+
+
+_cuda_backend_extras()

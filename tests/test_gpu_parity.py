@@ -191,3 +191,32 @@ def test_state_api_against_oracle():
     want = ost.root_T.size + st.n_leaf_groups * ni * nb + st.geometry.L1.size + st.geometry.L4.size + S_entries
     assert rep["total_entries"] == want
     assert st.S[0].dense.shape == ost.S[0].shape and len(st.psi) == 16
+
+
+def test_distributed_path_single_rank_cuda_backend():
+    """parallel.py with the CUDA backend at world size 1 (the exchange itself is covered by the
+    gloo tests in test_distributed.py) equals the single-process build."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1307_2665_b200 import parallel
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        tree, nodes, st = gpu_build(2, 3)
+        be = parallel.CudaBackend(tree)
+        comm = parallel.TorchComm()
+        ds = parallel.build_distributed(tree, problems.coefficients(2), comm, be)
+        assert rel(ds.root_T[0].cpu().numpy(), st.root_T.dense) < 1e-13
+        F = torch.from_numpy(problems.boundary_data(2, nodes.points[tree.root.I_e], seed=2, batch=5)).cuda()
+        u = parallel.solve_distributed(ds, F, comm)
+        full = parallel.gather_solution(ds, u, comm, 5)
+        assert rel(full, solver.solve(st, F.cpu().numpy())) < 1e-13
+    finally:
+        dist.destroy_process_group()
