@@ -341,7 +341,7 @@ def bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, w
     import torch.distributed as dist
 
     import paper_1307_2665_b200 as P
-    from paper_1307_2665_b200 import _native, parallel
+    from paper_1307_2665_b200 import _native, parallel, problems
 
     dev = torch.device("cuda")
     lib = _native.load()

@@ -678,11 +678,41 @@ extern "C" int hps_leaf_stage(int p, int ngroups, const double* const* fields, c
       HPS_CUDA_CHECK(cudaFuncSetAttribute(k_leaf16<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l16::SMEM));
       attr = true;
     }
+    // Keep as much of the per-CTA scratch in L2 as the persisting carve-out allows: the scratch is
+    // re-read and re-written by every panel, everything else is touched once.
+    static int persist = getenv("HPS_LEAF_L2PERSIST") ? atoi(getenv("HPS_LEAF_L2PERSIST")) : 1;
+    const size_t scratch = (size_t)leaf16_grid(ngroups) * a.scratch_stride * sizeof(double);
+    bool windowed = false;
+    if (persist) {
+      int dev = 0, maxp = 0, maxw = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+      if (maxp > 0 && maxw > 0) {
+        const size_t win = std::min(scratch, (size_t)maxw);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)maxp, win));
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.base_ptr = ws;
+        v.accessPolicyWindow.num_bytes = win;
+        v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        windowed = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+        cudaGetLastError();
+      }
+    }
     if (leaf16_threads() == 512)
       k_leaf16<512><<<leaf16_grid(ngroups), 512, l16::SMEM, st>>>(a);
     else
       k_leaf16<256><<<leaf16_grid(ngroups), 256, l16::SMEM, st>>>(a);
     HPS_LAUNCH_CHECK();
+    if (windowed) {
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.num_bytes = 0;
+      cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+      cudaCtxResetPersistingL2Cache();
+      cudaGetLastError();
+    }
     return HPS_OK;
   }
   a.scratch_stride = (long long)ni * (ni + nb + 2);
