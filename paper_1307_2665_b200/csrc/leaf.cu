@@ -680,7 +680,7 @@ extern "C" int hps_leaf_stage(int p, int ngroups, const double* const* fields, c
     }
     // Keep as much of the per-CTA scratch in L2 as the persisting carve-out allows: the scratch is
     // re-read and re-written by every panel, everything else is touched once.
-    static int persist = getenv("HPS_LEAF_L2PERSIST") ? atoi(getenv("HPS_LEAF_L2PERSIST")) : 1;
+    static int persist = getenv("HPS_LEAF_L2PERSIST") ? atoi(getenv("HPS_LEAF_L2PERSIST")) : 0;  // measured: no gain
     const size_t scratch = (size_t)leaf16_grid(ngroups) * a.scratch_stride * sizeof(double);
     bool windowed = false;
     if (persist) {
