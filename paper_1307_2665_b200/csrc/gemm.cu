@@ -1,4 +1,6 @@
 // Host launcher for the DMMA GEMM (tile selection) + the C-ABI test hook.
+#include <algorithm>
+
 #include "gemm.cuh"
 
 namespace hps {
@@ -29,6 +31,20 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
     return HPS_ERR_ARG;
   }
   if (p.K == 0) return HPS_OK;
+  if (p.batch > 65535) {  // gridDim.z limit: launch in batch chunks
+    for (int b0 = 0; b0 < p.batch; b0 += 65535) {
+      GemmParams q = p;
+      q.batch = std::min(65535, p.batch - b0);
+      q.A += (long long)b0 * p.strideA;
+      q.B += (long long)b0 * p.strideB;
+      q.C += (long long)b0 * p.strideC;
+      if (q.Bidx) q.Bidx += (long long)b0 * p.strideBidx;
+      q.batch_offset = p.batch_offset + b0;
+      int st = dgemm_launch(q, stream);
+      if (st != HPS_OK) return st;
+    }
+    return HPS_OK;
+  }
   double tiles128 = double((p.M + 127) / 128) * double((p.N + 127) / 128) * p.batch;
   if (p.M >= 128 && p.N >= 128 && tiles128 >= 148.0) return launch_cfg<128, 128, 16, 2, 4, 4>(p, stream);
   return launch_cfg<64, 64, 16, 2, 2, 3>(p, stream);

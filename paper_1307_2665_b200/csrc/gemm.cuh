@@ -22,6 +22,7 @@ struct GemmParams {
   double* C; long long ldc, strideC;
   double alpha, beta;
   int* nonfinite;  // optional: set to max batch index with a non-finite output
+  int batch_offset = 0;  // added to the reported batch index (batch-chunked launches)
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
@@ -146,7 +147,7 @@ dgemm_dmma_kernel(GemmParams p) {
       *reinterpret_cast<double2*>(dst) = v;
     }
   }
-  if (p.nonfinite && bad) atomicMax(p.nonfinite, b);
+  if (p.nonfinite && bad) atomicMax(p.nonfinite, b + p.batch_offset);
 }
 
 // Launch with a tile shape picked from the problem size. Returns HPS_OK or an error code.
