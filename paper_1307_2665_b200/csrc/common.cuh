@@ -59,6 +59,16 @@ __device__ __forceinline__ void sts64(double* p, double v) {
   asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(smem_u32(p)), "d"(v) : "memory");
 }
 
+// Reciprocal for pivots: MUFU approximation + 2 Newton steps (error ~1 ulp). About 60 cycles,
+// against ~230 for the IEEE division sequence, which sits on every pivot step's critical path.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_leaf16(LeafArgs a) {
           __syncthreads();
           if (act) {
             const double* pr = sProw + (j & 1) * 16;  // double-buffered: no barrier after the update
-            const double l = work[j] / pr[j];
+            const double l = work[j] * fast_rcp(pr[j]);
             work[j] = l;
 #pragma unroll
             for (int c = j + 1; c < 16; ++c) work[c] = fma(-l, pr[c], work[c]);

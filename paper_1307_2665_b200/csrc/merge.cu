@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(W * 32) k_gj_inverse(double* X, long long lda,
     const int pl = p & 31, pi = p >> 5;
     const double piv = ck[p];
     singular |= (piv == 0.0);
-    const double inv = 1.0 / piv;
+    const double inv = fast_rcp(piv);
     if (threadIdx.x == 0) { pivrow[k] = p; rowstep[p] = k; }
     // pivot row for this warp's columns (pi is warp-uniform: a uniform branch, no selects)
     double rp[CPW];
