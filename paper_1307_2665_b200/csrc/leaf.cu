@@ -14,27 +14,14 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "leaf.cuh"
 
 namespace hps {
 
 constexpr int LEAF_NB = 16;
 constexpr int LEAF_THREADS = 256;
 
-struct LeafArgs {
-  int p, ngroups;
-  // coefficient samples, rows = group representatives (ngroups x p^2); null => scalar
-  const double* field[6];
-  double scalar[6];
-  int present[6];  // 0 => scalar zero, term skipped (leafops.py:220-221)
-  const double* consts;  // Dx, Dy, Dxx, Dyy, L43e, L43i, L1, probe
-  const int* idx;        // J_i, J_e
-  double probe_max;
-  double* Psi;   // ngroups x ni x nb
-  double* T;     // ngroups x 4p x 4p
-  double* cond;  // ngroups
-  double* scratch;
-  long long scratch_stride;  // doubles per CTA slot
-};
+
 
 __global__ void __launch_bounds__(LEAF_THREADS) k_leaf(LeafArgs a) {
   extern __shared__ __align__(16) double sm[];
@@ -639,7 +626,9 @@ extern "C" int hps_debug_leaf_profile(long long* out, int reset) {
 #endif
 
 extern "C" size_t hps_leaf_workspace_bytes(int p, int ngroups) {
-  if (p == 16) return sizeof(double) * (size_t)leaf16_grid(ngroups) * l16::MROWS * l16::LDM + 256;
+  if (p == 16)
+    return sizeof(double) * std::max((size_t)leaf16_grid(ngroups) * l16::MROWS * l16::LDM,
+                                     (size_t)leaf16v3_grid(ngroups) * leaf16v3_scratch_doubles()) + 256;
   const int ni = (p - 2) * (p - 2), nb = 4 * (p - 1);
   const long long ldm = ni + nb + 2;
   return sizeof(double) * (size_t)leaf_grid(ngroups) * ni * ldm + 256;
@@ -670,6 +659,8 @@ extern "C" int hps_leaf_stage(int p, int ngroups, const double* const* fields, c
   a.cond = cond;
   const int ni = (p - 2) * (p - 2), nb = 4 * (p - 1);
   a.scratch = static_cast<double*>(ws);
+  static const int leaf_v = getenv("HPS_LEAF_V") ? atoi(getenv("HPS_LEAF_V")) : 3;
+  if (p == 16 && !getenv("HPS_LEAF_GENERIC") && leaf_v == 3) return launch_leaf16v3(a, st);
   if (p == 16 && !getenv("HPS_LEAF_GENERIC")) {
     a.scratch_stride = (long long)l16::MROWS * l16::LDM;
     static bool attr = false;

@@ -1,0 +1,550 @@
+// Leaf stage, p = 16, v3: right-looking blocked LU with implicit partial pivoting and look-ahead.
+// Reference math: leafops.py:217-302, solver.py:226-246. Same outputs as the v2/generic kernels:
+// Psi = -A_ii^{-1} A_ie, the probe condition estimate, and T = (L43e + L43i Psi) L1.
+//
+// One CTA per coefficient group, 2 CTAs per SM, 8 warps in two roles:
+//   * panel warps 0-3 own physical rows (thread t: rows t and t+128) and factor a 16-column panel
+//     in registers. Partial pivoting: a REDUX argmax over the active rows. No row swaps: a pivot
+//     row just leaves the active set.
+//   * update warps 4-7 apply the rank-16 update of the previous panel on DMMA, over the compact
+//     list of still-active rows only. They update the next panel's columns first, then signal
+//     the panel warps through a named barrier, so factor(k+1) overlaps update(k) on the
+//     remaining columns.
+// After the last panel, a blocked back substitution (DMMA off-diagonal blocks) yields
+// X = U^{-1} Y in place of Y in the pivot rows. The augmented matrix lives in a per-CTA global
+// scratch slot (200 x 260 fp64, L2-resident).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "leaf.cuh"
+
+namespace hps {
+#ifdef HPS_LEAF_PROFILE
+__device__ long long g_leaf3_prof[1024][16];
+#define P3_T(v) long long v = clock64()
+#define P3_ADD(slot, t0, who) do { if ((who)) atomicAdd((unsigned long long*)&g_leaf3_prof[blockIdx.x][slot], (unsigned long long)(clock64() - (t0))); } while (0)
+#else
+#define P3_T(v)
+#define P3_ADD(slot, t0, who)
+#endif
+namespace l3 {
+constexpr int NI = 196, NB = 60, NG = 64, NCOLS = 257, LDM = 260, MROWS = 200;
+constexpr int NRHS = LDM - NI;  // 64 (61 used)
+constexpr int THREADS = 256;
+constexpr int NPW = 4;  // panel warps
+constexpr int SA = 20;  // multiplier row stride (== 4 mod 16)
+constexpr int SB = 264; // U12 row stride (== 8 mod 16)
+constexpr int ST1 = 68;
+constexpr int NPANEL = (NI + 15) / 16;  // 13
+constexpr int OFF_A16 = 0;                         // 2 x MROWS x SA
+constexpr int OFF_U12 = OFF_A16 + 2 * MROWS * SA;  // 16 x SB
+constexpr int OFF_LU = OFF_U12 + 16 * SB;          // 16 x 17
+constexpr int OFF_PROW = OFF_LU + 16 * 17;         // 2 x 16
+constexpr int NDBL = OFF_PROW + 32;
+constexpr int NINT = 2 * MROWS + NI + NI + NB + 64;
+constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4 + 64;
+constexpr int BAR_PANEL = 1;      // panel warps only (128 threads)
+constexpr int BAR_LOOKAHEAD = 2;  // update warps arrive, panel warps sync (256 threads)
+}  // namespace l3
+
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
+  using namespace l3;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ unsigned long long s_key[NPW];
+  __shared__ int s_idx[NPW];
+  __shared__ int s_cnt[2 * NPW];
+  __shared__ int s_nact[2];
+  __shared__ int s_sing;
+  __shared__ double s_red[8];
+  double* sA16 = sm + OFF_A16;
+  double* sU12 = sm + OFF_U12;
+  double* sLU = sm + OFF_LU;
+  double* sProw = sm + OFF_PROW;
+  int* ib = reinterpret_cast<int*>(sm + NDBL);
+  int* sAct = ib;               // 2 x MROWS
+  int* sPiv = sAct + 2 * MROWS; // NI: physical row eliminated at step k
+  int* Ji = sPiv + NI;
+  int* Je = Ji + NI;
+  // assembly-phase aliases
+  double* coef = sA16;          // 6 x 256
+  double* Dx = coef + 6 * 256;  // Dx, Dy, Dxx, Dyy
+  double* Dy = Dx + 256;
+  double* Dxx = Dy + 256;
+  double* Dyy = Dxx + 256;
+  int* colmap = sAct;           // node -> M column (256)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const bool pwarp = warp < NPW;
+  const double* cL43e = a.consts + 4 * 256;
+  const double* cL43i = cL43e + NG * NB;
+  const double* cL1 = cL43i + NG * NI;
+  const double* cprobe = cL1 + NB * NG;
+  for (int i = tid; i < NI; i += THREADS) Ji[i] = a.idx[i];
+  for (int i = tid; i < NB; i += THREADS) Je[i] = a.idx[NI + i];
+  double* M = a.scratch + (long long)blockIdx.x * a.scratch_stride;
+
+  for (int grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
+    __syncthreads();
+    // ================= assembly (leafops.py:217-233, same per-entry op order) =================
+    P3_T(t_asm);
+    for (int i = tid; i < 4 * 256; i += THREADS) Dx[i] = a.consts[i];
+    for (int f = 0; f < 6; ++f) {
+      const double* src = a.field[f] ? a.field[f] + (long long)grp * 256 : nullptr;
+      for (int i = tid; i < 256; i += THREADS) coef[f * 256 + i] = src ? src[i] : a.scalar[f];
+    }
+    for (int i = tid; i < 256; i += THREADS) colmap[i] = -1;
+    if (tid == 0) s_sing = 0;
+    __syncthreads();
+    for (int i = tid; i < NI; i += THREADS) colmap[Ji[i]] = i;
+    for (int i = tid; i < NB; i += THREADS) colmap[Je[i]] = NI + i;
+    // zero-fill M (vectorised), probe column
+    for (int e = tid; e < MROWS * LDM / 2; e += THREADS)
+      reinterpret_cast<double2*>(M)[e] = make_double2(0.0, 0.0);
+    __syncthreads();
+    const bool dense = a.present[1] != 0;  // c12 != 0 couples every (i', j'): dense rows
+    double rowmax = 0.0;
+    for (int r = warp; r < NI; r += THREADS / 32) {
+      double* Mr = M + (long long)r * LDM;
+      const int na = Ji[r], ia = na >> 4, ja = na & 15;
+      double rs = 0.0;
+      auto entry = [&](int ib_, int jb_) {
+        double acc = 0.0;
+        if (a.present[0] && ja == jb_) acc += coef[0 * 256 + na] * (-Dxx[ia * 16 + ib_]);
+        if (a.present[1]) acc += coef[1 * 256 + na] * (-2.0 * (Dx[ia * 16 + ib_] * Dy[ja * 16 + jb_]));
+        if (a.present[2] && ia == ib_) acc += coef[2 * 256 + na] * (-Dyy[ja * 16 + jb_]);
+        if (a.present[3] && ja == jb_) acc += coef[3 * 256 + na] * Dx[ia * 16 + ib_];
+        if (a.present[4] && ia == ib_) acc += coef[4 * 256 + na] * Dy[ja * 16 + jb_];
+        if (ib_ == ia && jb_ == ja) acc += coef[5 * 256 + na];
+        return acc;
+      };
+      if (dense) {
+        for (int c = lane; c < NCOLS - 1; c += 32) {
+          const int nbn = c < NI ? Ji[c] : Je[c - NI];
+          const double v = entry(nbn >> 4, nbn & 15);
+          Mr[c] = v;
+          if (c < NI) rs += fabs(v);
+        }
+      } else {
+        // nonzeros only: the grid row (ib, ja) and the grid column (ia, jb) through node (ia, ja)
+        const int which = lane >> 4, t = lane & 15;  // lanes 0-15: vary ib; 16-31: vary jb (skip the diagonal)
+        const int ib_ = which == 0 ? t : ia, jb_ = which == 0 ? ja : t;
+        if (!(which == 1 && t == ja)) {
+          const int col = colmap[ib_ * 16 + jb_];
+          const double v = entry(ib_, jb_);
+          Mr[col] = v;
+          if (col < NI) rs += fabs(v);
+        }
+      }
+      if (lane == 0) Mr[NCOLS - 1] = cprobe[r];
+      rs = warp_sum(rs);
+      rowmax = fmax(rowmax, rs);
+    }
+    rowmax = warp_max(rowmax);
+    if (lane == 0) s_red[warp] = rowmax;
+    __syncthreads();
+    double anorm = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) anorm = fmax(anorm, s_red[w]);
+
+    // ================= blocked LU with look-ahead =================
+    // panel-warp state: rows r0 = tid, r1 = tid + 128
+    const int r0 = tid, r1 = tid + 128;
+    bool act0 = pwarp && r0 < NI, act1 = pwarp && r1 < NI;
+    int step0 = -1, step1 = -1;
+
+    auto factor = [&](int k) {  // panel warps only
+      const int k0 = 16 * k, kb = min(16, NI - k0);
+      double w0[16], w1[16];
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
+        if (act0 && j < kb) v0 = *reinterpret_cast<const double2*>(M + (long long)r0 * LDM + k0 + j);
+        if (act1 && j < kb) v1 = *reinterpret_cast<const double2*>(M + (long long)r1 * LDM + k0 + j);
+        w0[j] = v0.x; w0[j + 1] = (j + 1 < kb) ? v0.y : 0.0;
+        w1[j] = v1.x; w1[j + 1] = (j + 1 < kb) ? v1.y : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < kb) {
+          const unsigned long long k0key = act0 ? (unsigned long long)__double_as_longlong(fabs(w0[j])) : 0ull;
+          const unsigned long long k1key = act1 ? (unsigned long long)__double_as_longlong(fabs(w1[j])) : 0ull;
+          unsigned long long key = k0key;
+          int idx = act0 ? r0 : 0x7fffffff;
+          if (act1 && (k1key > key || (k1key == key && r1 < idx))) { key = k1key; idx = r1; }
+          const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+          const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+          const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+          const int wi = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)idx : 0xffffffffu);
+          if (lane == 0) {
+            s_key[warp] = ((unsigned long long)mhi << 32) | mlo;
+            s_idx[warp] = wi;
+          }
+          bar_sync(BAR_PANEL, NPW * 32);
+          unsigned long long bk = s_key[0];
+          int p = s_idx[0];
+#pragma unroll
+          for (int w = 1; w < NPW; ++w) {
+            const unsigned long long kk = s_key[w];
+            const int ii = s_idx[w];
+            if (kk > bk || (kk == bk && ii < p)) { bk = kk; p = ii; }
+          }
+          double* pr = sProw + (j & 1) * 16;
+          if (r0 == p) {
+            act0 = false; step0 = k0 + j;
+            if (w0[j] == 0.0) s_sing = 1;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) sts64(pr + c, w0[c]);
+          }
+          if (r1 == p) {
+            act1 = false; step1 = k0 + j;
+            if (w1[j] == 0.0) s_sing = 1;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) sts64(pr + c, w1[c]);
+          }
+          if (tid == 0) sPiv[k0 + j] = p;
+          bar_sync(BAR_PANEL, NPW * 32);
+          const double inv = fast_rcp(pr[j]);
+          if (act0) {
+            const double l = w0[j] * inv;
+            w0[j] = l;
+#pragma unroll
+            for (int c = j + 1; c < 16; ++c) w0[c] = fma(-l, pr[c], w0[c]);
+          }
+          if (act1) {
+            const double l = w1[j] * inv;
+            w1[j] = l;
+#pragma unroll
+            for (int c = j + 1; c < 16; ++c) w1[c] = fma(-l, pr[c], w1[c]);
+          }
+        }
+      }
+      // pivot rows of this panel: LU11 rows to smem, U part into M
+      if (step0 >= k0 && step0 < k0 + kb) {
+        const int rr = step0 - k0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) sts64(sLU + rr * 17 + c, w0[c]);
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c >= rr && c < kb) M[(long long)r0 * LDM + k0 + c] = w0[c];
+      }
+      if (step1 >= k0 && step1 < k0 + kb) {
+        const int rr = step1 - k0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) sts64(sLU + rr * 17 + c, w1[c]);
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c >= rr && c < kb) M[(long long)r1 * LDM + k0 + c] = w1[c];
+      }
+      // compact list of rows still active, with their (negated) multipliers for the update
+      const unsigned b0 = __ballot_sync(0xffffffffu, act0), b1 = __ballot_sync(0xffffffffu, act1);
+      if (lane == 0) { s_cnt[warp] = __popc(b0); s_cnt[NPW + warp] = __popc(b1); }
+      bar_sync(BAR_PANEL, NPW * 32);
+      int off0 = 0, off1 = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < NPW; ++w) {
+        if (w < warp) { off0 += s_cnt[w]; off1 += s_cnt[NPW + w]; }
+        tot += s_cnt[w];
+      }
+      off1 += tot;
+#pragma unroll
+      for (int w = 0; w < NPW; ++w) tot += s_cnt[NPW + w];
+      const unsigned lt = (1u << lane) - 1u;
+      const int buf = k & 1;
+      int* act = sAct + buf * MROWS;
+      double* A16 = sA16 + buf * MROWS * SA;
+      if (act0) {
+        const int i = off0 + __popc(b0 & lt);
+        act[i] = r0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sts64(A16 + i * SA + j, j < kb ? -w0[j] : 0.0);
+      }
+      if (act1) {
+        const int i = off1 + __popc(b1 & lt);
+        act[i] = r1;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sts64(A16 + i * SA + j, j < kb ? -w1[j] : 0.0);
+      }
+      if (tid == 0) s_nact[buf] = tot;
+    };
+
+    // rank-kb update of M[act rows][c0 + [cbeg, cend)] by the update warps (uw = 0..3). Work item:
+    // 8 rows x CW columns whose C loads are all issued before the DMMAs (one L2 round trip).
+    auto update = [&](int k, int cbeg, int cend, int uw) {
+      constexpr int CW = 128, NJ = CW / 8;
+      const int k0 = 16 * k, kb = min(16, NI - k0), c0 = k0 + kb, nT = LDM - c0;
+      const int buf = k & 1;
+      const int nact = s_nact[buf];
+      const int* act = sAct + buf * MROWS;
+      const double* A16 = sA16 + buf * MROWS * SA;
+      const int nrt = (nact + 7) >> 3;
+      const int ncw = (cend - cbeg + CW - 1) / CW;
+      const int lim = min(cend, nT);
+      for (int it = uw; it < nrt * ncw; it += 4) {
+        const int rt = it / ncw, cb = cbeg + (it - rt * ncw) * CW;
+        const int ri = rt * 8 + g;
+        const bool rv = ri < nact;
+        const int row = rv ? act[ri] : 0;
+        double af[4];
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) af[ks] = rv ? A16[ri * SA + 4 * ks + tq] : 0.0;
+        double* Mr = M + (long long)row * LDM + c0;
+        double acc[NJ][2];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int col = cb + 8 * j + 2 * tq;
+          if (rv && col < lim) {
+            const double2 v = *reinterpret_cast<const double2*>(Mr + col);
+            acc[j][0] = v.x;
+            acc[j][1] = v.y;
+          } else {
+            acc[j][0] = acc[j][1] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          if (4 * ks < kb) {
+            const double* Ur = sU12 + (4 * ks + tq) * SB + cb + g;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+              if (cb + 8 * j < lim) dmma_8x8x4(acc[j][0], acc[j][1], af[ks], Ur[8 * j]);
+          }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int col = cb + 8 * j + 2 * tq;
+          if (rv && col < lim) *reinterpret_cast<double2*>(Mr + col) = make_double2(acc[j][0], acc[j][1]);
+        }
+      }
+    };
+
+    P3_ADD(0, t_asm, tid == 0);
+    P3_T(t_f0);
+    if (pwarp) factor(0);
+    __syncthreads();
+    P3_ADD(1, t_f0, tid == 0);
+    for (int k = 0; k < NPANEL; ++k) {
+      P3_T(t_u12);
+      const int k0 = 16 * k, kb = min(16, NI - k0), c0 = k0 + kb, nT = LDM - c0;
+      // U12 = L11^{-1} M[P_k, c0:] (one trailing column per thread)
+      for (int cc = tid; cc < 256; cc += THREADS) {
+        double y[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          y[r] = (r < kb && cc < nT) ? M[(long long)sPiv[k0 + r] * LDM + c0 + cc] : 0.0;
+#pragma unroll
+        for (int r = 1; r < 16; ++r)
+          if (r < kb)
+#pragma unroll
+            for (int b = 0; b < r; ++b) y[r] = fma(-sLU[r * 17 + b], y[b], y[r]);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) sts64(sU12 + r * SB + cc, y[r]);
+        if (cc < nT)
+#pragma unroll
+          for (int r = 0; r < 16; ++r)
+            if (r < kb) M[(long long)sPiv[k0 + r] * LDM + c0 + cc] = y[r];
+      }
+      __syncthreads();
+      P3_ADD(2, t_u12, tid == 0);
+      P3_T(t_main);
+      const bool ahead = k + 1 < NPANEL;
+      if (!pwarp) {
+        const int uw = warp - NPW;
+        const int la = ahead ? min(16, nT) : 0;  // next panel's columns first
+        if (ahead) {
+          update(k, 0, la, uw);
+          __threadfence_block();
+          bar_arrive(BAR_LOOKAHEAD, THREADS);
+        }
+        P3_ADD(3, t_main, tid == 128);
+        update(k, la, nT, uw);
+        P3_ADD(4, t_main, tid == 128);
+      } else if (ahead) {
+        bar_sync(BAR_LOOKAHEAD, THREADS);
+        P3_ADD(5, t_main, tid == 0);
+        factor(k + 1);
+        P3_ADD(6, t_main, tid == 0);
+      }
+      __syncthreads();
+      P3_ADD(7, t_main, tid == 0);
+    }
+    P3_T(t_bs);
+
+    // ================= back substitution (right-looking), fused with T1 = L43i Psi =================
+    // For block kp from the last: X_blk = U11^{-1} Y[P_kp] (one RHS column per thread, into smem),
+    // Psi rows out, T1 += L43i[:, blk] (-X_blk) (each warp: 8 rows x 64 columns in registers), then
+    // Y[P_j] -= U[P_j, blk] X_blk for all earlier pivot rows (DMMA, 8-row items, parallel loads).
+    double* sX = sA16;                 // 16 x 66 : X block (B operand, SB-like padded stride)
+    constexpr int SX = 72;             // == 8 mod 16
+    double* Psi = a.Psi + (long long)grp * NI * NB;
+    double t1acc[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t1acc[j][0] = t1acc[j][1] = 0.0;
+    double pm = 0.0;
+    double* sY = sA16 + 16 * SX;  // 16 x SX: Y rows of the block
+    double* sU = sY + 16 * SX;    // 16 x 17: U11 of the block
+    for (int kp = NPANEL - 1; kp >= 0; --kp) {
+      const int k0 = 16 * kp, kb = min(16, NI - k0);
+      // stage Y[P_kp] (16 x 64) and U11 (16 x 16) with one round of parallel loads
+      for (int e = tid; e < 16 * (NRHS + 16); e += THREADS) {
+        const int r = e / (NRHS + 16), c = e - r * (NRHS + 16);
+        const double* Urow = M + (long long)sPiv[k0 + (r < kb ? r : 0)] * LDM;
+        if (c < NRHS) sY[r * SX + c] = r < kb ? Urow[NI + c] : 0.0;
+        else sU[r * 17 + (c - NRHS)] = (r < kb && c - NRHS < kb) ? Urow[k0 + c - NRHS] : 0.0;
+      }
+      __syncthreads();
+      if (tid < NRHS) {
+        double x[16];
+#pragma unroll
+        for (int r = 15; r >= 0; --r) {
+          if (r < kb) {
+            double v = sY[r * SX + tid];
+#pragma unroll
+            for (int b = r + 1; b < 16; ++b)
+              if (b < kb) v = fma(-sU[r * 17 + b], x[b], v);
+            x[r] = v * fast_rcp(sU[r * 17 + r]);
+          } else {
+            x[r] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) sts64(sX + r * SX + tid, x[r]);
+        if (tid < NB) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r)
+            if (r < kb) __stcs(Psi + (long long)(k0 + r) * NB + tid, -x[r]);
+        } else if (tid == NB) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r)
+            if (r < kb) pm = fmax(pm, fabs(x[r]));
+        }
+      }
+      __syncthreads();
+      {  // T1 += L43i[:, k0:k0+kb] * (-X_blk): warp rows 8w..8w+7, all 64 columns
+        const double* Arow = cL43i + (long long)(warp * 8 + g) * NI + k0;
+        for (int ks = 0; ks < kb; ks += 4) {
+          const double af = -__ldg(Arow + ks + tq);
+          const double* Xr = sX + (ks + tq) * SX + g;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dmma_8x8x4(t1acc[j][0], t1acc[j][1], af, Xr[8 * j]);
+        }
+      }
+      // Y[P_j] -= U[P_j, k0:k0+kb] X_blk for steps j < k0 (rows sPiv[0..k0))
+      const int nrt = (k0 + 7) >> 3;
+      for (int it = warp; it < nrt; it += THREADS / 32) {
+        const int ri = it * 8 + g;
+        const bool rv = ri < k0;
+        const double* Urow = M + (long long)(rv ? sPiv[ri] : 0) * LDM;
+        double af[4];
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) af[ks] = (rv && 4 * ks < kb) ? -Urow[k0 + 4 * ks + tq] : 0.0;
+        double acc[8][2];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (rv) {
+            const double2 v = *reinterpret_cast<const double2*>(Urow + NI + 8 * j + 2 * tq);
+            acc[j][0] = v.x;
+            acc[j][1] = v.y;
+          } else {
+            acc[j][0] = acc[j][1] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          if (4 * ks < kb) {
+            const double* Xr = sX + (4 * ks + tq) * SX + g;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], af[ks], Xr[8 * j]);
+          }
+        if (rv) {
+          double* Yr = const_cast<double*>(Urow) + NI;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<double2*>(Yr + 8 * j + 2 * tq) = make_double2(acc[j][0], acc[j][1]);
+        }
+      }
+      __syncthreads();
+    }
+    P3_ADD(8, t_bs, tid == 0);
+    P3_T(t_ep);
+    // probe condition estimate (leafops.py:293-294)
+    pm = warp_max(pm);
+    if (lane == 0) s_red[warp] = pm;
+    __syncthreads();
+    if (tid == 0) {
+      double mx = 0.0;
+      for (int w = 0; w < 8; ++w) mx = fmax(mx, s_red[w]);
+      const double cnd = anorm * mx / a.probe_max;
+      a.cond[grp] = (s_sing || !isfinite(cnd)) ? INFINITY : cnd;
+    }
+    // T1 (+ L43e) -> smem, then T = T1 L1
+    double* sT1 = sU12;  // 64 x ST1
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int col = 8 * j + 2 * tq;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = col + h;
+        sT1[(warp * 8 + g) * ST1 + cc] = cc < NB ? __ldg(cL43e + (warp * 8 + g) * NB + cc) + t1acc[j][h] : 0.0;
+      }
+    }
+    __syncthreads();
+    {
+      const int rr0 = warp * 8;
+      double acc[8][2];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+      for (int ks = 0; ks < NB; ks += 4) {
+        const double af = sT1[(rr0 + g) * ST1 + ks + tq];
+        const double* Brow = cL1 + (ks + tq) * NG;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], af, __ldg(Brow + 8 * j + g));
+      }
+      double* T = a.T + (long long)grp * NG * NG;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        __stcs(reinterpret_cast<double2*>(T + (rr0 + g) * NG + 8 * j + 2 * tq), make_double2(acc[j][0], acc[j][1]));
+    }
+    P3_ADD(9, t_ep, tid == 0);
+  }
+}
+
+#ifdef HPS_LEAF_PROFILE
+extern "C" int hps_debug_leaf3_profile(long long* out, int reset) {
+  if (reset) {
+    static long long z[1024][16] = {};
+    cudaMemcpyToSymbol(g_leaf3_prof, z, sizeof(z));
+    return 0;
+  }
+  cudaMemcpyFromSymbol(out, g_leaf3_prof, sizeof(long long) * 1024 * 16);
+  return 0;
+}
+#endif
+
+size_t leaf16v3_scratch_doubles() { return (size_t)l3::MROWS * l3::LDM; }
+
+int leaf16v3_grid(int ngroups) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int per_sm = getenv("HPS_LEAF3_CTAS_PER_SM") ? atoi(getenv("HPS_LEAF3_CTAS_PER_SM")) : 2;
+  return std::max(1, std::min(ngroups, per_sm * sms));
+}
+
+int launch_leaf16v3(LeafArgs& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(k_leaf16v3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l3::SMEM));
+    attr = true;
+  }
+  a.scratch_stride = (long long)leaf16v3_scratch_doubles();
+  k_leaf16v3<<<leaf16v3_grid(a.ngroups), l3::THREADS, l3::SMEM, st>>>(a);
+  HPS_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+}  // namespace hps
