@@ -1,9 +1,47 @@
 // Host launcher for the DMMA GEMM (tile selection) + the C-ABI test hook.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm.cuh"
 
 namespace hps {
+
+__global__ void k_splitk_reduce(GemmParams p) {
+  const long long mn = (long long)p.M * p.N;
+  const long long total = mn * p.batch;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / mn, rc = e - b * mn;
+    const int r = (int)(rc / p.N), c = (int)(rc - (long long)r * p.N);
+    const double* P = p.partial + b * p.split * mn + rc;
+    double s = 0.0;
+    for (int k = 0; k < p.split; ++k) s += P[k * mn];
+    double* dst = p.C + b * p.strideC + (long long)r * p.ldc + c;
+    double v = p.alpha * s;
+    if (p.beta != 0.0) v += p.beta * *dst;
+    if (p.nonfinite && !isfinite(v)) atomicMax(p.nonfinite, (int)b + p.batch_offset);
+    *dst = v;
+  }
+}
+
+// Split-K scratch: one growing device buffer (builds repeat the same shapes, so it settles after
+// the first build). The library enqueues on one stream at a time.
+static double* g_splitk = nullptr;
+static size_t g_splitk_n = 0;
+static double* splitk_scratch(size_t n) {
+  if (n > g_splitk_n) {
+    if (g_splitk) {
+      cudaDeviceSynchronize();
+      cudaFree(g_splitk);
+    }
+    if (cudaMalloc(&g_splitk, n * sizeof(double)) != cudaSuccess) {
+      g_splitk = nullptr;
+      g_splitk_n = 0;
+      return nullptr;
+    }
+    g_splitk_n = n;
+  }
+  return g_splitk;
+}
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
 static int launch_cfg(const GemmParams& p, cudaStream_t stream) {
@@ -14,9 +52,30 @@ static int launch_cfg(const GemmParams& p, cudaStream_t stream) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     attr_set = true;
   }
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.batch);
-  kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(p);
+  // split-K when the tile grid cannot fill the GPU and K is long (top levels, batched solve)
+  const long long tiles = (long long)((p.N + BN - 1) / BN) * ((p.M + BM - 1) / BM) * p.batch;
+  int split = 1;
+  static const int allow = getenv("HPS_SPLITK") ? atoi(getenv("HPS_SPLITK")) : 1;
+  if (allow && tiles < 148 && p.K >= 8 * BK) {
+    split = (int)std::min<long long>((2 * 148 + tiles - 1) / tiles, p.K / (4 * BK));
+    split = std::max(1, std::min(split, 16));
+    while (split > 1 && (long long)split * p.batch > 65535) --split;
+  }
+  GemmParams q = p;
+  if (split > 1) {
+    q.split = split;
+    q.partial = splitk_scratch((size_t)split * p.batch * (size_t)p.M * p.N);
+    if (!q.partial) q.split = 1;
+  }
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.batch * q.split);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(q);
   HPS_LAUNCH_CHECK();
+  if (q.split > 1) {
+    const long long total = (long long)p.M * p.N * p.batch;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+    k_splitk_reduce<<<blocks, 256, 0, stream>>>(q);
+    HPS_LAUNCH_CHECK();
+  }
   return HPS_OK;
 }
 

@@ -23,6 +23,8 @@ struct GemmParams {
   double alpha, beta;
   int* nonfinite;  // optional: set to max batch index with a non-finite output
   int batch_offset = 0;  // added to the reported batch index (batch-chunked launches)
+  int split = 1;         // split-K factor (blockIdx.z = batch * split + s)
+  double* partial = nullptr;  // split > 1: raw partial sums [batch][split][M][N]
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
@@ -46,7 +48,8 @@ dgemm_dmma_kernel(GemmParams p) {
   double* sA = smem;
   double* sB = smem + STAGES * Cfg::kStageA;
 
-  const int b = blockIdx.z;
+  const int b = blockIdx.z / p.split;
+  const int ks_idx = blockIdx.z - b * p.split;
   const int m0 = blockIdx.y * BM;
   const int n0 = blockIdx.x * BN;
   const int tid = threadIdx.x;
@@ -59,10 +62,13 @@ dgemm_dmma_kernel(GemmParams p) {
   const int* Bidx = p.Bidx ? p.Bidx + (long long)b * p.strideBidx : nullptr;
   double* C = p.C + (long long)b * p.strideC;
 
-  const int ktiles = p.K / BK;  // K % BK == 0 enforced by the launcher
+  const int kt_all = p.K / BK;  // K % BK == 0 enforced by the launcher
+  const int kt_per = (kt_all + p.split - 1) / p.split;
+  const int kt0 = ks_idx * kt_per;
+  const int ktiles = max(0, min(kt_all, kt0 + kt_per) - kt0);
 
   auto load_stage = [&](int stage, int kt) {
-    const int k0 = kt * BK;
+    const int k0 = (kt0 + kt) * BK;
     double* a_dst = sA + stage * Cfg::kStageA;
     constexpr int A_CHUNKS = BM * BK / 2;
 #pragma unroll
@@ -125,6 +131,20 @@ dgemm_dmma_kernel(GemmParams p) {
   }
   cp_async_wait<0>();
 
+  if (p.split > 1) {  // raw partial sums; k_splitk_reduce applies alpha/beta in a fixed order
+    double* P = p.partial + ((long long)b * p.split + ks_idx) * (long long)p.M * p.N;
+#pragma unroll
+    for (int i = 0; i < Cfg::TM; ++i) {
+      int r = m0 + a_row0 + i * 8;
+      if (r >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < Cfg::TN; ++j) {
+        int c = n0 + wn * (BN / WN) + j * 8 + 2 * t;
+        if (c < p.N) *reinterpret_cast<double2*>(P + (long long)r * p.N + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
+    return;
+  }
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < Cfg::TM; ++i) {
@@ -149,6 +169,9 @@ dgemm_dmma_kernel(GemmParams p) {
   }
   if (p.nonfinite && bad) atomicMax(p.nonfinite, b + p.batch_offset);
 }
+
+// C[b] = alpha * sum_s P[b][s] + beta * C[b], deterministic summation order.
+__global__ void k_splitk_reduce(GemmParams p);
 
 // Launch with a tile shape picked from the problem size. Returns HPS_OK or an error code.
 int dgemm_launch(const GemmParams& p, cudaStream_t stream);
