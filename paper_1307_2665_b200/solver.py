@@ -206,7 +206,36 @@ class SolverState:
 # ----------------------------------------------------------------------------------------------
 # Build
 # ----------------------------------------------------------------------------------------------
-def _sample(coeffs, lay, geom):
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        import concurrent.futures
+        import os
+
+        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)))
+    return _POOL
+
+
+def _eval_field(f, xs, ys, threads=True):
+    """f(xs, ys) for a pointwise coefficient callable. Large evaluations run on leaf-aligned row
+    chunks in a thread pool (numpy ufuncs release the GIL). Each element is computed by the same
+    SIMD code path as in a single call, since chunks are whole leaves, 256 points each."""
+    n = xs.shape[0]
+    if not threads or n < 256:
+        return f(xs, ys)
+    nchunk = max(1, min(16, n // 64))
+    bounds = np.linspace(0, n, nchunk + 1).astype(int)
+    parts = list(_pool().map(lambda ab: f(xs[ab[0]:ab[1]], ys[ab[0]:ab[1]]), zip(bounds[:-1], bounds[1:])))
+    if any(np.isscalar(q) or np.ndim(q) == 0 for q in parts):  # the callable returned a scalar
+        return f(xs, ys)
+    return np.concatenate([np.broadcast_to(np.asarray(q, dtype=float), (b1 - b0, xs.shape[1]))
+                           for q, b0, b1 in zip(parts, bounds[:-1], bounds[1:])])
+
+
+def _sample(coeffs, lay, geom, threads=True):
     """Coefficient samples on all leaf Chebyshev grids, heap leaf order (solver.py:196-206)."""
     lc = lay.leaf_cells
     xs = lay.xline[lc[:, 0]][:, None] + geom.grid_x[None, :]
@@ -214,7 +243,7 @@ def _sample(coeffs, lay, geom):
     fields = {}
     for name in COEFF_NAMES:
         f = getattr(coeffs, name)
-        fields[name] = f(xs, ys) if callable(f) else float(f)
+        fields[name] = _eval_field(f, xs, ys, threads) if callable(f) else float(f)
         v = np.atleast_1d(fields[name])
         if not np.all(np.isfinite(v)):
             bad = np.argwhere(~np.isfinite(np.broadcast_to(fields[name], xs.shape)))
