@@ -43,10 +43,10 @@ static double* splitk_scratch(size_t n) {
   return g_splitk;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool VEC = true>
 static int launch_cfg(const GemmParams& p, cudaStream_t stream) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
-  auto kern = dgemm_dmma_kernel<BM, BN, BK, WM, WN, STAGES>;
+  auto kern = dgemm_dmma_kernel<BM, BN, BK, WM, WN, STAGES, VEC>;
   static bool attr_set = false;  // per-instantiation
   if (!attr_set) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
@@ -81,15 +81,14 @@ static int launch_cfg(const GemmParams& p, cudaStream_t stream) {
 
 int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return HPS_OK;
-  if (p.K % 16 != 0 || p.N % 2 != 0 || (p.ldb % 2) || (p.ldc % 2) || (p.lda % 2) ||
-      (p.strideA % 2) || (p.strideB % 2) || (p.strideC % 2) ||
-      (reinterpret_cast<uintptr_t>(p.A) & 15) || (reinterpret_cast<uintptr_t>(p.B) & 15) ||
-      (reinterpret_cast<uintptr_t>(p.C) & 15)) {
-    set_error("dgemm: unsupported shape/alignment M=%d N=%d K=%d lda=%lld ldb=%lld ldc=%lld", p.M, p.N, p.K,
-              p.lda, p.ldb, p.ldc);
+  if (p.K <= 0) {
+    set_error("dgemm: K=%d", p.K);
     return HPS_ERR_ARG;
   }
-  if (p.K == 0) return HPS_OK;
+  const bool vec = !(p.K % 16 != 0 || p.N % 2 != 0 || (p.ldb % 2) || (p.ldc % 2) || (p.lda % 2) ||
+                     (p.strideA % 2) || (p.strideB % 2) || (p.strideC % 2) ||
+                     (reinterpret_cast<uintptr_t>(p.A) & 15) || (reinterpret_cast<uintptr_t>(p.B) & 15) ||
+                     (reinterpret_cast<uintptr_t>(p.C) & 15));
   if (p.batch > 65535) {  // gridDim.z limit: launch in batch chunks
     for (int b0 = 0; b0 < p.batch; b0 += 65535) {
       GemmParams q = p;
@@ -104,6 +103,7 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
     }
     return HPS_OK;
   }
+  if (!vec) return launch_cfg<64, 64, 16, 2, 2, 3, false>(p, stream);  // any shape (e.g. q = 21)
   double tiles128 = double((p.M + 127) / 128) * double((p.N + 127) / 128) * p.batch;
   if (p.M >= 128 && p.N >= 128 && tiles128 >= 148.0) return launch_cfg<128, 128, 16, 2, 4, 4>(p, stream);
   return launch_cfg<64, 64, 16, 2, 2, 3>(p, stream);

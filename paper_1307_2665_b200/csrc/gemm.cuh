@@ -40,7 +40,7 @@ struct GemmCfg {
   static_assert(BM % (WM * 8) == 0 && BN % (WN * 8) == 0 && BK % 4 == 0, "tile");
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool VEC = true>
 __global__ void __launch_bounds__(WM* WN * 32)
 dgemm_dmma_kernel(GemmParams p) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
@@ -62,13 +62,33 @@ dgemm_dmma_kernel(GemmParams p) {
   const int* Bidx = p.Bidx ? p.Bidx + (long long)b * p.strideBidx : nullptr;
   double* C = p.C + (long long)b * p.strideC;
 
-  const int kt_all = p.K / BK;  // K % BK == 0 enforced by the launcher
+  const int kt_all = VEC ? p.K / BK : (p.K + BK - 1) / BK;  // VEC: K % BK == 0 (launcher)
   const int kt_per = (kt_all + p.split - 1) / p.split;
   const int kt0 = ks_idx * kt_per;
   const int ktiles = max(0, min(kt_all, kt0 + kt_per) - kt0);
 
   auto load_stage = [&](int stage, int kt) {
     const int k0 = (kt0 + kt) * BK;
+    if constexpr (!VEC) {  // any shape / alignment: predicated scalar loads, zero padding
+      double* a_dst = sA + stage * Cfg::kStageA;
+      for (int e = tid; e < BM * BK; e += Cfg::kThreads) {
+        const int r = e / BK, c = e - r * BK;
+        const int gr = m0 + r, gk = k0 + c;
+        a_dst[r * Cfg::SA + c] = (gr < p.M && gk < p.K) ? A[(long long)gr * p.lda + gk] : 0.0;
+      }
+      double* b_dst = sB + stage * Cfg::kStageB;
+      for (int e = tid; e < BK * BN; e += Cfg::kThreads) {
+        const int r = e / BN, c = e - r * BN;
+        const int gk = k0 + r, gc = n0 + c;
+        double v = 0.0;
+        if (gk < p.K && gc < p.N) {
+          const long long row = Bidx ? (long long)Bidx[gk] : (long long)gk;
+          v = B[row * p.ldb + gc];
+        }
+        b_dst[r * Cfg::SB + c] = v;
+      }
+      return;
+    }
     double* a_dst = sA + stage * Cfg::kStageA;
     constexpr int A_CHUNKS = BM * BK / 2;
 #pragma unroll
@@ -140,7 +160,12 @@ dgemm_dmma_kernel(GemmParams p) {
 #pragma unroll
       for (int j = 0; j < Cfg::TN; ++j) {
         int c = n0 + wn * (BN / WN) + j * 8 + 2 * t;
-        if (c < p.N) *reinterpret_cast<double2*>(P + (long long)r * p.N + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        if constexpr (!VEC) {
+          if (c < p.N) P[(long long)r * p.N + c] = acc[i][j][0];
+          if (c + 1 < p.N) P[(long long)r * p.N + c + 1] = acc[i][j][1];
+        } else if (c < p.N) {
+          *reinterpret_cast<double2*>(P + (long long)r * p.N + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        }
       }
     }
     return;
@@ -155,6 +180,17 @@ dgemm_dmma_kernel(GemmParams p) {
       int c = n0 + wn * (BN / WN) + j * 8 + 2 * t;
       if (c >= p.N) continue;
       double* dst = C + (long long)r * p.ldc + c;
+      if constexpr (!VEC) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (c + h < p.N) {
+            double v = p.alpha * acc[i][j][h];
+            if (p.beta != 0.0) v += p.beta * dst[h];
+            bad |= !isfinite(v);
+            dst[h] = v;
+          }
+        continue;
+      }
       double2 v;
       v.x = p.alpha * acc[i][j][0];
       v.y = p.alpha * acc[i][j][1];

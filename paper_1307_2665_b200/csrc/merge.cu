@@ -15,6 +15,7 @@
 // sigma V V^T makes the system nonsingular and well conditioned (cond 1e2..1e3 measured). Its
 // solution is the particular S with V^T S = 0. That S is reproducible, while the reference's raw
 // S is rounding noise along V. T matches the reference (parity-gated in tests/).
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <vector>
@@ -414,34 +415,30 @@ static int gemm(int M, int N, int K, int batch, double alpha, const double* A, l
 static int inverse_rec(double* A, long long lda, long long strideA, int n, int batch, double* tmp, int* status,
                        int status_base, cudaStream_t st) {
   if (n <= 128) return inverse_small(A, lda, strideA, n, batch, status, status_base, st);
-  const int h = n / 2;
+  const int h = n / 2, h2 = n - h;  // unequal halves allowed (q = 21 gives n3 = 21 * 2^j)
   double* A11 = A;
   double* A12 = A + h;
   double* A21 = A + (long long)h * lda;
   double* A22 = A21 + h;
-  double* T12 = tmp;
-  double* T21 = tmp + (long long)batch * h * h;
-  double* deeper = T21 + (long long)batch * h * h;
-  const long long sT = (long long)h * h;
+  double* T12 = tmp;                              // h x h2
+  double* T21 = tmp + (long long)batch * h * h2;  // h2 x h
+  double* deeper = T21 + (long long)batch * h * h2;
+  const long long sT = (long long)h * h2;
   HPS_TRY(inverse_rec(A11, lda, strideA, h, batch, deeper, status, status_base, st));
-  HPS_TRY(gemm(h, h, h, batch, 1.0, A11, lda, strideA, A12, lda, strideA, 0.0, T12, h, sT, st));
-  HPS_TRY(gemm(h, h, h, batch, 1.0, A21, lda, strideA, A11, lda, strideA, 0.0, T21, h, sT, st));
-  HPS_TRY(gemm(h, h, h, batch, -1.0, A21, lda, strideA, T12, h, sT, 1.0, A22, lda, strideA, st));
-  HPS_TRY(inverse_rec(A22, lda, strideA, h, batch, deeper, status, status_base, st));
-  HPS_TRY(gemm(h, h, h, batch, -1.0, T12, h, sT, A22, lda, strideA, 0.0, A12, lda, strideA, st));
-  HPS_TRY(gemm(h, h, h, batch, -1.0, A22, lda, strideA, T21, h, sT, 0.0, A21, lda, strideA, st));
-  HPS_TRY(gemm(h, h, h, batch, -1.0, A12, lda, strideA, T21, h, sT, 1.0, A11, lda, strideA, st));
+  HPS_TRY(gemm(h, h2, h, batch, 1.0, A11, lda, strideA, A12, lda, strideA, 0.0, T12, h2, sT, st));
+  HPS_TRY(gemm(h2, h, h, batch, 1.0, A21, lda, strideA, A11, lda, strideA, 0.0, T21, h, sT, st));
+  HPS_TRY(gemm(h2, h2, h, batch, -1.0, A21, lda, strideA, T12, h2, sT, 1.0, A22, lda, strideA, st));
+  HPS_TRY(inverse_rec(A22, lda, strideA, h2, batch, deeper, status, status_base, st));
+  HPS_TRY(gemm(h, h2, h2, batch, -1.0, T12, h2, sT, A22, lda, strideA, 0.0, A12, lda, strideA, st));
+  HPS_TRY(gemm(h2, h, h2, batch, -1.0, A22, lda, strideA, T21, h, sT, 0.0, A21, lda, strideA, st));
+  HPS_TRY(gemm(h, h, h2, batch, -1.0, A12, lda, strideA, T21, h, sT, 1.0, A11, lda, strideA, st));
   return HPS_OK;
 }
 
 static size_t inverse_rec_tmp_doubles(int n, int batch) {
-  size_t s = 0;
-  while (n > 128) {
-    int h = n / 2;
-    s += 2ull * batch * h * h;
-    n = h;
-  }
-  return s;
+  if (n <= 128) return 0;
+  const int h = n / 2, h2 = n - h;
+  return 2ull * batch * h * h2 + std::max(inverse_rec_tmp_doubles(h, batch), inverse_rec_tmp_doubles(h2, batch));
 }
 
 }  // namespace hps
@@ -514,7 +511,7 @@ extern "C" size_t hps_inverse_workspace_bytes(int n, int batch) {
 
 extern "C" int hps_inverse_batched(int n, int batch, double* X, long long lda, long long strideX, void* ws,
                                    size_t ws_bytes, int* status, void* stream) {
-  if (ws_bytes < hps_inverse_workspace_bytes(n, batch) || (n > 128 && (n % 32))) {
+  if (ws_bytes < hps_inverse_workspace_bytes(n, batch) || n <= 0) {
     set_error("hps_inverse_batched: bad arguments n=%d ws=%zu", n, ws_bytes);
     return HPS_ERR_ARG;
   }

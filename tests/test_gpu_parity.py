@@ -220,3 +220,35 @@ def test_distributed_path_single_rank_cuda_backend():
         assert rel(full, solver.solve(st, F.cpu().numpy())) < 1e-13
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("q,L,cfg", [(21, 2, 2), (12, 3, 1), (10, 2, 3), (7, 3, 5)])
+def test_general_q_against_oracle(q, L, cfg):
+    """Any q >= 3 (the paper uses q = 21): generic leaf kernel, unaligned GEMM path, unequal
+    recursive-inverse halves."""
+    tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), L, q)
+    st = solver.build(tree, nodes, problems.coefficients(cfg), keep_level_T=True)
+    ot = O.build_tree((0, 1, 0, 1), L, q)
+    ost = O.build(ot, coeff_dict(problems.coefficients(cfg)), keep_T=True)
+    assert rel(st.T_leaf_groups.cpu().numpy(), ost.T_groups) < 1e-12
+    assert rel(st.root_T.dense, ost.root_T) < T_TOL[cfg]
+    F = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=1, batch=12)
+    u = solver.solve(st, F)
+    assert rel(O.leaf_cheb_boundary(ost, u), O.leaf_cheb_boundary(ost, O.solve(ost, F))) < U_TOL[cfg]
+
+
+@pytest.mark.parametrize("n,batch", [(16, 7), (100, 3), (128, 2), (168, 2), (336, 1), (512, 2)])
+def test_inverse_batched(n, batch):
+    from paper_1307_2665_b200 import _native
+
+    lib = _native.load()
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((batch, n, n)) + 3 * np.sqrt(n) * np.eye(n)
+    X = torch.from_numpy(A.copy()).cuda()
+    ws = torch.empty(lib.hps_inverse_workspace_bytes(n, batch), dtype=torch.uint8, device="cuda")
+    stw = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    _native.check(lib.hps_inverse_batched(n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(),
+                                          _native.ptr(stw), _native.stream_ptr()), "inverse")
+    Xi = X.cpu().numpy()
+    assert np.abs(A @ Xi - np.eye(n)).max() < 1e-11
+    assert int(stw.item()) == -1
