@@ -33,6 +33,7 @@ import time
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 sys.path.insert(0, HERE)
 
 FP64_PEAK_FILE = os.path.join(HERE, "profiles", "fp64_peak_r01.json")
@@ -241,7 +242,9 @@ def main():
         U = solver.solve_device(st, F_dev)
         return st, U, e
 
+    st = U = None
     for _ in range(args.warmup):
+        st = U = None  # free the previous step's operators first (L=9: ~50 GB of S + u)
         st, U, _ = step()
     torch.cuda.synchronize()
     solver.check_build(st)
@@ -251,6 +254,7 @@ def main():
     launches0 = lib.hps_launch_count()
     t_build, t_solve, stages = [], [], {}
     for _ in range(args.steps):
+        st = U = None
         flush.fill_(1.0)
         tl = []
         e0 = torch.cuda.Event(enable_timing=True)
@@ -297,7 +301,9 @@ def main():
     U_host = torch.empty((nodes.N, solver.rhs_ld(b)), dtype=torch.float64).pin_memory()
     e2e_t = []
     h2d = d2h = 0
+    st = U = None
     for it in range(max(2, args.steps)):
+        st2 = U2 = None
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         inp2 = solver.prepare(tree, nodes, co, device=dev, pinned=True)
