@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
   __shared__ int s_cnt[2 * NPW];
   __shared__ int s_nact[2];
   __shared__ int s_sing;
+  __shared__ int s_next;  // work-stealing counter for the trailing update
   __shared__ double s_red[8];
   double* sA16 = sm + OFF_A16;
   double* sU12 = sm + OFF_U12;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
     const int r0 = tid, r1 = tid + 128;
     bool act0 = pwarp && r0 < NI, act1 = pwarp && r1 < NI;
     int step0 = -1, step1 = -1;
+    int cidx0 = -1, cidx1 = -1;  // compact index of r0 / r1 in the last active list
 
     auto factor = [&](int k) {  // panel warps only
       const int k0 = 16 * k, kb = min(16, NI - k0);
@@ -168,6 +170,27 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
         if (act1 && j < kb) v1 = *reinterpret_cast<const double2*>(M + (long long)r1 * LDM + k0 + j);
         w0[j] = v0.x; w0[j + 1] = (j + 1 < kb) ? v0.y : 0.0;
         w1[j] = v1.x; w1[j + 1] = (j + 1 < kb) ? v1.y : 0.0;
+      }
+      if (k > 0) {  // apply panel k-1's rank-16 update to this panel's columns of my rows (registers)
+        const int kbp = 16;  // every panel but the last is full
+        const double* Ap = sA16 + ((k - 1) & 1) * MROWS * SA;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j < kbp) {
+            const double a0 = act0 ? Ap[cidx0 * SA + j] : 0.0;
+            const double a1 = act1 ? Ap[cidx1 * SA + j] : 0.0;
+            const double* Ur = sU12 + j * SB;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const double u = Ur[c];
+              w0[c] = fma(a0, u, w0[c]);
+              w1[c] = fma(a1, u, w1[c]);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c >= kb) { w0[c] = 0.0; w1[c] = 0.0; }
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -260,12 +283,14 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
       double* A16 = sA16 + buf * MROWS * SA;
       if (act0) {
         const int i = off0 + __popc(b0 & lt);
+        cidx0 = i;
         act[i] = r0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) sts64(A16 + i * SA + j, j < kb ? -w0[j] : 0.0);
       }
       if (act1) {
         const int i = off1 + __popc(b1 & lt);
+        cidx1 = i;
         act[i] = r1;
 #pragma unroll
         for (int j = 0; j < 16; ++j) sts64(A16 + i * SA + j, j < kb ? -w1[j] : 0.0);
@@ -275,6 +300,7 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
 
     // rank-kb update of M[act rows][c0 + [cbeg, cend)] by the update warps (uw = 0..3). Work item:
     // 8 rows x CW columns whose C loads are all issued before the DMMAs (one L2 round trip).
+    // uw >= 0: static round-robin over 4 update warps; uw < 0: pull items from s_next (any warp).
     auto update = [&](int k, int cbeg, int cend, int uw) {
       constexpr int CW = 128, NJ = CW / 8;
       const int k0 = 16 * k, kb = min(16, NI - k0), c0 = k0 + kb, nT = LDM - c0;
@@ -285,7 +311,14 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
       const int nrt = (nact + 7) >> 3;
       const int ncw = (cend - cbeg + CW - 1) / CW;
       const int lim = min(cend, nT);
-      for (int it = uw; it < nrt * ncw; it += 4) {
+      const int nitems = nrt * ncw;
+      for (int it = uw >= 0 ? uw : 0;;) {
+        if (uw < 0) {
+          int v = 0;
+          if (lane == 0) v = atomicAdd(&s_next, 1);
+          it = __shfl_sync(0xffffffffu, v, 0);
+        }
+        if (it >= nitems) break;
         const int rt = it / ncw, cb = cbeg + (it - rt * ncw) * CW;
         const int ri = rt * 8 + g;
         const bool rv = ri < nact;
@@ -319,6 +352,7 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
           const int col = cb + 8 * j + 2 * tq;
           if (rv && col < lim) *reinterpret_cast<double2*>(Mr + col) = make_double2(acc[j][0], acc[j][1]);
         }
+        if (uw >= 0) it += 4;
       }
     };
 
@@ -348,26 +382,26 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
           for (int r = 0; r < 16; ++r)
             if (r < kb) M[(long long)sPiv[k0 + r] * LDM + c0 + cc] = y[r];
       }
+      if (tid == 0) s_next = 0;
       __syncthreads();
       P3_ADD(2, t_u12, tid == 0);
       P3_T(t_main);
+      // The next panel's columns are updated by the panel warps themselves inside factor(k+1)
+      // (in registers, for their own rows), so the update warps start right after them and
+      // nobody waits for a look-ahead hand-off.
       const bool ahead = k + 1 < NPANEL;
+      const int la = ahead ? min(16, NI - 16 * (k + 1)) : 0;  // exactly the next panel's columns
       if (!pwarp) {
-        const int uw = warp - NPW;
-        const int la = ahead ? min(16, nT) : 0;  // next panel's columns first
-        if (ahead) {
-          update(k, 0, la, uw);
-          __threadfence_block();
-          bar_arrive(BAR_LOOKAHEAD, THREADS);
-        }
         P3_ADD(3, t_main, tid == 128);
-        update(k, la, nT, uw);
+        update(k, la, nT, -1);
         P3_ADD(4, t_main, tid == 128);
-      } else if (ahead) {
-        bar_sync(BAR_LOOKAHEAD, THREADS);
-        P3_ADD(5, t_main, tid == 0);
-        factor(k + 1);
-        P3_ADD(6, t_main, tid == 0);
+      } else {
+        if (ahead) {
+          P3_ADD(5, t_main, tid == 0);
+          factor(k + 1);
+          P3_ADD(6, t_main, tid == 0);
+        }
+        update(k, la, nT, -1);  // join the remaining trailing update
       }
       __syncthreads();
       P3_ADD(7, t_main, tid == 0);
