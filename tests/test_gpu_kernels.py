@@ -43,10 +43,22 @@ def test_dgemm_row_gather():
     assert rel(tC.cpu().numpy(), want) < 1e-14
 
 
-def test_dgemm_rejects_bad_shapes():
+@pytest.mark.parametrize("M,N,K,B", [(21, 7, 21, 3), (84, 84, 42, 2), (5, 3, 7, 1), (130, 66, 33, 4)])
+def test_dgemm_generic_shapes(M, N, K, B):
+    """Shapes the vectorised path cannot take (K % 16, odd N / leading dims) use the generic path."""
+    lib = _native.load()
+    rng = np.random.default_rng(M * N + K)
+    A, Bm, C = rng.standard_normal((B, M, K)), rng.standard_normal((B, K, N)), rng.standard_normal((B, M, N))
+    tA, tB, tC = cuda(A), cuda(Bm), cuda(C)
+    _native.check(lib.hps_dgemm_batched(M, N, K, B, 1.5, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N, None, 0,
+                                        -0.5, _native.ptr(tC), N, M * N, _native.stream_ptr()), "gemm")
+    assert rel(tC.cpu().numpy(), 1.5 * A @ Bm - 0.5 * C) < 1e-14
+
+
+def test_dgemm_rejects_empty_k():
     lib = _native.load()
     t = torch.zeros(64, dtype=torch.float64, device="cuda")
-    st = lib.hps_dgemm_batched(4, 4, 7, 1, 1.0, _native.ptr(t), 7, 0, _native.ptr(t), 4, 0, None, 0, 0.0,
+    st = lib.hps_dgemm_batched(4, 4, 0, 1, 1.0, _native.ptr(t), 4, 0, _native.ptr(t), 4, 0, None, 0, 0.0,
                                _native.ptr(t), 4, 0, _native.stream_ptr())
     assert st == _native.HPS_ERR_ARG
 
