@@ -43,7 +43,8 @@ struct ChildRef {
 
 __global__ void k_gather_xr(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b,
                             const int* __restrict__ j3a, const int* __restrict__ j3b, int n3, int ne,
-                            double* __restrict__ X, double* __restrict__ R) {
+                            double* __restrict__ X, double* __restrict__ R,
+                            unsigned long long* __restrict__ diagmax) {
   const int b = blockIdx.x;
   const int r = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -53,7 +54,13 @@ __global__ void k_gather_xr(ChildRef ch, const int* __restrict__ j1a, const int*
   const double* Tb = ch.bb(b) + (long long)j3b[r] * ch.m;
   double* Xr = X + ((long long)b * n3 + r) * n3;
   double* Rr = R + ((long long)b * n3 + r) * ne;
-  for (int c = lane; c < n3; c += 32) Xr[c] = Ta[j3a[c]] - Tb[j3b[c]];
+  for (int c = lane; c < n3; c += 32) {
+    const double v = Ta[j3a[c]] - Tb[j3b[c]];
+    Xr[c] = v;
+    // max |diag X| for the deflation shift: non-negative doubles order like their bit patterns,
+    // so an integer atomicMax is exact and independent of the CTA order
+    if (c == r && diagmax) atomicMax(diagmax + b, (unsigned long long)__double_as_longlong(fabs(v)));
+  }
   for (int c = lane; c < n1; c += 32) Rr[c] = -Ta[j1a[c]];
   for (int c = lane; c < n1; c += 32) Rr[n1 + c] = Tb[j2b[c]];
 }
@@ -354,14 +361,13 @@ __global__ void __launch_bounds__(128) k_merge_small(ChildRef ch, const int* __r
   }
 }
 
-// Deflation X += sigma V V^T, sigma = max |diag X|: one CTA per (segment row, merge).
-__global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs, const double* __restrict__ ve) {
-  __shared__ double red[32];
+// Deflation X += sigma V V^T, sigma = max |diag X| (reduced by k_gather_xr before any CTA here
+// modifies a diagonal block): one CTA per (segment row, merge).
+__global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs, const double* __restrict__ ve,
+                          const unsigned long long* __restrict__ diagmax) {
   const int b = blockIdx.x, sr = blockIdx.y;
   double* Xb = X + (long long)b * n * n;
-  double dm = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dm = fmax(dm, fabs(Xb[(long long)i * n + i]));
-  const double sigma = block_max(dm, red);
+  const double sigma = __longlong_as_double((long long)diagmax[b]);
   const int nseg = n / q;
   const int c0 = max(0, sr - 1) * q, c1 = min(nseg, sr + 2) * q;
   const int w = c1 - c0;
@@ -446,7 +452,7 @@ static size_t inverse_rec_tmp_doubles(int n, int batch) {
 using namespace hps;
 
 extern "C" size_t hps_merge_workspace_bytes(int nbatch, int n3, int ne) {
-  size_t d = size_t(nbatch) * (size_t(n3) * n3 + 2ull * n3 * ne) + inverse_rec_tmp_doubles(n3, nbatch);
+  size_t d = size_t(nbatch) * (size_t(n3) * n3 + 2ull * n3 * ne + 1) + inverse_rec_tmp_doubles(n3, nbatch);
   return d * sizeof(double) + 256;
 }
 
@@ -483,15 +489,19 @@ extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const d
   double* R = X + (size_t)nbatch * n3 * n3;
   double* Cm = R + (size_t)nbatch * n3 * ne;
   double* tmp = Cm + (size_t)nbatch * ne * n3;
+  unsigned long long* diagmax = reinterpret_cast<unsigned long long*>(tmp + inverse_rec_tmp_doubles(n3, nbatch));
+  const bool deflate = n3 > q;  // deflate the n3/q - 1 corner null modes
+  if (deflate) HPS_CUDA_CHECK(cudaMemsetAsync(diagmax, 0, sizeof(unsigned long long) * nbatch, st));
   ChildRef ch{T_child, child_stride, child_idx, m};
-  k_gather_xr<<<dim3(nbatch, (n3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, X, R);
+  k_gather_xr<<<dim3(nbatch, (n3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, X, R,
+                                                        deflate ? diagmax : nullptr);
   HPS_LAUNCH_CHECK();
   k_gather_ct<<<dim3(nbatch, (ne + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, Cm, T_out);
   HPS_LAUNCH_CHECK();
   const double* vs = vmode;
   const double* ve = vmode + q;
-  if (n3 > q) {  // deflate the n3/q - 1 corner null modes
-    k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vs, ve);
+  if (deflate) {
+    k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vs, ve, diagmax);
     HPS_LAUNCH_CHECK();
   }
   HPS_TRY(inverse_rec(X, n3, (long long)n3 * n3, n3, nbatch, tmp, status, status_base, st));

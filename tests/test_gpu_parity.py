@@ -137,6 +137,21 @@ def test_repeat_solve_and_build_are_bitwise_deterministic():
     assert all(torch.equal(a, b) for a, b in zip(st.S_levels, st2.S_levels))
 
 
+def test_full_size_constant_coefficient_build_is_bitwise_deterministic():
+    # cfg3 at full size exposed a cross-CTA race on max|diag X| in the deflation (fixed r01): every
+    # build of the same input must give bit-identical S and T at every depth.
+    c = problems.CONFIGS[3]
+    tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), c.L, 16)
+    inp = solver.prepare(tree, nodes, c.coefficients())
+    ref = solver.build_device(inp, keep_level_T=True)
+    for _ in range(3):
+        st = solver.build_device(inp, keep_level_T=True)
+        for d in range(len(ref.S_levels)):
+            assert torch.equal(ref.S_levels[d], st.S_levels[d]), f"S differs at depth {d}"
+            assert torch.equal(ref.level_T[d], st.level_T[d]), f"T differs at depth {d}"
+        del st
+
+
 def test_batched_solve_matches_single_rhs():
     tree, nodes, st = gpu_build(2, 3)
     F = problems.boundary_data(2, nodes.points[tree.root.I_e], seed=2, batch=20)
