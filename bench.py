@@ -283,7 +283,9 @@ def main():
     stage_ms = {k: float(np.mean(v)) * 1e3 for k, v in stages.items()}
     dom = max(stage_ms, key=stage_ms.get)
     ach = stage_flops[dom] / (stage_ms[dom] / 1e3) / 1e12
-    kernels = {"leaf": "hps::k_leaf"}.get(dom, "hps_merge_level (gather, deflate, k_gj_inverse, dgemm_dmma)")
+    leaf_kernel = "hps::k_leaf16v3" if q == 16 and os.environ.get("HPS_LEAF_V", "3") != "2" else (
+        "hps::k_leaf16" if q == 16 else "hps::k_leaf")
+    kernels = {"leaf": leaf_kernel}.get(dom, "hps_merge_level (gather, deflate, k_gj_inverse, dgemm_dmma)")
     build_flops = sum(stage_flops.values())
     solve_flops = O.solve_flops(L, q, b)
     S_bytes = sum((2 ** d) * O.depth_sizes(L, q, d)[0] * O.depth_sizes(L, q, d)[1] * 8 for d in range(2 * L))
@@ -296,30 +298,41 @@ def main():
                   "gbs_S_stream": S_bytes / ts / 1e9, "frac_hbm": S_bytes / ts / 1e9 / hpeak, "hbm_peak_source": hsrc},
     }
 
-    # ---- end-to-end through the public API, pinned host memory ----
+    # ---- end-to-end through the public API (solver.Pipeline), pinned host memory ----
+    # Every step is one full problem: host sampling + grouping of the coefficients, their H2D
+    # upload, the build, the H2D of the boundary data, the batched solve and the D2H of u. The
+    # pipeline overlaps the host work of step i+1 with the device work of step i.
     pin_F = torch.from_numpy(np.ascontiguousarray(F_host)).pin_memory()
-    U_host = torch.empty((nodes.N, solver.rhs_ld(b)), dtype=torch.float64).pin_memory()
-    e2e_t = []
-    h2d = d2h = 0
+    pipe = solver.Pipeline(tree, nodes, device=dev)
     st = U = None
-    for it in range(max(2, args.steps)):
-        st2 = U2 = None
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        inp2 = solver.prepare(tree, nodes, co, device=dev, pinned=True)
-        st2 = solver.build_device(inp2)
-        Fd = pin_F.to(dev, non_blocking=True)
-        U2 = solver.solve_device(st2, Fd)
-        U_host.copy_(U2, non_blocking=True)
-        solver.check_build(st2)
-        torch.cuda.synchronize()
-        e2e_t.append(time.perf_counter() - t0)
-        h2d = inp2.h2d_bytes() + pin_F.numel() * 8
-        d2h = U_host.numel() * 8 + 4 * 2 * L + 8 * inp2.ngroups
-    e2e = {"value": unknowns / float(np.median(e2e_t)), "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(d2h), "seconds_per_step": float(np.median(e2e_t)),
-           "includes": "coefficient sampling + grouping (host), H2D from pinned memory, build, status check, "
-                       "batched solve, D2H of u (N x ldu)"}
+    n_e2e = max(10, args.steps)  # a stream of problems: pipeline fill and drain are inside the total
+    for U, st in pipe.run([(co, pin_F)] * n_e2e):
+        st = None
+    st = U = None
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for U, st in pipe.run([(co, pin_F)] * n_e2e):
+        st = None  # drop each state once its solution is back (as a serving loop would)
+    torch.cuda.synchronize()
+    e2e_step = (time.perf_counter() - t0) / n_e2e
+    lat = []
+    for _ in range(2):  # one problem alone through the same pipeline: no overlap
+        t1 = time.perf_counter()
+        for U, st in pipe.run([(co, pin_F)]):
+            st = None
+        lat.append(time.perf_counter() - t1)
+    pipe.close()
+    inp_b = solver.prepare(tree, nodes, co, device=dev, pinned=True)
+    h2d = inp_b.h2d_bytes() + pin_F.numel() * 8
+    d2h = U.numel() * 8 + 4 * 2 * L + 8 * inp_b.ngroups + 8 * (inp_b.ngroups + inp_b.gid.size)
+    del inp_b
+    e2e = {"value": unknowns / e2e_step, "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "seconds_per_step": e2e_step, "steps": n_e2e,
+           "latency_s": float(min(lat)),
+           "includes": "per step: coefficient sampling on the host, H2D of the samples (pinned), leaf grouping "
+                       "on the device, build, status check, H2D of the boundary data, batched solve, D2H of u "
+                       "(N x ldu); solver.Pipeline overlaps step i+1's host work with step i's device work; "
+                       "latency_s = one problem alone"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -15,6 +15,8 @@
  *   hps_solve_level  <- SolutionOperator.apply inside solver.solve, solver.py:93-97 / 312-315,
  *                       for all parents of one depth and a batch of right-hand sides
  *   hps_dgemm_batched <- the BLAS dgemm behind `@` (merge.py:118, solver.py:71 apply_global_dtn)
+ *   hps_leaf_hash / hps_leaf_verify <- the leaf grouping of solver._leaf_stage, solver.py:208-222
+ *                       (np.unique over the stacked coefficient sample rows)
  */
 #ifndef HPS_B200_H
 #define HPS_B200_H
@@ -80,6 +82,15 @@ int hps_dgemm_batched(int M, int N, int K, int batch, double alpha, const double
                       long long strideA, const double* B, long long ldb, long long strideB,
                       const int* Bidx, long long strideBidx, double beta, double* C, long long ldc,
                       long long strideC, void* stream);
+
+/* Leaf grouping (solver.py:208-222). fields: HOST array of nfields (1..6) DEVICE pointers, each to
+ * n_leaf x row_len fp64 samples. hps_leaf_hash writes a 64-bit hash of every leaf's rows;
+ * hps_leaf_verify sets *mismatch (device int) to 1 if some leaf's rows differ bitwise from those of
+ * leaf rep_of[leaf], i.e. the hash grouping had a collision and must be redone exactly. */
+int hps_leaf_hash(int n_leaf, int row_len, int nfields, const double* const* fields,
+                  unsigned long long* hash, void* stream);
+int hps_leaf_verify(int n_leaf, int row_len, int nfields, const double* const* fields,
+                    const long long* rep_of, int* mismatch, void* stream);
 
 #ifdef __cplusplus
 }

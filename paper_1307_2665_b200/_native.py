@@ -24,7 +24,8 @@ HPS_ERR_ARG = 5
 #: every symbol include/hps_b200.h declares (tests check the .so exports all of them)
 EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_launch_count", "hps_leaf_workspace_bytes",
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
-           "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched")
+           "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched", "hps_leaf_hash",
+           "hps_leaf_verify")
 
 _lib = None
 
@@ -68,6 +69,10 @@ def load():
     lib.hps_inverse_workspace_bytes.restype = c_sz
     lib.hps_inverse_batched.argtypes = [c_int, c_int, c_dp, c_ll, c_ll, c_dp, c_sz, c_dp, c_dp]
     lib.hps_inverse_batched.restype = c_int
+    lib.hps_leaf_hash.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_dp), c_dp, c_dp]
+    lib.hps_leaf_hash.restype = c_int
+    lib.hps_leaf_verify.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_dp), c_dp, c_dp, c_dp]
+    lib.hps_leaf_verify.restype = c_int
     _lib = lib
     return lib
 

@@ -634,6 +634,40 @@ extern "C" size_t hps_leaf_workspace_bytes(int p, int ngroups) {
   return sizeof(double) * (size_t)leaf_grid(ngroups) * ni * ldm + 256;
 }
 
+// Optional L2 persistence window over the per-CTA leaf scratch (HPS_LEAF_L2PERSIST=1): the scratch
+// is re-read and re-written by every panel, everything else is touched once. Reset on scope exit.
+struct L2Window {
+  cudaStream_t st;
+  bool on = false;
+  L2Window(cudaStream_t s, void* base, size_t bytes) : st(s) {
+    static const int persist = getenv("HPS_LEAF_L2PERSIST") ? atoi(getenv("HPS_LEAF_L2PERSIST")) : 0;
+    if (!persist) return;
+    int dev = 0, maxp = 0, maxw = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (maxp <= 0 || maxw <= 0) return;
+    const size_t win = std::min(bytes, (size_t)maxw);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)maxp, win));
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = base;
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    on = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+    cudaGetLastError();
+  }
+  ~L2Window() {
+    if (!on) return;
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+    cudaGetLastError();
+  }
+};
+
 extern "C" int hps_leaf_stage(int p, int ngroups, const double* const* fields, const double* scalars,
                               const double* consts, const int* idx, double probe_max, double* Psi, double* T,
                               double* cond, void* ws, size_t ws_bytes, void* stream) {
@@ -660,7 +694,10 @@ extern "C" int hps_leaf_stage(int p, int ngroups, const double* const* fields, c
   const int ni = (p - 2) * (p - 2), nb = 4 * (p - 1);
   a.scratch = static_cast<double*>(ws);
   static const int leaf_v = getenv("HPS_LEAF_V") ? atoi(getenv("HPS_LEAF_V")) : 3;
-  if (p == 16 && !getenv("HPS_LEAF_GENERIC") && leaf_v == 3) return launch_leaf16v3(a, st);
+  if (p == 16 && !getenv("HPS_LEAF_GENERIC") && leaf_v == 3) {
+    L2Window window(st, ws, (size_t)leaf16v3_grid(ngroups) * leaf16v3_scratch_doubles() * sizeof(double));
+    return launch_leaf16v3(a, st);
+  }
   if (p == 16 && !getenv("HPS_LEAF_GENERIC")) {
     a.scratch_stride = (long long)l16::MROWS * l16::LDM;
     static bool attr = false;
@@ -671,39 +708,12 @@ extern "C" int hps_leaf_stage(int p, int ngroups, const double* const* fields, c
     }
     // Keep as much of the per-CTA scratch in L2 as the persisting carve-out allows: the scratch is
     // re-read and re-written by every panel, everything else is touched once.
-    static int persist = getenv("HPS_LEAF_L2PERSIST") ? atoi(getenv("HPS_LEAF_L2PERSIST")) : 0;  // measured: no gain
-    const size_t scratch = (size_t)leaf16_grid(ngroups) * a.scratch_stride * sizeof(double);
-    bool windowed = false;
-    if (persist) {
-      int dev = 0, maxp = 0, maxw = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-      if (maxp > 0 && maxw > 0) {
-        const size_t win = std::min(scratch, (size_t)maxw);
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)maxp, win));
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.base_ptr = ws;
-        v.accessPolicyWindow.num_bytes = win;
-        v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        windowed = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
-        cudaGetLastError();
-      }
-    }
+    L2Window window(st, ws, (size_t)leaf16_grid(ngroups) * a.scratch_stride * sizeof(double));
     if (leaf16_threads() == 512)
       k_leaf16<512><<<leaf16_grid(ngroups), 512, l16::SMEM, st>>>(a);
     else
       k_leaf16<256><<<leaf16_grid(ngroups), 256, l16::SMEM, st>>>(a);
     HPS_LAUNCH_CHECK();
-    if (windowed) {
-      cudaStreamAttrValue v{};
-      v.accessPolicyWindow.num_bytes = 0;
-      cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
-      cudaCtxResetPersistingL2Cache();
-      cudaGetLastError();
-    }
     return HPS_OK;
   }
   a.scratch_stride = (long long)ni * (ni + nb + 2);

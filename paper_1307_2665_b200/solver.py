@@ -219,23 +219,37 @@ def _pool():
     return _POOL
 
 
-def _eval_field(f, xs, ys, threads=True):
+def _eval_field(f, xs, ys, threads=True, out=None):
     """f(xs, ys) for a pointwise coefficient callable. Large evaluations run on leaf-aligned row
     chunks in a thread pool (numpy ufuncs release the GIL). Each element is computed by the same
-    SIMD code path as in a single call, since chunks are whole leaves, 256 points each."""
+    SIMD code path as in a single call, since chunks are whole leaves, 256 points each.
+    `out(shape)` optionally allocates the result (e.g. in pinned host memory); the chunks are then
+    written straight into it instead of being concatenated."""
     n = xs.shape[0]
     if not threads or n < 256:
         return f(xs, ys)
     nchunk = max(1, min(16, n // 64))
     bounds = np.linspace(0, n, nchunk + 1).astype(int)
-    parts = list(_pool().map(lambda ab: f(xs[ab[0]:ab[1]], ys[ab[0]:ab[1]]), zip(bounds[:-1], bounds[1:])))
-    if any(np.isscalar(q) or np.ndim(q) == 0 for q in parts):  # the callable returned a scalar
+    first = f(xs[bounds[0]:bounds[1]], ys[bounds[0]:bounds[1]])
+    if np.isscalar(first) or np.ndim(first) == 0:  # the callable returned a scalar
         return f(xs, ys)
-    return np.concatenate([np.broadcast_to(np.asarray(q, dtype=float), (b1 - b0, xs.shape[1]))
-                           for q, b0, b1 in zip(parts, bounds[:-1], bounds[1:])])
+    res = out(xs.shape) if out is not None else np.empty(xs.shape)
+    res[bounds[0]:bounds[1]] = np.broadcast_to(np.asarray(first, dtype=float), (bounds[1] - bounds[0], xs.shape[1]))
+
+    def run(ab):
+        b0, b1 = ab
+        q = f(xs[b0:b1], ys[b0:b1])
+        if np.isscalar(q) or np.ndim(q) == 0:
+            return False
+        res[b0:b1] = np.broadcast_to(np.asarray(q, dtype=float), (b1 - b0, xs.shape[1]))
+        return True
+
+    if not all(_pool().map(run, zip(bounds[1:-1], bounds[2:]))):
+        return f(xs, ys)
+    return res
 
 
-def _sample(coeffs, lay, geom, threads=True):
+def _sample(coeffs, lay, geom, threads=True, out=None):
     """Coefficient samples on all leaf Chebyshev grids, heap leaf order (solver.py:196-206)."""
     lc = lay.leaf_cells
     xs = lay.xline[lc[:, 0]][:, None] + geom.grid_x[None, :]
@@ -243,7 +257,7 @@ def _sample(coeffs, lay, geom, threads=True):
     fields = {}
     for name in COEFF_NAMES:
         f = getattr(coeffs, name)
-        fields[name] = _eval_field(f, xs, ys, threads) if callable(f) else float(f)
+        fields[name] = _eval_field(f, xs, ys, threads, out) if callable(f) else float(f)
         v = np.atleast_1d(fields[name])
         if not np.all(np.isfinite(v)):
             bad = np.argwhere(~np.isfinite(np.broadcast_to(fields[name], xs.shape)))
@@ -282,6 +296,35 @@ def _group(fields, n_leaf):
     rank = np.empty_like(order)
     rank[order] = np.arange(order.size)
     return first[order].astype(np.int64), rank[inv].astype(np.int64)
+
+
+def _group_device(dev_fields, n_leaf):
+    """_group on the device (solver.py:208-222): hash every leaf's sample rows (hps_leaf_hash),
+    bucket by hash, then check every leaf bitwise against its bucket's first leaf (hps_leaf_verify).
+    Returns (reps, gid) as device int64 tensors in _group's order (groups by first occurrence), or
+    None if the bitwise check found a hash collision (the caller regroups exactly on the host)."""
+    torch = _torch()
+    lib = _native.load()
+    dev = dev_fields[0].device
+    row = int(dev_fields[0].shape[1])
+    stream = _native.stream_ptr()
+    ptrs = (ctypes_vp * len(dev_fields))(*[_native.ptr(t).value for t in dev_fields])
+    h = torch.empty(n_leaf, dtype=torch.int64, device=dev)
+    _native.check(lib.hps_leaf_hash(n_leaf, row, len(dev_fields), ptrs, _native.ptr(h), stream), "hps_leaf_hash")
+    _, inv = torch.unique(h, sorted=True, return_inverse=True)
+    ng = int(inv.max()) + 1
+    ar = torch.arange(n_leaf, device=dev)
+    first = torch.full((ng,), n_leaf, dtype=torch.int64, device=dev).scatter_reduce_(0, inv, ar, "amin")
+    rep_of = first[inv].contiguous()
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    _native.check(lib.hps_leaf_verify(n_leaf, row, len(dev_fields), ptrs, _native.ptr(rep_of), _native.ptr(bad),
+                                      stream), "hps_leaf_verify")
+    order = torch.argsort(first)
+    rank = torch.empty_like(order)
+    rank[order] = torch.arange(ng, device=dev)
+    if int(bad.item()):
+        return None
+    return first[order], rank[inv]
 
 
 class _DeviceLayout:
@@ -332,14 +375,20 @@ class BuildInputs:
     fields_dev: list
     scalars: tuple
     device: object
+    uploaded_bytes: int = 0  # H2D bytes prepare() moved (full sample arrays, before grouping)
 
     @property
     def ngroups(self):
         return int(self.reps.size)
 
     def h2d_bytes(self):
+        if self.uploaded_bytes:
+            return int(self.uploaded_bytes)
         return int(sum(t.numel() * t.element_size() for t in self.fields_dev if t is not None)
                    + self.gid_dev.numel() * 4)
+
+    def device_tensors(self):
+        return [t for t in self.fields_dev if t is not None] + [self.gid_dev]
 
 
 def prepare(tree, nodeset, coeffs, *, device=None, pinned=False):
@@ -351,28 +400,50 @@ def prepare(tree, nodeset, coeffs, *, device=None, pinned=False):
     if q < 3:
         raise ValueError("p must be >= 3 (need an interior node)")
     geom = LeafGeometry.get(q, tree.leaf_width, tree.leaf_height)
-    fields = _sample(coeffs, lay, geom)  # ValueError on non-finite samples, as the reference
-    reps, gid = _group(fields, 1 << (2 * lay.L))
+    n_leaf = 1 << (2 * lay.L)
+    host_bufs = []
+    pinned = pinned and torch.cuda.is_available()
+
+    def pinned_out(shape):  # sample straight into page-locked memory (no staging copy)
+        t = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        host_bufs.append(t)
+        return t.numpy()
+
+    fields = _sample(coeffs, lay, geom, out=pinned_out if pinned else None)  # ValueError on non-finite samples
     _native.require_device()
     device = torch.device(device if device is not None else "cuda")
     dl = _DeviceLayout.get(lay, geom, device)
+    names = [n for n in COEFF_NAMES if not np.isscalar(fields[n])]
+    full = {}
+    for name in names:
+        v = fields[name]
+        h = next((t for t in host_bufs if t.numpy().ctypes.data == v.ctypes.data), None) if pinned else None
+        if h is None:
+            h = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64) if v.flags.writeable
+                                 else np.array(v, dtype=np.float64, order="C"))
+        full[name] = h.to(device, non_blocking=pinned)
+    # group bitwise-equal leaves on the device (host fallback on a hash collision)
+    grouped = _group_device([full[n] for n in names], n_leaf) if names else None
+    if grouped is not None:
+        reps_dev, gid_dev64 = grouped
+        reps, gid = reps_dev.cpu().numpy(), gid_dev64.cpu().numpy()
+        gid_dev = gid_dev64.to(torch.int32)
+    else:
+        reps, gid = _group(fields, n_leaf)
+        reps_dev = torch.from_numpy(reps).to(device)
+        gid_dev = torch.from_numpy(gid.astype(np.int32)).to(device)
     fields_dev, scalars = [], []
     for name in COEFF_NAMES:
-        v = fields[name]
-        if np.isscalar(v):
+        if name not in full:
             fields_dev.append(None)
-            scalars.append(float(v))
+            scalars.append(float(fields[name]))
         else:
-            h = torch.from_numpy(np.ascontiguousarray(v[reps]))
-            if pinned:
-                h = h.pin_memory()
-            fields_dev.append(h.to(device, non_blocking=pinned))
+            t = full[name]
+            fields_dev.append(t if reps.size == n_leaf else t.index_select(0, reps_dev))
             scalars.append(0.0)
-    h = torch.from_numpy(gid.astype(np.int32))
-    if pinned:
-        h = h.pin_memory()
-    gid_dev = h.to(device, non_blocking=pinned)
-    return BuildInputs(tree, nodeset, coeffs, lay, geom, dl, reps, gid, gid_dev, fields_dev, tuple(scalars), device)
+    up = sum(t.numel() * 8 for t in full.values())
+    return BuildInputs(tree, nodeset, coeffs, lay, geom, dl, reps, gid, gid_dev, fields_dev, tuple(scalars), device,
+                       uploaded_bytes=int(up))
 
 
 def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_threshold=math.inf,
@@ -485,13 +556,15 @@ def _marker(timeline, name):
 
 def check_build(state):
     """Read back the device status words and raise the reference's exceptions (one host sync)."""
-    cond = state._cond.cpu().numpy()
+    _raise_from_status(state, state._cond.cpu().numpy(), state._status.cpu().numpy())
+
+
+def _raise_from_status(state, cond, st):
     bad = np.flatnonzero(cond > RESONANCE_COND)
     if bad.size:  # first group in first-occurrence order (solver.py:235-239)
         j = int(bad[0])
         leaf_index = (1 << (2 * state.layout.L)) - 1 + int(state._reps[j])
         raise LeafResonanceError(box=leaf_index, cond=float(cond[j]))
-    st = state._status.cpu().numpy()
     for d in range(len(st) - 1, -1, -1):  # reference merges deepest (highest index) first
         if st[d] >= 0:
             raise MergeResonanceError(box=(1 << d) - 1 + int(st[d]), detail="non-finite solution operator")
@@ -554,6 +627,101 @@ def solve(state, f):
     U = solve_device(state, F)
     u = U[:, :F.shape[1]].cpu().numpy()
     return u[:, 0].copy() if single else u
+
+
+class Pipeline:
+    """Build + solve a stream of problems on one discretisation with host and device overlapped.
+
+    The reference builds and solves one problem per `build`/`solve` call (solver.py:170-316); a
+    service answering many coefficient fields / boundary data on the same tree runs that pair in a
+    loop. Here, while the device builds and solves problem i on the main stream, a host thread
+    samples, uploads and groups problem i+1's coefficients (`prepare`, pinned memory, its own
+    stream), and problem i-1's u and status words come back on a third stream. Every problem
+    still makes its own H2D copies and its own D2H of u; at most two states are alive at once.
+
+    `run(jobs)` takes an iterable of (coeffs, F), F a host (|Gamma|, b) or (|Gamma|,) array in
+    root.I_e order, and yields (U, state) per job in order: U is a pinned host tensor (N, ldu) whose
+    columns [:b] are the solutions, state the SolverState (valid until the caller drops it)."""
+
+    def __init__(self, tree, nodeset, *, device=None, overlap_results=True):
+        torch = _torch()
+        _native.require_device()
+        self.overlap_results = overlap_results
+        self.tree, self.nodeset = tree, nodeset
+        self.device = torch.device(device if device is not None else "cuda")
+        self._upload = torch.cuda.Stream(self.device)
+        self._main = torch.cuda.Stream(self.device)
+        self._d2h = torch.cuda.Stream(self.device)
+        import concurrent.futures
+        self._host = concurrent.futures.ThreadPoolExecutor(max_workers=1)
+
+    def _prepare(self, coeffs):
+        torch = _torch()
+        with torch.cuda.device(self.device), torch.cuda.stream(self._upload):
+            inp = prepare(self.tree, self.nodeset, coeffs, device=self.device, pinned=True)
+            ready = torch.cuda.Event()
+            ready.record(self._upload)
+        return inp, ready
+
+    def run(self, jobs):
+        torch = _torch()
+        it = iter(jobs)
+        job = next(it, None)
+        fut = self._host.submit(self._prepare, job[0]) if job is not None else None
+        pending = None
+        while fut is not None:
+            inp, ready = fut.result()
+            nxt = next(it, None)
+            F = job[1]
+            fut = self._host.submit(self._prepare, nxt[0]) if nxt is not None else None
+            with torch.cuda.device(self.device):
+                with torch.cuda.stream(self._main):
+                    self._main.wait_event(ready)
+                    for t in inp.device_tensors():
+                        t.record_stream(self._main)
+                    st = build_device(inp)
+                    Fh = F if torch.is_tensor(F) else torch.from_numpy(np.ascontiguousarray(np.asarray(F, dtype=float)))
+                    if Fh.dim() == 1:
+                        Fh = Fh[:, None]
+                    if not Fh.is_pinned():
+                        Fh = Fh.pin_memory()
+                    U = solve_device(st, Fh.to(self.device, non_blocking=True))
+                    solved = torch.cuda.Event()
+                    solved.record(self._main)
+                # results and status words come back on their own stream, so the next job's build
+                # is enqueued on the main stream before this job's D2H is waited for
+                with torch.cuda.stream(self._d2h):
+                    self._d2h.wait_event(solved)
+                    outs = []
+                    for t in (U, st._cond, st._status):
+                        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                        h.copy_(t, non_blocking=True)
+                        t.record_stream(self._d2h)
+                        outs.append(h)
+                    done = torch.cuda.Event()
+                    done.record(self._d2h)
+            del U
+            if pending is not None:
+                yield self._finish(*pending)
+            pending = (st, outs, done)
+            del st
+            if not self.overlap_results:
+                yield self._finish(*pending)
+                pending = None
+            job = nxt
+        if pending is not None:
+            yield self._finish(*pending)
+
+    @staticmethod
+    def _finish(st, outs, done):
+        done.synchronize()
+        U_host, cond, status = outs
+        _raise_from_status(st, cond.numpy(), status.numpy())
+        instrumentation.bump("solve")
+        return U_host, st
+
+    def close(self):
+        self._host.shutdown(wait=True)
 
 
 def apply_global_dtn(state, f):

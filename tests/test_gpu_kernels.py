@@ -80,3 +80,46 @@ def test_solve_level(nb, n3, ne, ldu, nrhs):
     for b in range(nb):
         ref[300 + b * n3:300 + (b + 1) * n3, :nrhs] = S[b] @ u[Ie[b], :nrhs]
     assert rel(tu.cpu().numpy()[:, :nrhs], ref[:, :nrhs]) < 1e-14
+
+
+def _host_fields(kind, n_leaf=1024, row=256, seed=0):
+    rng = np.random.default_rng(seed)
+    if kind == "distinct":
+        return {"c11": rng.standard_normal((n_leaf, row)), "c22": rng.standard_normal((n_leaf, row))}
+    if kind == "duplicates":  # 37 distinct rows scattered over the leaves, one field
+        base = rng.standard_normal((37, row))
+        return {"c": base[rng.integers(0, 37, n_leaf)]}
+    # two fields whose duplicate patterns differ: leaves group only where both agree
+    a, b = rng.standard_normal((5, row)), rng.standard_normal((3, row))
+    ia, ib = rng.integers(0, 5, n_leaf), rng.integers(0, 3, n_leaf)
+    f = {"c11": a[ia], "c1": b[ib]}
+    f["c11"][7] = -0.0 * f["c11"][7]  # signed zeros / bit patterns differ from +0.0
+    return f
+
+
+@pytest.mark.parametrize("kind", ["distinct", "duplicates", "mixed"])
+def test_device_grouping_matches_host(kind):
+    from paper_1307_2665_b200 import solver
+    fields = _host_fields(kind)
+    n_leaf = next(iter(fields.values())).shape[0]
+    full = dict.fromkeys(solver.COEFF_NAMES, 0.0)
+    full.update(fields)
+    reps_h, gid_h = solver._group(full, n_leaf)
+    dev = [cuda(full[n]) for n in solver.COEFF_NAMES if not np.isscalar(full[n])]
+    reps_d, gid_d = solver._group_device(dev, n_leaf)
+    assert np.array_equal(reps_d.cpu().numpy(), reps_h)
+    assert np.array_equal(gid_d.cpu().numpy(), gid_h)
+
+
+def test_leaf_verify_flags_a_wrong_representative():
+    import ctypes
+    lib = _native.load()
+    f = cuda(np.arange(4 * 256, dtype=np.float64).reshape(4, 256))
+    ptrs = (ctypes.c_void_p * 1)(_native.ptr(f).value)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ok = torch.tensor([0, 1, 2, 3], dtype=torch.int64, device="cuda")
+    _native.check(lib.hps_leaf_verify(4, 256, 1, ptrs, _native.ptr(ok), _native.ptr(flag), _native.stream_ptr()), "v")
+    assert int(flag.item()) == 0
+    wrong = torch.tensor([0, 0, 2, 3], dtype=torch.int64, device="cuda")
+    _native.check(lib.hps_leaf_verify(4, 256, 1, ptrs, _native.ptr(wrong), _native.ptr(flag), _native.stream_ptr()), "v")
+    assert int(flag.item()) == 1

@@ -267,3 +267,19 @@ def test_inverse_batched(n, batch):
     Xi = X.cpu().numpy()
     assert np.abs(A @ Xi - np.eye(n)).max() < 1e-11
     assert int(stw.item()) == -1
+
+
+def test_pipeline_matches_sequential_build_and_solve():
+    # solver.Pipeline overlaps the host preparation of job i+1 with the device work of job i; every
+    # job's u must be bitwise equal to a plain build + solve of that job alone.
+    tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), 4, 16)
+    pts = nodes.points[tree.root.I_e]
+    jobs = [(problems.coefficients(cfg), problems.boundary_data(2, pts, seed=cfg, batch=3)) for cfg in (2, 4, 3, 2)]
+    pipe = solver.Pipeline(tree, nodes)
+    got = [(U[:, :3].numpy().copy(), st.n_leaf_groups) for U, st in pipe.run(jobs)]
+    pipe.close()
+    assert len(got) == len(jobs)
+    for (co, F), (u, ng) in zip(jobs, got):
+        st = solver.build(tree, nodes, co)
+        assert ng == st.n_leaf_groups
+        assert np.array_equal(u, solver.solve(st, F))
