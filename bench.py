@@ -290,8 +290,17 @@ def main():
     solve_flops = O.solve_flops(L, q, b)
     S_bytes = sum((2 ** d) * O.depth_sizes(L, q, d)[0] * O.depth_sizes(L, q, d)[1] * 8 for d in range(2 * L))
     hpeak, hsrc = hbm_peak()
+    traffic, traffic_src = None, None  # DRAM bytes per launch of the dominant kernel (committed ncu capture)
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "leaf16v3_ncu_r01.json")
+    if dom == "leaf" and leaf_kernel == "hps::k_leaf16v3" and os.path.exists(prof):
+        pj = json.load(open(prof))
+        if pj.get("workload") == workload:
+            traffic = float(pj["dram_bytes_per_launch"])
+            traffic_src = (f"profiles/leaf16v3_ncu_r01.json: dram read+write per launch (ncu --set full); "
+                           f"algorithmic {pj['algorithmic_bytes_per_launch']:.3g} B")
     roofline = {
-        "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+        "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
+        "traffic_source": traffic_src,
         "kernel": dom, "kernels": kernels, "peak_source": peak_src,
         "stage_ms": stage_ms, "build_tflops": build_flops / tb / 1e12, "build_frac": build_flops / tb / 1e12 / peak,
         "solve": {"tflops": solve_flops / ts / 1e12, "frac_fp64": solve_flops / ts / 1e12 / peak,

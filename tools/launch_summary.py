@@ -13,7 +13,7 @@ def load(path):
             if d["Metric Name"] == "gpu__time_duration.sum":
                 v = float(d["Metric Value"].replace(",", ""))
                 u = d["Metric Unit"]
-                v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+                v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(u, 1.0)
                 out.append((d["Kernel Name"], d["Grid Size"], d["Block Size"], v))
     return out
 
