@@ -46,7 +46,6 @@ constexpr int NDBL = OFF_PROW + 32;
 constexpr int NINT = 2 * MROWS + NI + NI + NB + 64;
 constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4 + 64;
 constexpr int BAR_PANEL = 1;      // panel warps only (128 threads)
-constexpr int BAR_LOOKAHEAD = 2;  // update warps arrive, panel warps sync (256 threads)
 }  // namespace l3
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
