@@ -79,6 +79,43 @@ static int launch_cfg(const GemmParams& p, cudaStream_t stream) {
   return HPS_OK;
 }
 
+// 64 x 64 paired-fragment kernel (gemm.cuh): MINB CTAs per SM, split-K to fill 148 * MINB slots.
+template <int BK, int STAGES, int MINB>
+static int launch_cfg64(const GemmParams& p, cudaStream_t stream) {
+  using Cfg = Gemm64Cfg<BK, STAGES>;
+  auto kern = dgemm64_kernel<BK, STAGES, MINB>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    attr_set = true;
+  }
+  const long long tiles = (long long)((p.N + 63) / 64) * ((p.M + 63) / 64) * p.batch;
+  int split = 1;
+  static const int allow = getenv("HPS_SPLITK") ? atoi(getenv("HPS_SPLITK")) : 1;
+  const long long slots = 148LL * MINB;
+  if (allow && tiles < slots && p.K >= 4 * BK) {
+    split = (int)std::min<long long>((2 * slots + tiles - 1) / tiles, p.K / (2 * BK));
+    split = std::max(1, std::min(split, 16));
+    while (split > 1 && (long long)split * p.batch > 65535) --split;
+  }
+  GemmParams q = p;
+  if (split > 1) {
+    q.split = split;
+    q.partial = splitk_scratch((size_t)split * p.batch * (size_t)p.M * p.N);
+    if (!q.partial) q.split = 1;
+  }
+  dim3 grid((p.N + 63) / 64, (p.M + 63) / 64, p.batch * q.split);
+  kern<<<grid, 128, Cfg::kSmem, stream>>>(q);
+  HPS_LAUNCH_CHECK();
+  if (q.split > 1) {
+    const long long total = (long long)p.M * p.N * p.batch;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+    k_splitk_reduce<<<blocks, 256, 0, stream>>>(q);
+    HPS_LAUNCH_CHECK();
+  }
+  return HPS_OK;
+}
+
 int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return HPS_OK;
   if (p.K <= 0) {
@@ -104,7 +141,12 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
     return HPS_OK;
   }
   if (!vec) return launch_cfg<64, 64, 16, 2, 2, 3, false>(p, stream);  // any shape (e.g. q = 21)
+  // 64 x 64 paired-fragment tiles, BK 16, 3 stages, 3 CTAs per SM: measured best of
+  // {BK 16/32} x {2,3,4 stages} x {2,3,4 CTAs/SM} on the merge shapes (tools/gemm_variants.sh)
+  static const int v64 = getenv("HPS_GEMM64") ? atoi(getenv("HPS_GEMM64")) : 1;
+  if (v64) return launch_cfg64<16, 3, 3>(p, stream);
   double tiles128 = double((p.M + 127) / 128) * double((p.N + 127) / 128) * p.batch;
+  // HPS_GEMM64=0: the previous tiling (128 x 128 x 16, 8 warps of 64 x 32, one CTA per SM)
   if (p.M >= 128 && p.N >= 128 && tiles128 >= 148.0) return launch_cfg<128, 128, 16, 2, 4, 4>(p, stream);
   return launch_cfg<64, 64, 16, 2, 2, 3>(p, stream);
 }

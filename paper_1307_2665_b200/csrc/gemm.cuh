@@ -206,6 +206,165 @@ dgemm_dmma_kernel(GemmParams p) {
   if (p.nonfinite && bad) atomicMax(p.nonfinite, b + p.batch_offset);
 }
 
+// 64 x 64 CTA tile, 4 warps of 32 x 32, several CTAs per SM (the shape cuBLAS picks for DGEMM on
+// sm_100). Fragments are loaded in pairs with LDS.128:
+//  * k pairing: in every 8-deep k block, DMMA k-step s in {0,1} gives lane tq the k index
+//    2*tq + s, so a lane's A fragments of both steps, A[m][2tq], A[m][2tq+1], are adjacent;
+//  * n pairing: in every 16-column block, DMMA j in {0,1} takes column 2c + j for its fragment
+//    column c, so B[k][2g], B[k][2g+1] feed both DMMAs, and each lane ends up owning 4
+//    consecutive output columns per row.
+// Smem strides: A row = BK + 8 doubles (== 8 mod 16), B row = 64 + 2 doubles (== 2 mod 8): every
+// quarter-warp's 16-byte loads hit 8 distinct bank groups.
+template <int BK, int STAGES>
+struct Gemm64Cfg {
+  static constexpr int BM = 64, BN = 64, kThreads = 128;
+  static constexpr int SA = BK + 8;
+  static constexpr int SB = BN + 2;
+  static constexpr int kStageA = BM * SA;
+  static constexpr int kStageB = BK * SB;
+  static constexpr size_t kSmem = size_t(STAGES) * (kStageA + kStageB) * sizeof(double);
+};
+
+template <int BK, int STAGES, int MINB>
+__global__ void __launch_bounds__(128, MINB) dgemm64_kernel(GemmParams p) {
+  using Cfg = Gemm64Cfg<BK, STAGES>;
+  constexpr int BM = 64, BN = 64;
+  extern __shared__ __align__(128) double smem[];
+  double* sA = smem;
+  double* sB = smem + STAGES * Cfg::kStageA;
+  const int b = blockIdx.z / p.split;
+  const int ks_idx = blockIdx.z - b * p.split;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int g = lane >> 2, t = lane & 3;
+  const double* A = p.A + (long long)b * p.strideA;
+  const double* B = p.B + (long long)b * p.strideB;
+  const int* Bidx = p.Bidx ? p.Bidx + (long long)b * p.strideBidx : nullptr;
+  double* C = p.C + (long long)b * p.strideC;
+  const int kt_all = p.K / BK;
+  const int kt_per = (kt_all + p.split - 1) / p.split;
+  const int kt0 = ks_idx * kt_per;
+  const int ktiles = max(0, min(kt_all, kt0 + kt_per) - kt0);
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = (kt0 + kt) * BK;
+    double* a_dst = sA + stage * Cfg::kStageA;
+#pragma unroll
+    for (int c = tid; c < BM * BK / 2; c += 128) {
+      const int r = c / (BK / 2), cc = c % (BK / 2);
+      const int gr = m0 + r;
+      const bool ok = gr < p.M;
+      cp_async16(a_dst + r * Cfg::SA + 2 * cc, A + (long long)(ok ? gr : 0) * p.lda + k0 + 2 * cc, ok);
+    }
+    double* b_dst = sB + stage * Cfg::kStageB;
+#pragma unroll
+    for (int c = tid; c < BK * BN / 2; c += 128) {
+      const int r = c / (BN / 2), cc = c % (BN / 2);
+      const int gc = n0 + 2 * cc;
+      const bool ok = gc < p.N;
+      const long long row = Bidx ? (long long)Bidx[k0 + r] : (long long)(k0 + r);
+      cp_async16(b_dst + r * Cfg::SB + 2 * cc, B + row * p.ldb + (ok ? gc : 0), ok);
+    }
+  };
+
+  double acc[4][2][2][2];  // [m block][n pair][j][h]
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[i][q][j][0] = acc[i][q][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_stage(s, s);
+    cp_async_commit();
+  }
+  const int arow = wm * 32 + g;       // + 8 i
+  const int bcol = wn * 32 + 2 * g;   // + 16 q
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < ktiles) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* a_s = sA + (kt % STAGES) * Cfg::kStageA;
+    const double* b_s = sB + (kt % STAGES) * Cfg::kStageB;
+#pragma unroll
+    for (int kb = 0; kb < BK; kb += 8) {
+      double2 af[4], bf[2][2];  // af[i] = steps 0/1; bf[s][q] = (j0, j1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = *reinterpret_cast<const double2*>(a_s + (arow + 8 * i) * Cfg::SA + kb + 2 * t);
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          bf[s2][q] = *reinterpret_cast<const double2*>(b_s + (kb + 2 * t + s2) * Cfg::SB + bcol + 16 * q);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          dmma_8x8x4(acc[i][q][0][0], acc[i][q][0][1], af[i].x, bf[0][q].x);
+          dmma_8x8x4(acc[i][q][1][0], acc[i][q][1][1], af[i].x, bf[0][q].y);
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          dmma_8x8x4(acc[i][q][0][0], acc[i][q][0][1], af[i].y, bf[1][q].x);
+          dmma_8x8x4(acc[i][q][1][0], acc[i][q][1][1], af[i].y, bf[1][q].y);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+  // lane (g, t) owns rows arow + 8i, columns bcol' + 16q + 4t + {0,1,2,3} (= 2h + j)
+  const int ccol0 = n0 + wn * 32 + 4 * t;
+  if (p.split > 1) {
+    double* P = p.partial + ((long long)b * p.split + ks_idx) * (long long)p.M * p.N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = m0 + arow + 8 * i;
+      if (r >= p.M) continue;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = ccol0 + 16 * q;
+        double* dst = P + (long long)r * p.N + c;
+        if (c < p.N) *reinterpret_cast<double2*>(dst) = make_double2(acc[i][q][0][0], acc[i][q][1][0]);
+        if (c + 2 < p.N) *reinterpret_cast<double2*>(dst + 2) = make_double2(acc[i][q][0][1], acc[i][q][1][1]);
+      }
+    }
+    return;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + arow + 8 * i;
+    if (r >= p.M) continue;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = ccol0 + 16 * q;
+      double* dst = C + (long long)r * p.ldc + c;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (c + 2 * h >= p.N) continue;
+        double2 v = make_double2(p.alpha * acc[i][q][0][h], p.alpha * acc[i][q][1][h]);
+        if (p.beta != 0.0) {
+          const double2 o = *reinterpret_cast<const double2*>(dst + 2 * h);
+          v.x += p.beta * o.x;
+          v.y += p.beta * o.y;
+        }
+        bad |= !isfinite(v.x) || !isfinite(v.y);
+        *reinterpret_cast<double2*>(dst + 2 * h) = v;
+      }
+    }
+  }
+  if (p.nonfinite && bad) atomicMax(p.nonfinite, b + p.batch_offset);
+}
+
 // C[b] = alpha * sum_s P[b][s] + beta * C[b], deterministic summation order.
 __global__ void k_splitk_reduce(GemmParams p);
 
