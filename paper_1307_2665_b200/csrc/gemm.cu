@@ -93,8 +93,14 @@ static int launch_cfg64(const GemmParams& p, cudaStream_t stream) {
   int split = 1;
   static const int allow = getenv("HPS_SPLITK") ? atoi(getenv("HPS_SPLITK")) : 1;
   const long long slots = 148LL * MINB;
-  if (allow && tiles < slots && p.K >= 4 * BK) {
+  static const int mode = getenv("HPS_SPLIT_MODE") ? atoi(getenv("HPS_SPLIT_MODE")) : 1;  // 1: measured better (r01)
+  if (mode == 0 && allow && tiles < slots && p.K >= 4 * BK) {
     split = (int)std::min<long long>((2 * slots + tiles - 1) / tiles, p.K / (2 * BK));
+    split = std::max(1, std::min(split, 16));
+    while (split > 1 && (long long)split * p.batch > 65535) --split;
+  }
+  if (mode == 1 && allow && 2 * tiles < slots && p.K >= 8 * BK) {  // about one wave
+    split = (int)std::min<long long>((slots + tiles - 1) / tiles, p.K / (4 * BK));
     split = std::max(1, std::min(split, 16));
     while (split > 1 && (long long)split * p.batch > 65535) --split;
   }
@@ -143,8 +149,11 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
   if (!vec) return launch_cfg<64, 64, 16, 2, 2, 3, false>(p, stream);  // any shape (e.g. q = 21)
   // 64 x 64 paired-fragment tiles, BK 16, 3 stages, 3 CTAs per SM: measured best of
   // {BK 16/32} x {2,3,4 stages} x {2,3,4 CTAs/SM} on the merge shapes (tools/gemm_variants.sh)
+  // Narrow row-gather GEMMs (the batched solve with b <= 64: one 64-column tile, small M,
+  // latency-bound on the index-then-row loads) measured 7-12 us per depth faster on the LDS.64
+  // 64 x 64 kernel below; at b = 256 the paired kernel wins (cfg5 solve 97.8 vs 104.3 ms).
   static const int v64 = getenv("HPS_GEMM64") ? atoi(getenv("HPS_GEMM64")) : 1;
-  if (v64) return launch_cfg64<16, 3, 3>(p, stream);
+  if (v64 && !(p.Bidx && p.N <= 64)) return launch_cfg64<16, 3, 3>(p, stream);
   double tiles128 = double((p.M + 127) / 128) * double((p.N + 127) / 128) * p.batch;
   // HPS_GEMM64=0: the previous tiling (128 x 128 x 16, 8 warps of 64 x 32, one CTA per SM)
   if (p.M >= 128 && p.N >= 128 && tiles128 >= 148.0) return launch_cfg<128, 128, 16, 2, 4, 4>(p, stream);

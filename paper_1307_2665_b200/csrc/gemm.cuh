@@ -247,24 +247,45 @@ __global__ void __launch_bounds__(128, MINB) dgemm64_kernel(GemmParams p) {
   const int kt0 = ks_idx * kt_per;
   const int ktiles = max(0, min(kt_all, kt0 + kt_per) - kt0);
 
+  // Each thread copies the same 4 A chunks and 4 B chunks (16 B) of every stage: source pointers
+  // and smem offsets are computed once and advanced by BK per k tile.
+  constexpr int NCA = BM * BK / 2 / 128, NCB = BK * BN / 2 / 128;
+  static_assert(NCA * 128 == BM * BK / 2 && NCB * 128 == BK * BN / 2, "chunks");
+  const double* a_src[NCA];
+  int a_off[NCA];
+  bool a_ok[NCA];
+#pragma unroll
+  for (int i = 0; i < NCA; ++i) {
+    const int c = tid + 128 * i, r = c / (BK / 2), cc = c % (BK / 2);
+    a_ok[i] = m0 + r < p.M;
+    a_src[i] = A + (long long)(a_ok[i] ? m0 + r : 0) * p.lda + (long long)kt0 * BK + 2 * cc;
+    a_off[i] = r * Cfg::SA + 2 * cc;
+  }
+  const double* b_src[NCB];
+  int b_off[NCB], b_row[NCB];
+  bool b_ok[NCB];
+#pragma unroll
+  for (int i = 0; i < NCB; ++i) {
+    const int c = tid + 128 * i, r = c / (BN / 2), cc = c % (BN / 2);
+    b_ok[i] = n0 + 2 * cc < p.N;
+    b_row[i] = r;
+    b_src[i] = B + (b_ok[i] ? n0 + 2 * cc : 0) + (Bidx ? 0 : ((long long)kt0 * BK + r) * p.ldb);
+    b_off[i] = r * Cfg::SB + 2 * cc;
+  }
+  const long long b_step = (long long)BK * p.ldb;
   auto load_stage = [&](int stage, int kt) {
-    const int k0 = (kt0 + kt) * BK;
     double* a_dst = sA + stage * Cfg::kStageA;
 #pragma unroll
-    for (int c = tid; c < BM * BK / 2; c += 128) {
-      const int r = c / (BK / 2), cc = c % (BK / 2);
-      const int gr = m0 + r;
-      const bool ok = gr < p.M;
-      cp_async16(a_dst + r * Cfg::SA + 2 * cc, A + (long long)(ok ? gr : 0) * p.lda + k0 + 2 * cc, ok);
-    }
+    for (int i = 0; i < NCA; ++i) cp_async16(a_dst + a_off[i], a_src[i] + kt * BK, a_ok[i]);
     double* b_dst = sB + stage * Cfg::kStageB;
+    if (Bidx) {
+      const int k0 = (kt0 + kt) * BK;
 #pragma unroll
-    for (int c = tid; c < BK * BN / 2; c += 128) {
-      const int r = c / (BN / 2), cc = c % (BN / 2);
-      const int gc = n0 + 2 * cc;
-      const bool ok = gc < p.N;
-      const long long row = Bidx ? (long long)Bidx[k0 + r] : (long long)(k0 + r);
-      cp_async16(b_dst + r * Cfg::SB + 2 * cc, B + row * p.ldb + (ok ? gc : 0), ok);
+      for (int i = 0; i < NCB; ++i)
+        cp_async16(b_dst + b_off[i], b_src[i] + (long long)Bidx[k0 + b_row[i]] * p.ldb, b_ok[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NCB; ++i) cp_async16(b_dst + b_off[i], b_src[i] + kt * b_step, b_ok[i]);
     }
   };
 
