@@ -18,6 +18,7 @@ __global__ void k_splitk_reduce(GemmParams p) {
     double* dst = p.C + b * p.strideC + (long long)r * p.ldc + c;
     double v = p.alpha * s;
     if (p.beta != 0.0) v += p.beta * *dst;
+    if (p.blk_j1a) v += blk_value(p, (int)b, r, c);
     if (p.nonfinite && !isfinite(v)) atomicMax(p.nonfinite, (int)b + p.batch_offset);
     *dst = v;
   }

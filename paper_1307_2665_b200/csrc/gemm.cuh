@@ -14,6 +14,21 @@
 
 namespace hps {
 
+// Children of merge b in a level-batched tree (merge.cu): T matrices at T + idx[2b]*stride and
+// T + idx[2b+1]*stride (idx null: children 2b, 2b+1), each m x m.
+struct ChildRef {
+  const double* T;
+  long long stride;
+  const int* idx;
+  int m;
+  __device__ __forceinline__ const double* a(int b) const {
+    return T + (long long)(idx ? idx[2 * b] : 2 * b) * stride;
+  }
+  __device__ __forceinline__ const double* bb(int b) const {
+    return T + (long long)(idx ? idx[2 * b + 1] : 2 * b + 1) * stride;
+  }
+};
+
 struct GemmParams {
   int M, N, K, batch;
   const double* A; long long lda, strideA;
@@ -25,7 +40,24 @@ struct GemmParams {
   int batch_offset = 0;  // added to the reported batch index (batch-chunked launches)
   int split = 1;         // split-K factor (blockIdx.z = batch * split + s)
   double* partial = nullptr;  // split > 1: raw partial sums [batch][split][M][N]
+  // Optional fused block-diagonal addend of the merge update T = blkdiag(Ta11, Tb22) + C S
+  // (replaces beta * C): for merge b (= batch index + batch_offset), n1 = M / 2,
+  // blk[r][c] = Ta[j1a[r]][j1a[c]] (r, c < n1), Tb[j2b[r-n1]][j2b[c-n1]] (r, c >= n1), else 0.
+  ChildRef blk{nullptr, 0, nullptr, 0};
+  const int* blk_j1a = nullptr;
+  const int* blk_j2b = nullptr;
 };
+
+__device__ __forceinline__ double blk_value(const GemmParams& p, int b, int r, int c) {
+  const int n1 = p.M >> 1;
+  const bool top = r < n1;
+  if ((c < n1) != top) return 0.0;
+  const int gb = b + p.batch_offset;
+  const double* src = top ? p.blk.a(gb) : p.blk.bb(gb);
+  const int rm = top ? p.blk_j1a[r] : p.blk_j2b[r - n1];
+  const int cm = top ? p.blk_j1a[c] : p.blk_j2b[c - n1];
+  return src[(long long)rm * p.blk.m + cm];
+}
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
 struct GemmCfg {
@@ -186,6 +218,7 @@ dgemm_dmma_kernel(GemmParams p) {
           if (c + h < p.N) {
             double v = p.alpha * acc[i][j][h];
             if (p.beta != 0.0) v += p.beta * dst[h];
+            if (p.blk_j1a) v += blk_value(p, b, r, c + h);
             bad |= !isfinite(v);
             dst[h] = v;
           }
@@ -198,6 +231,10 @@ dgemm_dmma_kernel(GemmParams p) {
         double2 o = *reinterpret_cast<const double2*>(dst);
         v.x += p.beta * o.x;
         v.y += p.beta * o.y;
+      }
+      if (p.blk_j1a) {
+        v.x += blk_value(p, b, r, c);
+        v.y += blk_value(p, b, r, c + 1);
       }
       bad |= !isfinite(v.x) || !isfinite(v.y);
       *reinterpret_cast<double2*>(dst) = v;
@@ -377,6 +414,10 @@ __global__ void __launch_bounds__(128, MINB) dgemm64_kernel(GemmParams p) {
           const double2 o = *reinterpret_cast<const double2*>(dst + 2 * h);
           v.x += p.beta * o.x;
           v.y += p.beta * o.y;
+        }
+        if (p.blk_j1a) {
+          v.x += blk_value(p, b, r, c + 2 * h);
+          v.y += blk_value(p, b, r, c + 2 * h + 1);
         }
         bad |= !isfinite(v.x) || !isfinite(v.y);
         *reinterpret_cast<double2*>(dst + 2 * h) = v;

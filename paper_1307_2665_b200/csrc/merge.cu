@@ -28,18 +28,7 @@ namespace hps {
 // ---------------------------------------------------------------------------------------------
 // Gathers: one warp per output row, lanes over columns (maps come in runs of q -> coalesced).
 // ---------------------------------------------------------------------------------------------
-struct ChildRef {
-  const double* T;
-  long long stride;
-  const int* idx;  // may be null: children of merge b are 2b, 2b+1
-  int m;           // child dimension
-  __device__ __forceinline__ const double* a(int b) const {
-    return T + (long long)(idx ? idx[2 * b] : 2 * b) * stride;
-  }
-  __device__ __forceinline__ const double* bb(int b) const {
-    return T + (long long)(idx ? idx[2 * b + 1] : 2 * b + 1) * stride;
-  }
-};
+// ChildRef (children of merge b) lives in gemm.cuh: the T GEMM epilogue reads the blkdiag through it.
 
 __global__ void k_gather_xr(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b,
                             const int* __restrict__ j3a, const int* __restrict__ j3b, int n3, int ne,
@@ -65,9 +54,9 @@ __global__ void k_gather_xr(ChildRef ch, const int* __restrict__ j1a, const int*
   for (int c = lane; c < n1; c += 32) Rr[n1 + c] = Tb[j2b[c]];
 }
 
-__global__ void k_gather_ct(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b,
-                            const int* __restrict__ j3a, const int* __restrict__ j3b, int n3, int ne,
-                            double* __restrict__ Cm, double* __restrict__ T) {
+__global__ void k_gather_c(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b,
+                           const int* __restrict__ j3a, const int* __restrict__ j3b, int n3, int ne,
+                           double* __restrict__ Cm) {
   const int b = blockIdx.x;
   const int r = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -76,15 +65,8 @@ __global__ void k_gather_ct(ChildRef ch, const int* __restrict__ j1a, const int*
   const bool top = r < n1;
   const double* src = top ? ch.a(b) + (long long)j1a[r] * ch.m : ch.bb(b) + (long long)j2b[r - n1] * ch.m;
   const int* j3 = top ? j3a : j3b;
-  const int* jk = top ? j1a : j2b;
   double* Cr = Cm + ((long long)b * ne + r) * n3;
-  double* Tr = T + ((long long)b * ne + r) * ne;
   for (int c = lane; c < n3; c += 32) Cr[c] = src[j3[c]];
-  const int own = top ? 0 : n1;
-  for (int c = lane; c < n1; c += 32) {
-    Tr[own + c] = src[jk[c]];
-    Tr[(n1 - own) + c] = 0.0;
-  }
 }
 
 __device__ __forceinline__ int g_of(int lane) { return lane >> 2; }
@@ -496,7 +478,7 @@ extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const d
   k_gather_xr<<<dim3(nbatch, (n3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, X, R,
                                                         deflate ? diagmax : nullptr);
   HPS_LAUNCH_CHECK();
-  k_gather_ct<<<dim3(nbatch, (ne + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, Cm, T_out);
+  k_gather_c<<<dim3(nbatch, (ne + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, Cm);
   HPS_LAUNCH_CHECK();
   const double* vs = vmode;
   const double* ve = vmode + q;
@@ -508,8 +490,14 @@ extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const d
   HPS_TRY(gemm(n3, ne, n3, nbatch, 1.0, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, 0.0, S_out, ne,
                (long long)n3 * ne, st, status));
   // nonfinite flag reports merge index; shift by status_base happens on the host side
-  HPS_TRY(gemm(ne, ne, n3, nbatch, 1.0, Cm, n3, (long long)ne * n3, S_out, ne, (long long)n3 * ne, 1.0, T_out, ne,
-               (long long)ne * ne, st));
+  {  // T = blkdiag(Ta[j1a, j1a], Tb[j2b, j2b]) + C S, the blkdiag read by the GEMM epilogue
+    GemmParams gp{ne, ne, n3, nbatch, Cm, n3, (long long)ne * n3, S_out, ne, (long long)n3 * ne, nullptr, 0,
+                  T_out, ne, (long long)ne * ne, 1.0, 0.0, nullptr};
+    gp.blk = ch;
+    gp.blk_j1a = j1a;
+    gp.blk_j2b = j2b;
+    HPS_TRY(dgemm_launch(gp, st));
+  }
   return HPS_OK;
 }
 
