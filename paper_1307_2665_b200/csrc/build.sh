@@ -7,14 +7,19 @@ NVCC="${NVCC:-nvcc}"
 FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
        -I"${here}" -I"${here}/../../include" --expt-relaxed-constexpr ${HPS_NVCC_EXTRA:-})
 objs=()
+pids=()
 mkdir -p "${HPS_OBJ:-${here}/../build_obj}"
 for f in capi gemm merge solve leaf leaf3 group; do
   o="${HPS_OBJ:-${here}/../build_obj}/${f}.o"
   if [[ ! -f "$o" || "${here}/${f}.cu" -nt "$o" || "${here}/common.cuh" -nt "$o" || "${here}/gemm.cuh" -nt "$o" || "${here}/leaf.cuh" -nt "$o" ]]; then
+    rm -f "$o"
     "$NVCC" "${FLAGS[@]}" -c "${here}/${f}.cu" -o "$o" &
+    pids+=($!)
   fi
   objs+=("$o")
 done
-wait
+for pid in "${pids[@]}"; do
+  wait "$pid" || { echo "build.sh: compile failed" >&2; exit 1; }
+done
 "$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$out" "${objs[@]}" -lcudart_static -lrt -ldl -lpthread
 echo "built $out"

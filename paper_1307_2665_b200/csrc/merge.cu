@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -211,6 +212,256 @@ __global__ void __launch_bounds__(W * 32) k_gj_inverse(double* X, long long lda,
   if (singular && status && threadIdx.x == 0) atomicMax(status, status_base + b);
 }
 
+// Blocked Gauss-Jordan inverse (n <= 8*NT), same pivoting rule as k_gj_inverse (partial pivoting,
+// ties to the smallest row, implicit row order), built for a short critical path:
+//  * the matrix lives in registers in DMMA C-fragment layout: warp w owns columns 16w..16w+15,
+//    lane (g, tq) holds a[r][c][h] = A(8r + g, 16w + 8c + 2tq + h);
+//  * pivots go in blocks of 8 (one 8-column tile). The warp owning the tile factors it alone
+//    (REDUX argmax, shuffles, no CTA barrier). A block of GJ steps acts on every other column as
+//    I + W E_P^T, with W = (panel after the block) - E_P (E_P: unit vectors at the 8 pivot rows);
+//  * every other tile then takes A += W A[P, :] on DMMA (k = 8: two m8n8k4 k-steps);
+//  * look-ahead: the owner of the next tile updates that tile first and factors it while the
+//    other warps run their updates, so one __syncthreads per 8 pivots.
+// Sizes that are not a multiple of 8 are padded with identity rows/columns.
+#ifdef HPS_GJ_PROFILE
+__device__ long long g_gj_prof[8];
+extern "C" int hps_debug_gj_profile(long long* out, int reset) {
+  if (reset) {
+    long long z[8] = {};
+    cudaMemcpyToSymbol(g_gj_prof, z, sizeof(z));
+    return 0;
+  }
+  cudaMemcpyFromSymbol(out, g_gj_prof, sizeof(long long) * 8);
+  return 0;
+}
+#endif
+template <int NT>
+__global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, long long strideX, int n, int* status,
+                                                   int status_base) {
+  constexpr int NM = 8 * NT, W = NT / 2, RPL = NM / 32 > 0 ? NM / 32 : 1;
+  static_assert(NT % 2 == 0 && W >= 1, "NT");
+  __shared__ double sW[2][NM][9];     // panel of the current / next block after its 8 GJ steps
+  __shared__ int sP[2][8];            // pivot rows of the block
+  __shared__ double sAP[W][8][17];    // per warp: A[P, its 16 columns] before the block update
+  __shared__ double sDum[10];         // store sink for lanes that do not hold a staged row (never read)
+  __shared__ unsigned char usedrow[NM];
+  __shared__ int pivrow[NM], rowstep[NM];
+  __shared__ int s_sing;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tq = lane & 3;
+  double* Xb = X + (long long)blockIdx.x * strideX;
+  double a[NT][2][2];
+#pragma unroll
+  for (int r = 0; r < NT; ++r)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int R = 8 * r + g, C = 16 * warp + 8 * c + 2 * tq + h;
+        a[r][c][h] = (R < n && C < n) ? Xb[(long long)R * lda + C] : (R == C ? 1.0 : 0.0);
+      }
+  for (int i = threadIdx.x; i < NM; i += blockDim.x) usedrow[i] = 0;
+  if (threadIdx.x == 0) s_sing = 0;
+
+  // Factor the 8 columns of my tile C (block kb) with 8 sequential GJ steps, one warp, row layout:
+  // the tile goes through shared memory so lane l holds rows l + 32i, all 8 columns.
+  auto panel = [&](auto cc, int kb) {
+    constexpr int C = decltype(cc)::value;
+    double(*Pb)[9] = sW[kb & 1];
+#pragma unroll
+    for (int r = 0; r < NT; ++r)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) Pb[8 * r + g][2 * tq + h] = a[r][C][h];
+    __syncwarp();
+    double pr[RPL][8];
+    bool used[RPL];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int R = lane + 32 * i;
+      used[i] = R >= NM || usedrow[R];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pr[i][j] = R < NM ? Pb[R][j] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      unsigned long long best = 0ull;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const unsigned long long key = used[i] ? 0ull : (unsigned long long)__double_as_longlong(fabs(pr[i][t]));
+        const int idx = used[i] ? 0x7fffffff : lane + 32 * i;
+        if (key > best || (key == best && idx < bi)) { best = key; bi = idx; }
+      }
+      const unsigned hi = (unsigned)(best >> 32), lo = (unsigned)best;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+      const int p = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)bi : 0xffffffffu);
+      const int pl = p & 31, pi = p >> 5;
+      double rp[8];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+        if (pi == i) {  // warp-uniform
+          if (lane == pl) used[i] = true;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rp[j] = __shfl_sync(0xffffffffu, pr[i][j], pl);
+        }
+      const double piv = rp[t];
+      const double inv = fast_rcp(piv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) rp[j] = j == t ? inv : rp[j] * inv;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const double f = pr[i][t];
+        pr[i][t] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pr[i][j] = fma(-f, rp[j], pr[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const bool mine = pi == i && lane == pl;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pr[i][j] = mine ? rp[j] : pr[i][j];
+      }
+      if (lane == 0) {
+        sP[kb & 1][t] = p;
+        usedrow[p] = 1;
+        pivrow[8 * kb + t] = p;
+        rowstep[p] = 8 * kb + t;
+        if (piv == 0.0) s_sing = 1;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int R = lane + 32 * i;
+      if (R < NM)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) Pb[R][j] = pr[i][j];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NT; ++r)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) a[r][C][h] = Pb[8 * r + g][2 * tq + h];
+  };
+  // A[:, my tile C] += Panel(kb) A[P(kb), tile C]; the pivot rows were zeroed when staged
+  auto update_tile = [&](auto cc, int kb) {
+    constexpr int C = decltype(cc)::value;
+    const double(*Pb)[9] = sW[kb & 1];
+    const double b0 = sAP[warp][tq][8 * C + g], b1 = sAP[warp][4 + tq][8 * C + g];
+#pragma unroll
+    for (int r = 0; r < NT; ++r) {
+      dmma_8x8x4(a[r][C][0], a[r][C][1], Pb[8 * r + g][tq], b0);
+      dmma_8x8x4(a[r][C][0], a[r][C][1], Pb[8 * r + g][4 + tq], b1);
+    }
+  };
+  using C0 = std::integral_constant<int, 0>;
+  using C1 = std::integral_constant<int, 1>;
+
+  __syncthreads();
+#ifdef HPS_GJ_PROFILE
+  const long long p00 = clock64();
+#endif
+  if (warp == 0) panel(C0{}, 0);
+#ifdef HPS_GJ_PROFILE
+  if (warp == 0 && lane == 0 && blockIdx.x == 0) atomicAdd((unsigned long long*)&g_gj_prof[6], (unsigned long long)(clock64() - p00));
+#endif
+  __syncthreads();
+#ifdef HPS_GJ_PROFILE
+  long long pacc[6] = {0, 0, 0, 0, 0, 0};
+#endif
+  for (int kb = 0; kb < NT; ++kb) {
+#ifdef HPS_GJ_PROFILE
+    long long q0 = clock64(), q1 = q0, q2 = q0, q3 = q0;
+#endif
+    const int own = kb >> 1, ownc = kb & 1;  // tile of block kb: already final
+    const bool keep0 = warp == own && ownc == 0, keep1 = warp == own && ownc == 1;
+    // stage my pivot rows of block kb, zeroing them in the tiles that take the update:
+    // a_new = a + Panel A_P on non-pivot rows, a_new = Panel A_P on pivot rows (no cancellation)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int p = sP[kb & 1][t], rp = p >> 3;
+      const bool mine = g == (p & 7);
+      // lanes not holding row p write to a dummy slot: no divergent branch
+      double* d = mine ? &sAP[warp][t][2 * tq] : sDum;
+      const bool z0 = mine && !keep0, z1 = mine && !keep1;
+      switch (rp) {  // warp-uniform
+#define HPS_GJ_STAGE(R)                                                       \
+  case R:                                                                     \
+    if constexpr (R < NT) {                                                   \
+      d[0] = a[R][0][0];                                                      \
+      d[1] = a[R][0][1];                                                      \
+      d[8] = a[R][1][0];                                                      \
+      d[9] = a[R][1][1];                                                      \
+      a[R][0][0] = z0 ? 0.0 : a[R][0][0];                                     \
+      a[R][0][1] = z0 ? 0.0 : a[R][0][1];                                     \
+      a[R][1][0] = z1 ? 0.0 : a[R][1][0];                                     \
+      a[R][1][1] = z1 ? 0.0 : a[R][1][1];                                     \
+    }                                                                         \
+    break;
+        HPS_GJ_STAGE(0) HPS_GJ_STAGE(1) HPS_GJ_STAGE(2) HPS_GJ_STAGE(3)
+        HPS_GJ_STAGE(4) HPS_GJ_STAGE(5) HPS_GJ_STAGE(6) HPS_GJ_STAGE(7)
+        HPS_GJ_STAGE(8) HPS_GJ_STAGE(9) HPS_GJ_STAGE(10) HPS_GJ_STAGE(11)
+        HPS_GJ_STAGE(12) HPS_GJ_STAGE(13) HPS_GJ_STAGE(14) HPS_GJ_STAGE(15)
+#undef HPS_GJ_STAGE
+        default: break;
+      }
+    }
+    __syncwarp();
+#ifdef HPS_GJ_PROFILE
+    q1 = clock64();
+#endif
+    const int nx = kb + 1, nown = nx >> 1, nownc = nx & 1;
+    if (nx < NT && warp == nown) {
+      if (nownc == 0) {
+        update_tile(C0{}, kb);
+#ifdef HPS_GJ_PROFILE
+        q2 = clock64();
+#endif
+        panel(C0{}, nx);
+#ifdef HPS_GJ_PROFILE
+        q3 = clock64();
+#endif
+        if (!keep1) update_tile(C1{}, kb);
+      } else {
+        update_tile(C1{}, kb);
+#ifdef HPS_GJ_PROFILE
+        q2 = clock64();
+#endif
+        panel(C1{}, nx);
+#ifdef HPS_GJ_PROFILE
+        q3 = clock64();
+#endif
+        if (!keep0) update_tile(C0{}, kb);
+      }
+    } else {
+      if (!keep0) update_tile(C0{}, kb);
+      if (!keep1) update_tile(C1{}, kb);
+    }
+#ifdef HPS_GJ_PROFILE
+    long long q4 = clock64();
+#endif
+    __syncthreads();
+#ifdef HPS_GJ_PROFILE
+    long long q5 = clock64();
+    if (warp == nown && nx < NT) { pacc[0] += q1 - q0; pacc[1] += q2 - q1; pacc[2] += q3 - q2; pacc[3] += q4 - q3; pacc[4] += q5 - q4; pacc[5] += q5 - q0; }
+#endif
+  }
+#ifdef HPS_GJ_PROFILE
+  if (lane == 0 && blockIdx.x == 0)
+    for (int q = 0; q < 6; ++q) atomicAdd((unsigned long long*)&g_gj_prof[q], (unsigned long long)pacc[q]);
+#endif
+  // inv(X)[rowstep[R]][pivrow[C]] = B[R][C]
+#pragma unroll
+  for (int r = 0; r < NT; ++r)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int R = 8 * r + g, C = 16 * warp + 8 * c + 2 * tq + h;
+        if (R < n && C < n) Xb[(long long)rowstep[R] * lda + pivrow[C]] = a[r][c][h];
+      }
+  if (s_sing && status && threadIdx.x == 0) atomicMax(status, status_base + (int)blockIdx.x);
+}
+
 // Fused merge for small interfaces (n3 <= 32, ne <= 192: the deepest depths), one CTA per merge:
 //   [X | R] gathered into shared memory -> deflate X -> Gauss-Jordan with partial pivoting on the
 //   augmented rows (so the right block becomes S = X^-1 R directly) -> S out ->
@@ -362,23 +613,31 @@ __global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs
 // In-place batched inverse of n x n blocks (n <= 128), stride lda.
 static int inverse_small(double* X, long long lda, long long strideX, int n, int batch, int* status,
                          int status_base, cudaStream_t st) {
+  if (n > 128) {
+    set_error("inverse_small: n=%d > 128", n);
+    return HPS_ERR_ARG;
+  }
+  static const int v = getenv("HPS_GJ_V") ? atoi(getenv("HPS_GJ_V")) : 3;
+  if (v == 3) {  // blocked GJ (8-pivot panels, DMMA block updates)
+    if (n <= 16)
+      k_gj_blk<2><<<batch, 32, 0, st>>>(X, lda, strideX, n, status, status_base);
+    else if (n <= 32)
+      k_gj_blk<4><<<batch, 64, 0, st>>>(X, lda, strideX, n, status, status_base);
+    else if (n <= 64)
+      k_gj_blk<8><<<batch, 128, 0, st>>>(X, lda, strideX, n, status, status_base);
+    else
+      k_gj_blk<16><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
+    HPS_LAUNCH_CHECK();
+    return HPS_OK;
+  }
   if (n <= 16)
     k_gj_inverse<1, 8, 2><<<batch, 64, 0, st>>>(X, lda, strideX, n, status, status_base);
   else if (n <= 32)
     k_gj_inverse<1, 8, 4><<<batch, 128, 0, st>>>(X, lda, strideX, n, status, status_base);
   else if (n <= 64)
     k_gj_inverse<2, 8, 8><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
-  else if (n <= 128) {
-    static const int w16 = getenv("HPS_GJ128_W") ? atoi(getenv("HPS_GJ128_W")) : 8;  // 16 warps measured slower
-    if (w16 == 16)
-      k_gj_inverse<4, 8, 16><<<batch, 512, 0, st>>>(X, lda, strideX, n, status, status_base);
-    else
-      k_gj_inverse<4, 16, 8><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
-  }
-  else {
-    set_error("inverse_small: n=%d > 128", n);
-    return HPS_ERR_ARG;
-  }
+  else
+    k_gj_inverse<4, 16, 8><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
   HPS_LAUNCH_CHECK();
   return HPS_OK;
 }
@@ -402,7 +661,8 @@ static int gemm(int M, int N, int K, int batch, double alpha, const double* A, l
 // Base blocks (<= 128) use pivoted Gauss-Jordan in shared memory.
 static int inverse_rec(double* A, long long lda, long long strideA, int n, int batch, double* tmp, int* status,
                        int status_base, cudaStream_t st) {
-  if (n <= 128) return inverse_small(A, lda, strideA, n, batch, status, status_base, st);
+  static const int base = getenv("HPS_INV_BASE") ? atoi(getenv("HPS_INV_BASE")) : 128;
+  if (n <= base || n <= 16) return inverse_small(A, lda, strideA, n, batch, status, status_base, st);
   const int h = n / 2, h2 = n - h;  // unequal halves allowed (q = 21 gives n3 = 21 * 2^j)
   double* A11 = A;
   double* A12 = A + h;
@@ -424,7 +684,7 @@ static int inverse_rec(double* A, long long lda, long long strideA, int n, int b
 }
 
 static size_t inverse_rec_tmp_doubles(int n, int batch) {
-  if (n <= 128) return 0;
+  if (n <= 16) return 0;  // (workspace sized for the smallest recursion base, HPS_INV_BASE)
   const int h = n / 2, h2 = n - h;
   return 2ull * batch * h * h2 + std::max(inverse_rec_tmp_doubles(h, batch), inverse_rec_tmp_doubles(h2, batch));
 }
