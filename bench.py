@@ -210,9 +210,9 @@ def main():
         return
 
     import torch
-    from oracle import hps_oracle as O
     import paper_1307_2665_b200 as P
     from paper_1307_2665_b200 import _native, solver
+    from paper_1307_2665_b200 import work as Wk
 
     if world > 1 or args.force_distributed:
         import torch.distributed as dist
@@ -276,10 +276,9 @@ def main():
 
     # ---- roofline of the dominant stage ----
     peak, peak_src = fp64_peak()
-    stage_flops = {"leaf": inp.ngroups * O.leaf_flops(q)}
+    stage_flops = {"leaf": inp.ngroups * Wk.leaf_flops(q)}
     for d in range(2 * L):
-        n3, ne = O.depth_sizes(L, q, d)
-        stage_flops[f"merge_d{d}"] = (2 ** d) * (2 / 3 * n3 ** 3 + 2 * n3 * n3 * ne + 2 * n3 * ne * ne)
+        stage_flops[f"merge_d{d}"] = Wk.merge_flops_depth(L, q, d)
     stage_ms = {k: float(np.mean(v)) * 1e3 for k, v in stages.items()}
     dom = max(stage_ms, key=stage_ms.get)
     ach = stage_flops[dom] / (stage_ms[dom] / 1e3) / 1e12
@@ -287,9 +286,10 @@ def main():
         "hps::k_leaf16" if q == 16 else "hps::k_leaf")
     kernels = {"leaf": leaf_kernel}.get(dom, "hps_merge_level (gather, deflate, k_gj_inverse, dgemm_dmma)")
     build_flops = sum(stage_flops.values())
-    solve_flops = O.solve_flops(L, q, b)
-    S_bytes = sum((2 ** d) * O.depth_sizes(L, q, d)[0] * O.depth_sizes(L, q, d)[1] * 8 for d in range(2 * L))
+    solve_flops = Wk.solve_flops(L, q, b)
+    S_bytes = Wk.solve_S_bytes(L, q)
     hpeak, hsrc = hbm_peak()
+    t_roof = Wk.build_roofline_seconds(L, q, inp.ngroups, peak, hpeak)
     traffic, traffic_src = None, None  # DRAM bytes per launch of the dominant kernel (committed ncu capture)
     prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "leaf16v3_ncu_r01.json")
     if dom == "leaf" and leaf_kernel == "hps::k_leaf16v3" and os.path.exists(prof):
@@ -303,6 +303,8 @@ def main():
         "traffic_source": traffic_src,
         "kernel": dom, "kernels": kernels, "peak_source": peak_src,
         "stage_ms": stage_ms, "build_tflops": build_flops / tb / 1e12, "build_frac": build_flops / tb / 1e12 / peak,
+        "build_roofline": {"t_roof_ms": t_roof * 1e3, "t_meas_ms": tb * 1e3, "frac": t_roof / tb,
+                           "model": "sum over stages of max(flop/FP64 peak, bytes/HBM peak), SURVEY.md 8d"},
         "solve": {"tflops": solve_flops / ts / 1e12, "frac_fp64": solve_flops / ts / 1e12 / peak,
                   "gbs_S_stream": S_bytes / ts / 1e9, "frac_hbm": S_bytes / ts / 1e9 / hpeak, "hbm_peak_source": hsrc},
     }

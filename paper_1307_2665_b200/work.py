@@ -1,0 +1,56 @@
+"""Algorithmic work model of the hot path: flop and minimum-byte counts per stage,
+used by bench.py's roofline. Standard LAPACK counts; leaf work is per distinct coefficient group,
+as in the reference (solver.py:208-246)."""
+
+
+def depth_sizes(L, q, d):
+    """(n3, ne) of every parent at depth d (0 = root) of a 4^L-leaf tree with q Gauss nodes per
+    leaf side: even depths split vertically (square parents), odd depths horizontally."""
+    j = d // 2
+    if d % 2 == 0:
+        side = 2 ** (L - j)
+        return side * q, 4 * side * q
+    w, h = 2 ** (L - j - 1), 2 ** (L - j)
+    return w * q, 2 * (w + h) * q
+
+
+def leaf_flops(p):
+    """Per group: LU of A_ii, solve for the n_b + 1 right-hand sides (A_ie and the probe),
+    T1 = L43i Psi and T = T1 L1."""
+    ni, nb, ng = (p - 2) ** 2, 4 * (p - 1), 4 * p
+    return 2.0 / 3.0 * ni ** 3 + 2.0 * ni ** 2 * (nb + 1) + 2.0 * ng * ni * nb + 2.0 * ng * nb * ng
+
+
+def leaf_bytes(p, nfields=6):
+    """Per group: coefficient samples in, T and Psi out."""
+    ni, nb, ng = (p - 2) ** 2, 4 * (p - 1), 4 * p
+    return 8.0 * (nfields * p * p + ng * ng + ni * nb)
+
+
+def merge_flops_depth(L, q, d):
+    n3, ne = depth_sizes(L, q, d)
+    return (2 ** d) * (2.0 / 3.0 * n3 ** 3 + 2.0 * n3 ** 2 * ne + 2.0 * n3 * ne ** 2)
+
+
+def merge_bytes_depth(L, q, d):
+    """Children's T in (two m x m, m = ne/2 + n3), S and T out."""
+    n3, ne = depth_sizes(L, q, d)
+    m = ne // 2 + n3
+    return (2 ** d) * 8.0 * (2 * m * m + n3 * ne + ne * ne)
+
+
+def solve_flops(L, q, b):
+    return 2.0 * b * sum((2 ** d) * depth_sizes(L, q, d)[0] * depth_sizes(L, q, d)[1] for d in range(2 * L))
+
+
+def solve_S_bytes(L, q):
+    return 8.0 * sum((2 ** d) * depth_sizes(L, q, d)[0] * depth_sizes(L, q, d)[1] for d in range(2 * L))
+
+
+def build_roofline_seconds(L, q, ngroups, f64_tflops, hbm_gbs):
+    """t_roof = sum over stages of max(flop / FP64 peak, bytes / HBM peak)."""
+    F, B = f64_tflops * 1e12, hbm_gbs * 1e9
+    t = max(ngroups * leaf_flops(q) / F, ngroups * leaf_bytes(q) / B)
+    for d in range(2 * L):
+        t += max(merge_flops_depth(L, q, d) / F, merge_bytes_depth(L, q, d) / B)
+    return t

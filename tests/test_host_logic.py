@@ -93,3 +93,18 @@ def test_boundary_data_generators():
 
 def test_unknowns_definition():
     assert O.unknowns(6, 16) == 1048576 and O.unknowns(9, 16) == 67108864
+
+
+def test_work_model_matches_oracle_counts():
+    # bench.py's roofline uses paper_1307_2665_b200.work (no oracle import on the measured path);
+    # it must agree with the oracle's LAPACK-count restatement
+    from paper_1307_2665_b200 import work as W
+    for L in (2, 4, 6, 9):
+        for d in range(2 * L):
+            assert W.depth_sizes(L, 16, d) == O.depth_sizes(L, 16, d)
+        assert abs(sum(W.merge_flops_depth(L, 16, d) for d in range(2 * L)) - O.merge_flops(L, 16)) < 1e-6 * O.merge_flops(L, 16)
+        assert abs(W.solve_flops(L, 16, 64) - O.solve_flops(L, 16, 64)) < 1.0
+    assert W.leaf_flops(16) == O.leaf_flops(16)
+    # SURVEY.md §8d build totals: cfg2 1.79e11 flop
+    tot = 4096 * W.leaf_flops(16) + sum(W.merge_flops_depth(6, 16, d) for d in range(12))
+    assert abs(tot - 1.79e11) / 1.79e11 < 0.01

@@ -4,7 +4,7 @@ sys.path.insert(0, ".")
 import numpy as np, torch
 import paper_1307_2665_b200 as P
 from paper_1307_2665_b200 import solver, problems
-from oracle import hps_oracle as O
+from paper_1307_2665_b200 import work as O
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 L = int(sys.argv[2]) if len(sys.argv) > 2 else problems.CONFIGS[cfg].L
 c = problems.CONFIGS[cfg]
