@@ -17,6 +17,10 @@
  *   hps_dgemm_batched <- the BLAS dgemm behind `@` (merge.py:118, solver.py:71 apply_global_dtn)
  *   hps_leaf_hash / hps_leaf_verify <- the leaf grouping of solver._leaf_stage, solver.py:208-222
  *                       (np.unique over the stacked coefficient sample rows)
+ *   hps_leaf_fields / hps_eval_points <- _leaf_field + the barycentric evaluation of post_process and
+ *                       boundary_flux_at, solver.py:349-400
+ *   hps_gauge_sides / hps_gauge_gather <- (new) Gauss-node solution
+ *                       re-tabulated from the leaf fields with the L4 blocks (leafops.py:191-198)
  */
 #ifndef HPS_B200_H
 #define HPS_B200_H
@@ -91,6 +95,25 @@ int hps_leaf_hash(int n_leaf, int row_len, int nfields, const double* const* fie
                   unsigned long long* hash, void* stream);
 int hps_leaf_verify(int n_leaf, int row_len, int nfields, const double* const* fields,
                     const long long* rep_of, int* mismatch, void* stream);
+
+/* Post-processing (solver.py:349-400). U: N x ldu node-major solution (nrhs columns used).
+ * hps_leaf_fields: for s < nlist, leaf = leaves[s]: W[s][i*p+j][r] (ldw = nrhs) = the p x p Chebyshev
+ *   field of RHS r: w_e = L1 u[leaf_Ie[leaf][0..4p)], w_i = Psi[gid[leaf]] w_e, scattered by J_e / J_i.
+ *   L1: 4(p-1) x 4p; Psi: groups x (p-2)^2 x 4(p-1).
+ * hps_eval_points: out[t][r] = sum_ij rx[t][i] W[slot[t]][i*p+j][r] ry[t][j] (rx, ry: npts x p).
+ * hps_gauge_sides: side[s][k][r] = Gauss value at the k-th I_e node of listed leaf s re-tabulated from
+ *   W[s] (sides S, E, N, W: Qx W[:,0], Qy W[p-1,:], Qx W[:,p-1], Qy W[0,:]; Qx, Qy: p x p).
+ * hps_gauge_gather: u_out[node][r] = mean of side rows src[2 node], src[2 node + 1] (-1: absent);
+ *   src[2 node] == -1 keeps u_in[node][r]. */
+int hps_leaf_fields(int nlist, int p, const double* U, int ldu, int nrhs, const int* leaves,
+                    const int* leaf_Ie, const int* gid, const double* L1, const double* Psi,
+                    const int* J_i, const int* J_e, double* W, void* stream);
+int hps_eval_points(int npts, int p, const double* W, int nrhs, const int* slot, const double* rx,
+                    const double* ry, double* out, void* stream);
+int hps_gauge_sides(int nlist, int p, const double* W, int nrhs, const double* Qx, const double* Qy,
+                    double* side, void* stream);
+int hps_gauge_gather(int N, int nrhs, const double* side, const int* src, const double* u_in,
+                     int ldu_in, double* u_out, int ldu_out, void* stream);
 
 #ifdef __cplusplus
 }

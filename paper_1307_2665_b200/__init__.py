@@ -10,7 +10,7 @@ from . import errors, grid, instrumentation, leafops, problems, solver  # noqa: 
 from .errors import ConfigError, LeafResonanceError, MergeResonanceError, SolverError  # noqa: F401
 from .grid import BoxTree, GlobalNodeSet, Rectangle, build_tree  # noqa: F401
 from .leafops import CoefficientField, LeafGeometry  # noqa: F401
-from .solver import (SolverState, apply_global_dtn, boundary_flux_at, build, memory_report,  # noqa: F401
-                     post_process, solve, solve_device)
+from .solver import (Pipeline, SolverState, apply_global_dtn, boundary_flux_at, build,  # noqa: F401
+                     gauge_fixed_solution, leaf_fields, memory_report, post_process, solve, solve_device)
 
 __version__ = "0.1.0"

@@ -25,7 +25,7 @@ HPS_ERR_ARG = 5
 EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_launch_count", "hps_leaf_workspace_bytes",
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
            "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched", "hps_leaf_hash",
-           "hps_leaf_verify")
+           "hps_leaf_verify", "hps_leaf_fields", "hps_eval_points", "hps_gauge_sides", "hps_gauge_gather")
 
 _lib = None
 
@@ -73,6 +73,15 @@ def load():
     lib.hps_leaf_hash.restype = c_int
     lib.hps_leaf_verify.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_dp), c_dp, c_dp, c_dp]
     lib.hps_leaf_verify.restype = c_int
+    lib.hps_leaf_fields.argtypes = [c_int, c_int, c_dp, c_int, c_int, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp,
+                                    c_dp, c_dp]
+    lib.hps_leaf_fields.restype = c_int
+    lib.hps_eval_points.argtypes = [c_int, c_int, c_dp, c_int, c_dp, c_dp, c_dp, c_dp, c_dp]
+    lib.hps_eval_points.restype = c_int
+    lib.hps_gauge_sides.argtypes = [c_int, c_int, c_dp, c_int, c_dp, c_dp, c_dp, c_dp]
+    lib.hps_gauge_sides.restype = c_int
+    lib.hps_gauge_gather.argtypes = [c_int, c_int, c_dp, c_dp, c_dp, c_int, c_dp, c_int, c_dp]
+    lib.hps_gauge_gather.restype = c_int
     _lib = lib
     return lib
 

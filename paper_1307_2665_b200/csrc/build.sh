@@ -9,7 +9,7 @@ FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompil
 objs=()
 pids=()
 mkdir -p "${HPS_OBJ:-${here}/../build_obj}"
-for f in capi gemm merge solve leaf leaf3 group; do
+for f in capi gemm merge solve leaf leaf3 group post; do
   o="${HPS_OBJ:-${here}/../build_obj}/${f}.o"
   if [[ ! -f "$o" || "${here}/${f}.cu" -nt "$o" || "${here}/common.cuh" -nt "$o" || "${here}/gemm.cuh" -nt "$o" || "${here}/leaf.cuh" -nt "$o" ]]; then
     rm -f "$o"

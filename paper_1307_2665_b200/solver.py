@@ -42,6 +42,9 @@ __all__ = [
     "apply_global_dtn",
     "post_process",
     "boundary_flux_at",
+    "leaf_fields",
+    "gauge_fixed_solution",
+    "Pipeline",
     "memory_report",
 ]
 
@@ -748,68 +751,197 @@ def apply_global_dtn(state, f):
 
 
 # ----------------------------------------------------------------------------------------------
-# Post-processing on the host (solver.py:330-432); these read the lazily materialised state
+# Post-processing on the device (solver.py:330-400): per-leaf Chebyshev
+# fields from the solution (hps_leaf_fields), point evaluation (hps_eval_points), and the
+# gauge-fixed Gauss-node solution re-tabulated from the fields (hps_gauge_sides / _gather).
 # ----------------------------------------------------------------------------------------------
-def _owning_leaf(state, x, y):
-    tree = state.tree
+class _PostTables:
+    """Per-(layout, geometry, device) tables of the post-processing kernels."""
+
+    _cache = {}
+
+    @classmethod
+    def get(cls, lay, geom, device):
+        key = (id(lay), geom.p, geom.width, geom.height, str(device))
+        v = cls._cache.get(key)
+        if v is None:
+            v = cls._cache[key] = cls(lay, geom, device)
+        return v
+
+    def __init__(self, lay, geom, device):
+        torch = _torch()
+        dev = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
+        self.leaf_Ie = dev(lay.leaf_I_e, np.int32)
+        self.L1 = dev(geom.L1, np.float64)
+        self.J_i = dev(geom.J_i, np.int32)
+        self.J_e = dev(geom.J_e, np.int32)
+        self.Qx = dev(geom.Qx, np.float64)
+        self.Qy = dev(geom.Qy, np.float64)
+        # owners of every node: rows leaf * 4q + k of the side table; outer-boundary nodes have one
+        # owner and keep the Dirichlet data (src -1)
+        flat = np.ascontiguousarray(lay.leaf_I_e).reshape(-1)
+        order = np.argsort(flat, kind="stable")
+        counts = np.bincount(flat, minlength=lay.N)
+        start = np.concatenate([[0], np.cumsum(counts)[:-1]])
+        src = np.full((lay.N, 2), -1, dtype=np.int32)
+        two = counts == 2
+        src[two, 0] = order[start[two]]
+        src[two, 1] = order[start[two] + 1]
+        self.src = dev(src, np.int32)
+        cells = np.asarray(lay.leaf_cells)
+        n = 1 << lay.L
+        self.cell_leaf = np.empty((n, n), dtype=np.int64)
+        self.cell_leaf[cells[:, 0], cells[:, 1]] = np.arange(cells.shape[0])
+
+
+def _gid_dev(state):
+    g = getattr(state, "_gid_dev", None)
+    if g is None:
+        torch = _torch()
+        g = torch.from_numpy(np.ascontiguousarray(state.leaf_group, dtype=np.int32)).to(state.device)
+        state._gid_dev = g
+    return g
+
+
+def _solution_device(state, u):
+    """(U device (N, ld), nrhs, single) from a host vector/batch or a device solve output."""
+    torch = _torch()
+    if torch.is_tensor(u):
+        U = u if u.dim() == 2 else u[:, None]
+        if U.device.type != "cuda":
+            U = U.to(state.device)
+        return U.contiguous().to(torch.float64), U.shape[1], u.dim() == 1
+    a = np.asarray(u, dtype=float)
+    single = a.ndim == 1
+    a = a[:, None] if single else a
+    if a.shape[0] != state.layout.N:
+        raise ValueError(f"solution must have {state.layout.N} rows")
+    return torch.from_numpy(np.ascontiguousarray(a)).to(state.device), a.shape[1], single
+
+
+def _leaf_fields_dev(state, U, nrhs, leaves):
+    torch = _torch()
+    lib = _native.load()
+    tb = _PostTables.get(state.layout, state.geometry, state.device)
+    p = state.geometry.p
+    lv = torch.from_numpy(np.ascontiguousarray(leaves, dtype=np.int32)).to(state.device)
+    W = torch.empty((len(leaves), p * p, nrhs), dtype=torch.float64, device=state.device)
+    _native.check(lib.hps_leaf_fields(len(leaves), p, _native.ptr(U), U.shape[1], nrhs, _native.ptr(lv),
+                                      _native.ptr(tb.leaf_Ie), _native.ptr(_gid_dev(state)), _native.ptr(tb.L1),
+                                      _native.ptr(state.psi_groups), _native.ptr(tb.J_i), _native.ptr(tb.J_e),
+                                      _native.ptr(W), _native.stream_ptr()), "hps_leaf_fields")
+    return W
+
+
+def leaf_fields(state, u, leaves=None):
+    """p x p Chebyshev field of every (or every listed) leaf, x1-major (solver.py:349-356), on the
+    device: (n, p, p) for a vector u, (n, p, p, b) for a batch. Invariant under the interface null
+    modes, so it is the gauge-free output of a solve."""
+    U, nrhs, single = _solution_device(state, u)
+    n_leaf = 1 << (2 * state.layout.L)
+    leaves = np.arange(n_leaf) if leaves is None else np.asarray(leaves)
+    p = state.geometry.p
+    W = _leaf_fields_dev(state, U, nrhs, leaves).view(len(leaves), p, p, nrhs)
+    return W[..., 0] if single else W
+
+
+def _owning_leaves(state, pts):
+    """Vectorised _owning_leaf (solver.py:330-346): leaf slot and leaf lower corner per point."""
+    tree, lay = state.tree, state.layout
     dom = tree.domain
-    if not dom.contains(x, y):
-        raise ValueError(f"target ({x}, {y}) lies outside the domain")
+    x, y = pts[:, 0], pts[:, 1]
+    inside = (x >= dom.x_lo) & (x <= dom.x_hi) & (y >= dom.y_lo) & (y <= dom.y_hi)
+    if not np.all(inside):
+        k = int(np.flatnonzero(~inside)[0])
+        raise ValueError(f"target ({x[k]}, {y[k]}) lies outside the domain")
     n = 1 << tree.levels
 
     def cell(t, extent):
-        s = (t / extent) * n
-        i = int(np.floor(s))
-        if i == s and i > 0:
-            i -= 1
-        return min(max(i, 0), n - 1)
+        s_ = (t / extent) * n
+        i = np.floor(s_).astype(np.int64)
+        i = np.where((i == s_) & (i > 0), i - 1, i)
+        return np.clip(i, 0, n - 1)
 
-    return tree.leaf_at(cell(x - dom.x_lo, dom.width), cell(y - dom.y_lo, dom.height))
+    ix, iy = cell(x - dom.x_lo, dom.width), cell(y - dom.y_lo, dom.height)
+    tb = _PostTables.get(lay, state.geometry, state.device)
+    return tb.cell_leaf[ix, iy], lay.xline[ix], lay.yline[iy]
 
 
-def _leaf_field(state, u, leaf):
-    geom = state.geometry
-    w_e = geom.L1 @ u[leaf.I_e]
-    w_i = state.psi[leaf.index] @ w_e
-    w = np.zeros(geom.p ** 2)
-    w[geom.J_e] = w_e
-    w[geom.J_i] = w_i
-    return w.reshape(geom.p, geom.p)
+def _eval(state, u, pts, rx, ry, leaf):
+    torch = _torch()
+    lib = _native.load()
+    U, nrhs, single = _solution_device(state, u)
+    uniq, slot = np.unique(leaf, return_inverse=True)
+    W = _leaf_fields_dev(state, U, nrhs, uniq)
+    dev = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(state.device)
+    # the argument tensors must stay referenced until the launch: a temporary freed inside the call
+    # expression goes back to the caching allocator and the next one may reuse its block
+    slot_d, rx_d, ry_d = dev(slot, np.int32), dev(rx, np.float64), dev(ry, np.float64)
+    out = torch.empty((len(pts), nrhs), dtype=torch.float64, device=state.device)
+    _native.check(lib.hps_eval_points(len(pts), state.geometry.p, _native.ptr(W), nrhs, _native.ptr(slot_d),
+                                      _native.ptr(rx_d), _native.ptr(ry_d), _native.ptr(out), _native.stream_ptr()),
+                  "hps_eval_points")
+    r = out.cpu().numpy()
+    return r[:, 0].copy() if single else r
 
 
 def post_process(state, u, targets):
-    """Solution at arbitrary points via leaf spectral interpolation (solver.py:359-377)."""
+    """Solution at arbitrary points via leaf spectral interpolation (solver.py:359-377), on the
+    device. u: the solve output (vector, (N, b) batch, or the device tensor of solve_device)."""
     geom = state.geometry
-    out = np.empty(len(targets))
-    cache = {}
-    for t, (x, y) in enumerate(targets):
-        leaf = _owning_leaf(state, x, y)
-        W = cache.get(leaf.index)
-        if W is None:
-            W = cache[leaf.index] = _leaf_field(state, u, leaf)
-        rx = interp_matrix(geom.cheb_x, [x - leaf.rect.x_lo])
-        ry = interp_matrix(geom.cheb_y, [y - leaf.rect.y_lo])
-        out[t] = float((rx @ W @ ry.T)[0, 0])
-    return out
+    pts = np.asarray(targets, dtype=float).reshape(-1, 2)
+    if pts.shape[0] == 0:
+        return np.empty(0)
+    leaf, xlo, ylo = _owning_leaves(state, pts)
+    rx = interp_matrix(geom.cheb_x, pts[:, 0] - xlo)
+    ry = interp_matrix(geom.cheb_y, pts[:, 1] - ylo)
+    return _eval(state, u, pts, rx, ry, leaf)
 
 
 def boundary_flux_at(state, u, targets):
-    """Coordinate-derivative flux at outer-boundary points (solver.py:380-400)."""
+    """Coordinate-derivative flux at outer-boundary points (solver.py:380-400), on the device:
+    d/dx1 on the vertical sides, d/dx2 on the horizontal ones (rx Dx W ry^T, rx W (ry Dy)^T)."""
     geom = state.geometry
     dom = state.tree.domain
-    out = np.empty(len(targets))
-    for t, (x, y) in enumerate(targets):
-        on_v = x in (dom.x_lo, dom.x_hi)
-        on_h = y in (dom.y_lo, dom.y_hi)
-        if not (on_v or on_h):
-            raise ValueError(f"target ({x}, {y}) is not on the outer boundary")
-        leaf = _owning_leaf(state, x, y)
-        W = _leaf_field(state, u, leaf)
-        dW = geom.Dx @ W if (on_v and not on_h) else W @ geom.Dy.T
-        rx = interp_matrix(geom.cheb_x, [x - leaf.rect.x_lo])
-        ry = interp_matrix(geom.cheb_y, [y - leaf.rect.y_lo])
-        out[t] = float((rx @ dW @ ry.T)[0, 0])
-    return out
+    pts = np.asarray(targets, dtype=float).reshape(-1, 2)
+    if pts.shape[0] == 0:
+        return np.empty(0)
+    x, y = pts[:, 0], pts[:, 1]
+    on_v = (x == dom.x_lo) | (x == dom.x_hi)
+    on_h = (y == dom.y_lo) | (y == dom.y_hi)
+    if not np.all(on_v | on_h):
+        k = int(np.flatnonzero(~(on_v | on_h))[0])
+        raise ValueError(f"target ({x[k]}, {y[k]}) is not on the outer boundary")
+    leaf, xlo, ylo = _owning_leaves(state, pts)
+    rx = interp_matrix(geom.cheb_x, x - xlo)
+    ry = interp_matrix(geom.cheb_y, y - ylo)
+    dx = on_v & ~on_h
+    rx[dx] = rx[dx] @ geom.Dx
+    ry[~dx] = ry[~dx] @ geom.Dy
+    return _eval(state, u, pts, rx, ry, leaf)
+
+
+def gauge_fixed_solution(state, u):
+    """Gauss-node solution re-tabulated from the leaf Chebyshev fields.
+
+    Every node on a leaf edge takes the mean of its two leaves' side interpolants (the L4 blocks,
+    Qx W[:,0], Qy W[p-1,:], Qx W[:,p-1], Qy W[0,:]); outer-boundary nodes keep the Dirichlet data.
+    Unlike the raw solve output, whose interface values carry the null-mode gauge,
+    this u is a function of the null-mode-invariant fields only. Returns a device tensor (N, b)."""
+    torch = _torch()
+    lib = _native.load()
+    U, nrhs, single = _solution_device(state, u)
+    lay, geom = state.layout, state.geometry
+    tb = _PostTables.get(lay, geom, state.device)
+    n_leaf = 1 << (2 * lay.L)
+    W = _leaf_fields_dev(state, U, nrhs, np.arange(n_leaf))
+    side = torch.empty((n_leaf, 4 * geom.p, nrhs), dtype=torch.float64, device=state.device)
+    _native.check(lib.hps_gauge_sides(n_leaf, geom.p, _native.ptr(W), nrhs, _native.ptr(tb.Qx), _native.ptr(tb.Qy),
+                                      _native.ptr(side), _native.stream_ptr()), "hps_gauge_sides")
+    out = torch.empty((lay.N, nrhs), dtype=torch.float64, device=state.device)
+    _native.check(lib.hps_gauge_gather(lay.N, nrhs, _native.ptr(side), _native.ptr(tb.src), _native.ptr(U), U.shape[1],
+                                       _native.ptr(out), nrhs, _native.stream_ptr()), "hps_gauge_gather")
+    return out[:, 0] if single else out
 
 
 def memory_report(state):

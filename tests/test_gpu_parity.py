@@ -177,6 +177,40 @@ def test_counters_and_stage_separation():
         solver.solve(st, np.zeros(5))
 
 
+def _owner(tree, x, y):
+    # the reference's owning-leaf rule (solver.py:330-346), restated for the tests
+    n, dom = 1 << tree.levels, tree.domain
+
+    def cell(t, extent):
+        s = (t / extent) * n
+        i = int(np.floor(s))
+        if i == s and i > 0:
+            i -= 1
+        return min(max(i, 0), n - 1)
+
+    return tree.leaf_at(cell(x - dom.x_lo, dom.width), cell(y - dom.y_lo, dom.height))
+
+
+def _oracle_point_values(tree, st, W, pts, deriv=False):
+    # rx W ry^T (or the boundary-flux derivative) from oracle leaf fields W (n_leaf, p*p[, b])
+    dom, g = tree.domain, st.geometry
+    out = []
+    for (x, y) in pts:
+        leaf = _owner(tree, x, y)
+        Wk = W[leaf.index - (4 ** tree.levels - 1)]
+        Wk = Wk.reshape((16, 16) + Wk.shape[1:])
+        rx = P.grid.interp_matrix(g.cheb_x, [x - leaf.rect.x_lo])[0]
+        ry = P.grid.interp_matrix(g.cheb_y, [y - leaf.rect.y_lo])[0]
+        if deriv:
+            on_v, on_h = x in (dom.x_lo, dom.x_hi), y in (dom.y_lo, dom.y_hi)
+            if on_v and not on_h:
+                rx = rx @ g.Dx
+            else:
+                ry = ry @ g.Dy
+        out.append(np.einsum("i,ij...,j->...", rx, Wk, ry))
+    return np.array(out)
+
+
 def test_state_api_against_oracle():
     cfg, L = 2, 2
     tree, nodes, st = gpu_build(cfg, L)
@@ -191,7 +225,7 @@ def test_state_api_against_oracle():
     W = O.leaf_cheb_field(ost, uo)
     ref = []
     for (x, y) in pts:
-        leaf = tree.boxes[solver._owning_leaf(st, x, y).index]
+        leaf = _owner(tree, x, y)
         k = leaf.index - (4 ** L - 1)
         Wk = W[k].reshape(16, 16)
         rx = P.grid.interp_matrix(st.geometry.cheb_x, [x - leaf.rect.x_lo])
@@ -283,3 +317,61 @@ def test_pipeline_matches_sequential_build_and_solve():
         st = solver.build(tree, nodes, co)
         assert ng == st.n_leaf_groups
         assert np.array_equal(u, solver.solve(st, F))
+
+
+@pytest.mark.parametrize("cfg,L", [(2, 2), (4, 3)])
+def test_device_post_processing_against_oracle_fields(cfg, L):
+    # hps_leaf_fields / hps_eval_points vs the oracle's null-mode-invariant leaf fields
+    tree, nodes, st = gpu_build(cfg, L)
+    ot = O.build_tree((0, 1, 0, 1), L, 16)
+    ost = O.build(ot, coeff_dict(problems.coefficients(cfg)))
+    F = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=5, batch=3)
+    U = solver.solve(st, F)
+    Wo = O.leaf_cheb_field(ost, O.solve(ost, F))          # (n_leaf, p*p, 3)
+    tol = 1e-10 if cfg in (1, 2, 5) else 1e-8
+    Wd = solver.leaf_fields(st, U).cpu().numpy()          # (n_leaf, p, p, 3)
+    assert rel(Wd.reshape(Wo.shape), Wo) < tol
+    w1 = solver.leaf_fields(st, U[:, 1]).cpu().numpy()    # vector input
+    assert rel(w1.reshape(Wo.shape[:2]), Wo[:, :, 1]) < tol
+    rng = np.random.default_rng(7)
+    pts = np.concatenate([rng.uniform(0, 1, (50, 2)), [[0.5, 0.5], [0.25, 0.75], [0.0, 0.0], [1.0, 1.0], [0.125, 1.0]]])
+    got = solver.post_process(st, U, pts)
+    assert got.shape == (len(pts), 3)
+    assert rel(got, _oracle_point_values(tree, st, Wo, pts)) < tol
+    assert rel(solver.post_process(st, U[:, 0], pts), got[:, 0]) < 1e-14
+    bpts = [(0.0, 0.3), (1.0, 0.6), (0.2, 0.0), (0.7, 1.0), (0.0, 0.0), (1.0, 0.5)]
+    assert rel(solver.boundary_flux_at(st, U, bpts), _oracle_point_values(tree, st, Wo, bpts, deriv=True)) < tol
+    with pytest.raises(ValueError):
+        solver.post_process(st, U, [(1.5, 0.5)])
+    with pytest.raises(ValueError):
+        solver.boundary_flux_at(st, U, [(0.5, 0.5)])
+
+
+def test_gauge_fixed_solution_laplace_exact_and_invariant():
+    # Gauss-node u re-tabulated from the leaf fields: physical (matches the exact solution),
+    # keeps the Dirichlet data on the outer boundary, and equals the oracle re-tabulation
+    cfg, L = 1, 3
+    tree, nodes, st = gpu_build(cfg, L)
+    f = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=0)
+    u = solver.solve(st, f)
+    ug = solver.gauge_fixed_solution(st, u).cpu().numpy()
+    ex = problems.exact_solution(cfg, nodes.points[:, 0], nodes.points[:, 1])
+    assert np.max(np.abs(ug - ex)) < 1e-10
+    root_ie = np.asarray(tree.root.I_e)
+    assert np.array_equal(ug[root_ie], np.asarray(f, dtype=float))
+    # oracle re-tabulation: per leaf sides Qx W[:,0], Qy W[p-1,:], Qx W[:,p-1], Qy W[0,:], averaged
+    ot = O.build_tree((0, 1, 0, 1), L, 16)
+    ost = O.build(ot, coeff_dict(problems.coefficients(cfg)))
+    Wo = O.leaf_cheb_field(ost, O.solve(ost, f)).reshape(-1, 16, 16)
+    g = st.geometry
+    acc, cnt = np.zeros(nodes.N), np.zeros(nodes.N)
+    for k, b in enumerate(ot.leaves):
+        Wk = Wo[k]
+        side = np.concatenate([g.Qx @ Wk[:, 0], g.Qy @ Wk[15, :], g.Qx @ Wk[:, 15], g.Qy @ Wk[0, :]])
+        np.add.at(acc, ot.I_e[b], side)
+        np.add.at(cnt, ot.I_e[b], 1.0)
+    ref = acc / cnt
+    ref[root_ie] = f
+    assert rel(ug, ref) < 1e-12
+    ug2 = solver.gauge_fixed_solution(st, u).cpu().numpy()
+    assert np.array_equal(ug, ug2)
