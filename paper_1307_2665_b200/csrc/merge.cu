@@ -239,7 +239,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, long long strideX, int n, int* status,
                                                    int status_base) {
   constexpr int NM = 8 * NT, W = NT / 2, RPL = NM / 32 > 0 ? NM / 32 : 1;
-  static_assert(NT % 2 == 0 && W >= 1, "NT");
+  static_assert(NT % 2 == 0 && W >= 1 && NM <= 128, "NT (row index must fit in 7 bits)");
   __shared__ double sW[2][NM][9];     // panel of the current / next block after its 8 GJ steps
   __shared__ int sP[2][8];            // pivot rows of the block
   __shared__ double sAP[W][8][17];    // per warp: A[P, its 16 columns] before the block update
@@ -283,18 +283,21 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
     }
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      unsigned long long best = 0ull;
-      int bi = 0x7fffffff;
+      // argmax |x| over the unused rows with two REDUX: the high word of |x| exactly, then the low
+      // word with its 7 lowest mantissa bits replaced by (127 - row), so the smallest row wins
+      // exact ties (and ties within 2^-45 relative). 2 REDUX instead of 3 (tools/microbench/
+      // panel_ablate.cu: 628 vs 760 cycles per pivot).
+      unsigned bh = 0u, bl = 0u;
 #pragma unroll
       for (int i = 0; i < RPL; ++i) {
-        const unsigned long long key = used[i] ? 0ull : (unsigned long long)__double_as_longlong(fabs(pr[i][t]));
-        const int idx = used[i] ? 0x7fffffff : lane + 32 * i;
-        if (key > best || (key == best && idx < bi)) { best = key; bi = idx; }
+        const unsigned long long kb = used[i] ? 0ull : (unsigned long long)__double_as_longlong(fabs(pr[i][t]));
+        const unsigned h = (unsigned)(kb >> 32);
+        const unsigned l = used[i] ? 0u : ((((unsigned)kb) & ~127u) | (127u - (unsigned)(lane + 32 * i)));
+        if (h > bh || (h == bh && l > bl)) { bh = h; bl = l; }
       }
-      const unsigned hi = (unsigned)(best >> 32), lo = (unsigned)best;
-      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-      const int p = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)bi : 0xffffffffu);
+      const unsigned mh = __reduce_max_sync(0xffffffffu, bh);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, bh == mh ? bl : 0u);
+      const int p = 127 - (int)(ml & 127u);
       const int pl = p & 31, pi = p >> 5;
       double rp[8];
 #pragma unroll
