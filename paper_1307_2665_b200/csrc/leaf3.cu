@@ -35,7 +35,7 @@ constexpr int NRHS = LDM - NI;  // 64 (61 used)
 constexpr int THREADS = 256;
 constexpr int NPW = 4;  // panel warps
 constexpr int SA = 20;  // multiplier row stride (== 4 mod 16)
-constexpr int SB = 264; // U12 row stride (== 8 mod 16)
+constexpr int SB = 260; // U12 row stride (== 4 mod 16: the DMMA B-fragment loads are conflict-free)
 constexpr int ST1 = 68;
 constexpr int NPANEL = (NI + 15) / 16;  // 13
 constexpr int OFF_A16 = 0;                         // 2 x MROWS x SA
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
   double* Dy = Dx + 256;
   double* Dxx = Dy + 256;
   double* Dyy = Dxx + 256;
-  int* colmap = sAct;           // node -> M column (256)
+  int* colmap = sAct;           // node (i, j) -> M column, at [i * 17 + j] (272 <= 2 * MROWS)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
@@ -98,11 +98,11 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
       const double* src = a.field[f] ? a.field[f] + (long long)grp * 256 : nullptr;
       for (int i = tid; i < 256; i += THREADS) coef[f * 256 + i] = src ? src[i] : a.scalar[f];
     }
-    for (int i = tid; i < 256; i += THREADS) colmap[i] = -1;
+    for (int i = tid; i < 16 * 17; i += THREADS) colmap[i] = -1;
     if (tid == 0) s_sing = 0;
     __syncthreads();
-    for (int i = tid; i < NI; i += THREADS) colmap[Ji[i]] = i;
-    for (int i = tid; i < NB; i += THREADS) colmap[Je[i]] = NI + i;
+    for (int i = tid; i < NI; i += THREADS) colmap[(Ji[i] >> 4) * 17 + (Ji[i] & 15)] = i;
+    for (int i = tid; i < NB; i += THREADS) colmap[(Je[i] >> 4) * 17 + (Je[i] & 15)] = NI + i;
     // zero-fill M (vectorised), probe column
     for (int e = tid; e < MROWS * LDM / 2; e += THREADS)
       reinterpret_cast<double2*>(M)[e] = make_double2(0.0, 0.0);
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
         const int which = lane >> 4, t = lane & 15;  // lanes 0-15: vary ib; 16-31: vary jb (skip the diagonal)
         const int ib_ = which == 0 ? t : ia, jb_ = which == 0 ? ja : t;
         if (!(which == 1 && t == ja)) {
-          const int col = colmap[ib_ * 16 + jb_];
+          const int col = colmap[ib_ * 17 + jb_];
           const double v = entry(ib_, jb_);
           Mr[col] = v;
           if (col < NI) rs += fabs(v);
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
     // Psi rows out, T1 += L43i[:, blk] (-X_blk) (each warp: 8 rows x 64 columns in registers), then
     // Y[P_j] -= U[P_j, blk] X_blk for all earlier pivot rows (DMMA, 8-row items, parallel loads).
     double* sX = sA16;                 // 16 x 66 : X block (B operand, SB-like padded stride)
-    constexpr int SX = 72;             // == 8 mod 16
+    constexpr int SX = 68;             // == 4 mod 16 (conflict-free B fragments)
     double* Psi = a.Psi + (long long)grp * NI * NB;
     double t1acc[8][2];
 #pragma unroll
