@@ -10,6 +10,7 @@ seg = data[starts[-1]:] if starts else data
 by_kind = collections.defaultdict(float)
 depth = -1
 by_depth = collections.defaultdict(float)
+by_dk = collections.defaultdict(float)
 for name, grid, block, us in seg:
     short = name.split("(")[0].replace("void ", "").replace("hps::", "")
     if "k_gather_xr" in short:
@@ -17,10 +18,12 @@ for name, grid, block, us in seg:
     key = short[:48]
     by_kind[key] += us
     by_depth[depth] += us
+    by_dk[(depth, key[:28])] += us
 tot = sum(by_kind.values())
 print(f"one build: {tot/1e3:.3f} ms serialized over {len(seg)} launches")
 for k, v in sorted(by_kind.items(), key=lambda x: -x[1]):
     print(f"  {v/1e3:8.3f} ms {100*v/tot:5.1f}%  {k}")
 print("by merge step (launch order; -1 = leaf stage):")
 for d, v in sorted(by_depth.items()):
-    print(f"  step {d:3d}: {v/1e3:8.3f} ms")
+    parts = ", ".join(f"{k} {u:.0f}us" for (dd, k), u in sorted(by_dk.items(), key=lambda x: -x[1]) if dd == d)
+    print(f"  step {d:3d}: {v/1e3:8.3f} ms   {parts}")
