@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--levels", type=int, default=None, help="override L (exploration only)")
     ap.add_argument("--batch", type=int, default=None, help="override solve batch b")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="enqueue the build eagerly instead of replaying CUDA graphs")
     ap.add_argument("--force-distributed", action="store_true",
                     help="run the subtree/NCCL path even at world size 1 (plumbing check)")
     return ap.parse_args()
@@ -235,11 +236,20 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
     # ---- device-resident timed steps ----
+    # Default: the build (one CUDA graph per stage) and the solve replayed from solver.BuildGraph,
+    # inputs already in its static buffers; --no-graph: eager enqueue of the same kernels.
+    graph = None if args.no_graph else solver.BuildGraph(inp, nrhs=b)
+    if graph is not None:
+        graph.load(inp, F_dev)
+
     def step(timeline=None):
-        st = solver.build_device(inp, timeline=timeline)
+        if graph is not None:
+            st = graph.replay_build(timeline)
+        else:
+            st = solver.build_device(inp, timeline=timeline)
         e = torch.cuda.Event(enable_timing=True)
         e.record()
-        U = solver.solve_device(st, F_dev)
+        U = graph.replay_solve() if graph is not None else solver.solve_device(st, F_dev)
         return st, U, e
 
     st = U = None
@@ -267,7 +277,8 @@ def main():
         t_solve.append(e1.elapsed_time(e2) / 1e3)
         for name, a, z in tl:
             stages.setdefault(name, []).append(a.elapsed_time(z) / 1e3)
-    launches = lib.hps_launch_count() - launches0
+    # a replay does not pass through the library's host-side launch counter: count the captured ones
+    launches = graph.launches * args.steps if graph is not None else lib.hps_launch_count() - launches0
     torch.cuda.synchronize()
     clk = clocks.stop()
     tb, ts = float(np.mean(t_build)), float(np.mean(t_solve))
@@ -358,6 +369,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload, "unknowns": unknowns, "batch": b, "leaf_groups": inp.ngroups,
                        "l2": "flushed (256 MB write) between timed steps, outside the step events",
+                       "launch": ("CUDA graphs (solver.BuildGraph: one per build stage + one for the solve)"
+                                  if graph is not None else "eager"),
                        "build_ms": tb * 1e3, "solve_ms": ts * 1e3,
                        "build_unknowns_per_s": unknowns / tb, "solve_unknowns_per_s": unknowns * b / ts},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

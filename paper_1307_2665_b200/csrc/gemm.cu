@@ -25,20 +25,22 @@ __global__ void k_splitk_reduce(GemmParams p) {
 }
 
 // Split-K scratch: one growing device buffer (builds repeat the same shapes, so it settles after
-// the first build). The library enqueues on one stream at a time.
+// the first build). The library enqueues on one stream at a time. A buffer it outgrows is never
+// freed: a captured CUDA graph (solver.BuildGraph) may still reference it.
 static double* g_splitk = nullptr;
 static size_t g_splitk_n = 0;
-static double* splitk_scratch(size_t n) {
+static double* splitk_scratch(size_t n, cudaStream_t st) {
   if (n > g_splitk_n) {
-    if (g_splitk) {
-      cudaDeviceSynchronize();
-      cudaFree(g_splitk);
-    }
-    if (cudaMalloc(&g_splitk, n * sizeof(double)) != cudaSuccess) {
-      g_splitk = nullptr;
-      g_splitk_n = 0;
+    // no allocation inside a stream capture (it would invalidate the capture): the caller then
+    // runs without split-K. BuildGraph warms up first, so captures normally find it allocated.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    double* fresh = nullptr;
+    if (cudaMalloc(&fresh, n * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
       return nullptr;
     }
+    g_splitk = fresh;
     g_splitk_n = n;
   }
   return g_splitk;
@@ -65,7 +67,7 @@ static int launch_cfg(const GemmParams& p, cudaStream_t stream) {
   GemmParams q = p;
   if (split > 1) {
     q.split = split;
-    q.partial = splitk_scratch((size_t)split * p.batch * (size_t)p.M * p.N);
+    q.partial = splitk_scratch((size_t)split * p.batch * (size_t)p.M * p.N, stream);
     if (!q.partial) q.split = 1;
   }
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.batch * q.split);
@@ -108,7 +110,7 @@ static int launch_cfg64(const GemmParams& p, cudaStream_t stream) {
   GemmParams q = p;
   if (split > 1) {
     q.split = split;
-    q.partial = splitk_scratch((size_t)split * p.batch * (size_t)p.M * p.N);
+    q.partial = splitk_scratch((size_t)split * p.batch * (size_t)p.M * p.N, stream);
     if (!q.partial) q.split = 1;
   }
   dim3 grid((p.N + 63) / 64, (p.M + 63) / 64, p.batch * q.split);

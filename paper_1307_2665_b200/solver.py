@@ -45,6 +45,7 @@ __all__ = [
     "leaf_fields",
     "gauge_fixed_solution",
     "Pipeline",
+    "BuildGraph",
     "memory_report",
 ]
 
@@ -450,8 +451,12 @@ def prepare(tree, nodeset, coeffs, *, device=None, pinned=False):
 
 
 def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_threshold=math.inf,
-                 hbs_leaf_size=64):
-    """Enqueue the leaf stage and every merge level on the current stream (no host sync)."""
+                 hbs_leaf_size=64, stage_begin=None):
+    """Enqueue the leaf stage and every merge level on the current stream (no host sync).
+    `stage_begin(name)`, if given, is called before each stage ("leaf", "merge_d<d>"): BuildGraph
+    uses it to capture one CUDA graph per stage."""
+    if stage_begin is not None:
+        stage_begin("leaf")
     torch = _torch()
     lib = _native.load()
     lay, geom, dl, device = inp.layout, inp.geom, inp.dev_layout, inp.device
@@ -489,6 +494,8 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
     level_T = [None] * (2 * L) if keep_level_T else None
     child_T, child_stride, child_idx = Tleaf, ng * ng, inp.gid_dev
     for d in range(2 * L - 1, -1, -1):
+        if stage_begin is not None:
+            stage_begin(f"merge_d{d}")
         dlay = lay.depths[d]
         nbatch, n3, ne, m = dlay.n_boxes, dlay.n3, dlay.ne, dlay.m
         S = torch.empty((nbatch, n3, ne), dtype=torch.float64, device=device)
@@ -725,6 +732,117 @@ class Pipeline:
 
     def close(self):
         self._host.shutdown(wait=True)
+
+
+class BuildGraph:
+    """One build (and optionally one batched solve) captured into CUDA graphs and replayed.
+
+    For loops that rebuild the same discretisation with new coefficient samples (time stepping,
+    parameter sweeps, benchmarks): the ~290 kernel launches of a build become one graph launch per
+    stage (the leaf stage and each merge depth) plus one for the solve. That removes the launch
+    gaps, which dominate the small, latency-bound top merges, and keeps per-stage event timing
+    possible between the replays.
+
+    `BuildGraph(inp, nrhs)` captures for inputs shaped like `inp` (same tree, same number of leaf
+    groups, same non-constant coefficient fields and constant values). `run(inp, F)` copies the
+    new inputs into the graphs' static buffers, replays, and returns (state, U): both live in
+    the graphs' memory pool and are overwritten by the next run. `check_build(state)` works as
+    usual. Replays enqueue on the current stream. `launches` is the number of library kernel
+    launches one build + solve replay performs."""
+
+    def __init__(self, inp, nrhs=0):
+        torch = _torch()
+        lib = _native.load()
+        self.torch = torch
+        self.layout, self.ngroups, self.scalars = inp.layout, inp.ngroups, tuple(inp.scalars)
+        self._present = tuple(t is not None for t in inp.fields_dev)
+        fields = [None if t is None else t.clone() for t in inp.fields_dev]
+        self._inp = BuildInputs(inp.tree, inp.nodeset, inp.coeffs, inp.layout, inp.geom, inp.dev_layout,
+                                inp.reps, inp.gid, inp.gid_dev.clone(), fields, tuple(inp.scalars), inp.device)
+        self.nrhs = int(nrhs)
+        self._F = (torch.zeros((len(inp.layout.root_I_e), self.nrhs), dtype=torch.float64, device=inp.device)
+                   if self.nrhs else None)
+        side = torch.cuda.Stream(inp.device)
+        side.wait_stream(torch.cuda.current_stream())
+        pool = torch.cuda.graph_pool_handle()
+        self.stages = []
+        n0 = lib.hps_launch_count()
+        with torch.cuda.stream(side):
+            st = build_device(self._inp)  # warm-up: lazy attributes and scratch sizes outside the capture
+            if self.nrhs:
+                solve_device(st, self._F)
+            del st
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()  # the warm-up state's memory (L=9: ~50 GB) back before the capture
+            n0 = lib.hps_launch_count()
+
+            def begin(name):
+                if self.stages:
+                    self.stages[-1][1].capture_end()
+                g = torch.cuda.CUDAGraph()
+                g.capture_begin(pool=pool)
+                self.stages.append((name, g))
+
+            self.state = build_device(self._inp, stage_begin=begin)
+            self.stages[-1][1].capture_end()
+            self.solve_graph, self.U = None, None
+            if self.nrhs:
+                self.solve_graph = torch.cuda.CUDAGraph()
+                self.solve_graph.capture_begin(pool=pool)
+                self.U = solve_device(self.state, self._F)
+                self.solve_graph.capture_end()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.launches = int(lib.hps_launch_count() - n0)
+
+    def matches(self, inp):
+        return (inp.layout is self.layout and inp.ngroups == self.ngroups and tuple(inp.scalars) == self.scalars
+                and tuple(t is not None for t in inp.fields_dev) == self._present)
+
+    def load(self, inp=None, F=None):
+        """Copy new inputs (and boundary data) into the static buffers (stream-ordered)."""
+        if inp is not None:
+            if not self.matches(inp):
+                raise ValueError("BuildGraph: inputs differ in layout, group count or coefficient structure")
+            for dst, src in zip(self._inp.fields_dev, inp.fields_dev):
+                if dst is not None:
+                    dst.copy_(src, non_blocking=True)
+            self._inp.gid_dev.copy_(inp.gid_dev, non_blocking=True)
+            st = self.state
+            st._reps, st.leaf_group, st.coeffs = inp.reps, inp.gid, inp.coeffs
+            st.psi = _LazyPsi(st.psi_groups, inp.gid, (1 << (2 * self.layout.L)) - 1)
+            st._gid_dev = None
+        if F is not None:
+            if not self.nrhs:
+                raise ValueError("BuildGraph: captured without a solve (nrhs=0)")
+            Ft = F if self.torch.is_tensor(F) else self.torch.from_numpy(np.ascontiguousarray(F, dtype=np.float64))
+            self._F.copy_(Ft.reshape(self._F.shape), non_blocking=True)
+
+    def replay_build(self, timeline=None):
+        """Replay the build stages; with `timeline` (a list), append (name, start, end) events."""
+        for name, g in self.stages:
+            if timeline is None:
+                g.replay()
+            else:
+                e0 = self.torch.cuda.Event(enable_timing=True)
+                e1 = self.torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                timeline.append((name, e0, e1))
+        return self.state
+
+    def replay_solve(self):
+        if self.solve_graph is None:
+            raise ValueError("BuildGraph: captured without a solve (nrhs=0)")
+        self.solve_graph.replay()
+        return self.U
+
+    def run(self, inp=None, F=None):
+        self.load(inp, F)
+        self.replay_build()
+        U = self.replay_solve() if self.solve_graph is not None else None
+        return self.state, U
 
 
 def apply_global_dtn(state, f):

@@ -375,3 +375,27 @@ def test_gauge_fixed_solution_laplace_exact_and_invariant():
     assert rel(ug, ref) < 1e-12
     ug2 = solver.gauge_fixed_solution(st, u).cpu().numpy()
     assert np.array_equal(ug, ug2)
+
+
+def test_build_graph_replays_equal_eager_builds():
+    # solver.BuildGraph: a captured build + batched solve replayed with new inputs must give the
+    # same bits as an eager build and solve of those inputs
+    from paper_1307_2665_b200.leafops import CoefficientField
+    tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), 4, 16)
+    pts = nodes.points[tree.root.I_e]
+    co = [CoefficientField(c11=lambda x, y, a=a: 1.0 + a * np.sin(3 * x) * np.cos(2 * y), c22=lambda x, y: 1.0 + 0.3 * x * y)
+          for a in (0.1, 0.4, 0.25)]
+    F = [problems.boundary_data(2, pts, seed=s, batch=5) for s in range(3)]
+    inps = [solver.prepare(tree, nodes, c) for c in co]
+    g = solver.BuildGraph(inps[0], nrhs=5)
+    assert g.launches > 0
+    for inp, Fk, c in zip(inps, F, co):
+        st, U = g.run(inp, Fk)
+        solver.check_build(st)
+        got_T = st.root_T.device_tensor.clone()
+        got_U = U[:, :5].clone()
+        ref = solver.build_device(inp)
+        Uref = solver.solve_device(ref, torch.from_numpy(np.ascontiguousarray(Fk)).cuda())
+        assert torch.equal(got_T, ref.root_T.device_tensor)
+        assert torch.equal(got_U, Uref[:, :5])
+        assert rel(solver.post_process(st, U[:, :5], [(0.3, 0.6)]), solver.post_process(ref, Uref[:, :5], [(0.3, 0.6)])) == 0
