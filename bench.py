@@ -325,7 +325,7 @@ def main():
     # upload, the build, the H2D of the boundary data, the batched solve and the D2H of u. The
     # pipeline overlaps the host work of step i+1 with the device work of step i.
     pin_F = torch.from_numpy(np.ascontiguousarray(F_host)).pin_memory()
-    pipe = solver.Pipeline(tree, nodes, device=dev)
+    pipe = solver.Pipeline(tree, nodes, device=dev, reuse_graphs=not args.no_graph)
     st = U = None
     n_e2e = max(10, args.steps)  # a stream of problems: pipeline fill and drain are inside the total
     for U, st in pipe.run([(co, pin_F)] * n_e2e):
@@ -353,7 +353,8 @@ def main():
            "latency_s": float(min(lat)),
            "includes": "per step: coefficient sampling on the host, H2D of the samples (pinned), leaf grouping "
                        "on the device, build, status check, H2D of the boundary data, batched solve, D2H of u "
-                       "(N x ldu); solver.Pipeline overlaps step i+1's host work with step i's device work; "
+                       "(N x ldu); solver.Pipeline overlaps step i+1's host work with step i's device work "
+                       "(and replays build + solve from two alternating CUDA-graph captures); "
                        "latency_s = one problem alone"}
 
     cpu = None

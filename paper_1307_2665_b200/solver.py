@@ -653,10 +653,16 @@ class Pipeline:
     root.I_e order, and yields (U, state) per job in order: U is a pinned host tensor (N, ldu) whose
     columns [:b] are the solutions, state the SolverState (valid until the caller drops it)."""
 
-    def __init__(self, tree, nodeset, *, device=None, overlap_results=True):
+    def __init__(self, tree, nodeset, *, device=None, overlap_results=True, reuse_graphs=False):
         torch = _torch()
         _native.require_device()
         self.overlap_results = overlap_results
+        # reuse_graphs: build + solve replayed from two alternating BuildGraph captures (keyed by the
+        # group count, coefficient structure and batch width; other jobs run eagerly). A yielded
+        # state then lives in graph memory and is valid until the next item is requested.
+        self.reuse_graphs = reuse_graphs
+        self._graphs = [{}, {}]
+        self._jobs = 0
         self.tree, self.nodeset = tree, nodeset
         self.device = torch.device(device if device is not None else "cuda")
         self._upload = torch.cuda.Stream(self.device)
@@ -689,13 +695,20 @@ class Pipeline:
                     self._main.wait_event(ready)
                     for t in inp.device_tensors():
                         t.record_stream(self._main)
-                    st = build_device(inp)
                     Fh = F if torch.is_tensor(F) else torch.from_numpy(np.ascontiguousarray(np.asarray(F, dtype=float)))
                     if Fh.dim() == 1:
                         Fh = Fh[:, None]
                     if not Fh.is_pinned():
                         Fh = Fh.pin_memory()
-                    U = solve_device(st, Fh.to(self.device, non_blocking=True))
+                    Fd = Fh.to(self.device, non_blocking=True)
+                    g = self._graph_for(inp, Fd.shape[1]) if self.reuse_graphs else None
+                    if g is not None:
+                        g.load(inp, Fd)
+                        st = g.replay_build()
+                        U = g.replay_solve()
+                    else:
+                        st = build_device(inp)
+                        U = solve_device(st, Fd)
                     solved = torch.cuda.Event()
                     solved.record(self._main)
                 # results and status words come back on their own stream, so the next job's build
@@ -721,6 +734,17 @@ class Pipeline:
             job = nxt
         if pending is not None:
             yield self._finish(*pending)
+
+    def _graph_for(self, inp, nrhs):
+        slot = self._graphs[self._jobs & 1]
+        self._jobs += 1
+        key = (inp.ngroups, tuple(t is not None for t in inp.fields_dev), tuple(inp.scalars), int(nrhs))
+        g = slot.get(key)
+        if g is None:
+            if len(slot) >= 4:  # bound the captured memory
+                slot.clear()
+            g = slot[key] = BuildGraph(inp, nrhs=nrhs)
+        return g
 
     @staticmethod
     def _finish(st, outs, done):

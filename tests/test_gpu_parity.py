@@ -309,14 +309,15 @@ def test_pipeline_matches_sequential_build_and_solve():
     tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), 4, 16)
     pts = nodes.points[tree.root.I_e]
     jobs = [(problems.coefficients(cfg), problems.boundary_data(2, pts, seed=cfg, batch=3)) for cfg in (2, 4, 3, 2)]
-    pipe = solver.Pipeline(tree, nodes)
-    got = [(U[:, :3].numpy().copy(), st.n_leaf_groups) for U, st in pipe.run(jobs)]
-    pipe.close()
-    assert len(got) == len(jobs)
-    for (co, F), (u, ng) in zip(jobs, got):
-        st = solver.build(tree, nodes, co)
-        assert ng == st.n_leaf_groups
-        assert np.array_equal(u, solver.solve(st, F))
+    for graphs in (False, True):
+        pipe = solver.Pipeline(tree, nodes, reuse_graphs=graphs)
+        got = [(U[:, :3].numpy().copy(), st.n_leaf_groups) for U, st in pipe.run(jobs + jobs)]
+        pipe.close()
+        assert len(got) == 2 * len(jobs)
+        for (co, F), (u, ng) in zip(jobs + jobs, got):
+            st = solver.build(tree, nodes, co)
+            assert ng == st.n_leaf_groups
+            assert np.array_equal(u, solver.solve(st, F))
 
 
 @pytest.mark.parametrize("cfg,L", [(2, 2), (4, 3)])
