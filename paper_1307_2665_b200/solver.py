@@ -800,11 +800,13 @@ class BuildGraph:
             torch.cuda.empty_cache()  # the warm-up state's memory (L=9: ~50 GB) back before the capture
             n0 = lib.hps_launch_count()
 
+            # thread_local: other host threads (the Pipeline's preparation thread) may sync or
+            # allocate pinned memory meanwhile without invalidating this capture
             def begin(name):
                 if self.stages:
                     self.stages[-1][1].capture_end()
                 g = torch.cuda.CUDAGraph()
-                g.capture_begin(pool=pool)
+                g.capture_begin(pool=pool, capture_error_mode="thread_local")
                 self.stages.append((name, g))
 
             self.state = build_device(self._inp, stage_begin=begin)
@@ -812,7 +814,7 @@ class BuildGraph:
             self.solve_graph, self.U = None, None
             if self.nrhs:
                 self.solve_graph = torch.cuda.CUDAGraph()
-                self.solve_graph.capture_begin(pool=pool)
+                self.solve_graph.capture_begin(pool=pool, capture_error_mode="thread_local")
                 self.U = solve_device(self.state, self._F)
                 self.solve_graph.capture_end()
         torch.cuda.current_stream().wait_stream(side)

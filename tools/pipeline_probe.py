@@ -11,7 +11,7 @@ tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), c.L, 16)
 co = c.coefficients()
 F = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=0, batch=c.batch)
 F = torch.from_numpy(np.ascontiguousarray(F if F.ndim == 2 else F[:, None])).pin_memory()
-pipe = solver.Pipeline(tree, nodes)
+pipe = solver.Pipeline(tree, nodes, reuse_graphs=len(sys.argv) > 3)
 T0 = [0.0]
 log = []
 orig = pipe._prepare
