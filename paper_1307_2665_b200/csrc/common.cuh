@@ -61,6 +61,10 @@ __device__ __forceinline__ void sts64(double* p, double v) {
 
 // Reciprocal for pivots: MUFU approximation + 2 Newton steps (error ~1 ulp). About 60 cycles,
 // against ~230 for the IEEE division sequence, which sits on every pivot step's critical path.
+// Named barriers (ids 1..15; 0 is __syncthreads): sync waits, arrive only signals.
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 __device__ __forceinline__ double fast_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));

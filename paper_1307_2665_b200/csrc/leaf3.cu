@@ -48,8 +48,6 @@ constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4 + 64;
 constexpr int BAR_PANEL = 1;      // panel warps only (128 threads)
 }  // namespace l3
 
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
   using namespace l3;

@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
   __shared__ int sP[2][8];            // pivot rows of the block
   __shared__ double sAP[W][8][17];    // per warp: A[P, its 16 columns] before the block update
   __shared__ double sDum[10];         // store sink for lanes that do not hold a staged row (never read)
+  __shared__ unsigned sCand[2][2];    // 2-warp panel: each warp's (hi, lo) argmax candidate
+  __shared__ __align__(16) double sRowP[2][8];  // 2-warp panel: the pivot row (by pivot parity)
   __shared__ unsigned char usedrow[NM];
   __shared__ int pivrow[NM], rowstep[NM];
   __shared__ int s_sing;
@@ -345,6 +347,107 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
 #pragma unroll
       for (int h = 0; h < 2; ++h) a[r][C][h] = Pb[8 * r + g][2 * tq + h];
   };
+  // Two-warp panel (n > 32): the tile's owner (role 0, rows 0..NM/2) and a helper warp (role 1, rows
+  // NM/2..NM) factor the 8 columns together, 2 rows per lane. Per pivot: a 2-REDUX argmax in each
+  // warp, the two candidates exchanged through shared memory (64-thread named barrier), the pivot
+  // row published by its lane (second barrier). Half the per-lane rows of the single-warp panel.
+  constexpr int BAR_PANEL2 = 1, HALF = NM / 2, RPL2 = NM >= 64 ? NM / 64 : 1;
+  auto panel2 = [&](auto cc, int kb, int role) {
+    constexpr int C = decltype(cc)::value;
+    double(*Pb)[9] = sW[kb & 1];
+    if (role == 0) {
+#pragma unroll
+      for (int r = 0; r < NT; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) Pb[8 * r + g][2 * tq + h] = a[r][C][h];
+    }
+    bar_sync(BAR_PANEL2, 64);
+    double pr[RPL2][8];
+    bool used[RPL2];
+#pragma unroll
+    for (int i = 0; i < RPL2; ++i) {
+      const int R = role * HALF + lane + 32 * i;
+      used[i] = usedrow[R];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pr[i][j] = Pb[R][j];
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      unsigned bh = 0u, bl = 0u;
+#pragma unroll
+      for (int i = 0; i < RPL2; ++i) {
+        const int R = role * HALF + lane + 32 * i;
+        const unsigned long long kb2 = used[i] ? 0ull : (unsigned long long)__double_as_longlong(fabs(pr[i][t]));
+        const unsigned h = (unsigned)(kb2 >> 32);
+        const unsigned l = used[i] ? 0u : ((((unsigned)kb2) & ~127u) | (127u - (unsigned)R));
+        if (h > bh || (h == bh && l > bl)) { bh = h; bl = l; }
+      }
+      const unsigned mh = __reduce_max_sync(0xffffffffu, bh);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, bh == mh ? bl : 0u);
+      if (lane == 0) { sCand[role][0] = mh; sCand[role][1] = ml; }
+      bar_sync(BAR_PANEL2, 64);
+      const unsigned h0 = sCand[0][0], l0 = sCand[0][1], h1 = sCand[1][0], l1 = sCand[1][1];
+      const unsigned wl = (h1 > h0 || (h1 == h0 && l1 > l0)) ? l1 : l0;
+      const int p = 127 - (int)(wl & 127u);
+      const int prole = p >= HALF, pq = p - prole * HALF, pl = pq & 31, pi = pq >> 5;
+      if (role == prole && lane == pl) {
+#pragma unroll
+        for (int i = 0; i < RPL2; ++i)
+          if (pi == i) {
+            used[i] = true;
+#pragma unroll
+            for (int j = 0; j < 8; j += 2)
+              *reinterpret_cast<double2*>(&sRowP[t & 1][j]) = make_double2(pr[i][j], pr[i][j + 1]);
+          }
+      }
+      bar_sync(BAR_PANEL2, 64);
+      double rp[8];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(&sRowP[t & 1][j]);
+        rp[j] = v.x;
+        rp[j + 1] = v.y;
+      }
+      const double piv = rp[t];
+      const double inv = fast_rcp(piv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) rp[j] = j == t ? inv : rp[j] * inv;
+#pragma unroll
+      for (int i = 0; i < RPL2; ++i) {
+        const double f = pr[i][t];
+        pr[i][t] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pr[i][j] = fma(-f, rp[j], pr[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < RPL2; ++i) {
+        const bool mine = role == prole && pi == i && lane == pl;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pr[i][j] = mine ? rp[j] : pr[i][j];
+      }
+      if (role == 0 && lane == 0) {
+        sP[kb & 1][t] = p;
+        usedrow[p] = 1;
+        pivrow[8 * kb + t] = p;
+        rowstep[p] = 8 * kb + t;
+        if (piv == 0.0) s_sing = 1;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RPL2; ++i) {
+      const int R = role * HALF + lane + 32 * i;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) Pb[R][j] = pr[i][j];
+    }
+    bar_sync(BAR_PANEL2, 64);
+    if (role == 0) {
+#pragma unroll
+      for (int r = 0; r < NT; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) a[r][C][h] = Pb[8 * r + g][2 * tq + h];
+    }
+  };
+  constexpr bool TWO = NT >= 8;  // two-warp panel when each warp gets >= 1 row per lane
   // A[:, my tile C] += Panel(kb) A[P(kb), tile C]; the pivot rows were zeroed when staged
   auto update_tile = [&](auto cc, int kb) {
     constexpr int C = decltype(cc)::value;
@@ -363,7 +466,11 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
 #ifdef HPS_GJ_PROFILE
   const long long p00 = clock64();
 #endif
-  if (warp == 0) panel(C0{}, 0);
+  if constexpr (TWO) {
+    if (warp < 2) panel2(C0{}, 0, warp);
+  } else {
+    if (warp == 0) panel(C0{}, 0);
+  }
 #ifdef HPS_GJ_PROFILE
   if (warp == 0 && lane == 0 && blockIdx.x == 0) atomicAdd((unsigned long long*)&g_gj_prof[6], (unsigned long long)(clock64() - p00));
 #endif
@@ -419,7 +526,7 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
 #ifdef HPS_GJ_PROFILE
         q2 = clock64();
 #endif
-        panel(C0{}, nx);
+        if constexpr (TWO) panel2(C0{}, nx, 0); else panel(C0{}, nx);
 #ifdef HPS_GJ_PROFILE
         q3 = clock64();
 #endif
@@ -429,12 +536,17 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
 #ifdef HPS_GJ_PROFILE
         q2 = clock64();
 #endif
-        panel(C1{}, nx);
+        if constexpr (TWO) panel2(C1{}, nx, 0); else panel(C1{}, nx);
 #ifdef HPS_GJ_PROFILE
         q3 = clock64();
 #endif
         if (!keep0) update_tile(C0{}, kb);
       }
+    } else if (TWO && nx < NT && warp == (nown ^ 1)) {
+      // helper of the next panel: one of my tile updates, the panel, then the other update
+      if (!keep0) update_tile(C0{}, kb);
+      panel2(C0{}, nx, 1);  // (the helper's tile index is unused)
+      if (!keep1) update_tile(C1{}, kb);
     } else {
       if (!keep0) update_tile(C0{}, kb);
       if (!keep1) update_tile(C1{}, kb);
