@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
   __shared__ int sP[2][8];            // pivot rows of the block
   __shared__ double sAP[W][8][17];    // per warp: A[P, its 16 columns] before the block update
   __shared__ double sDum[10];         // store sink for lanes that do not hold a staged row (never read)
-  __shared__ unsigned sCand[2][2];    // 2-warp panel: each warp's (hi, lo) argmax candidate
+  __shared__ unsigned sCand[4][2];    // multi-warp panel: each warp's (hi, lo) argmax candidate
   __shared__ __align__(16) double sRowP[2][8];  // 2-warp panel: the pivot row (by pivot parity)
   __shared__ unsigned char usedrow[NM];
   __shared__ int pivrow[NM], rowstep[NM];
@@ -347,11 +347,13 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
 #pragma unroll
       for (int h = 0; h < 2; ++h) a[r][C][h] = Pb[8 * r + g][2 * tq + h];
   };
-  // Two-warp panel (n > 32): the tile's owner (role 0, rows 0..NM/2) and a helper warp (role 1, rows
-  // NM/2..NM) factor the 8 columns together, 2 rows per lane. Per pivot: a 2-REDUX argmax in each
-  // warp, the two candidates exchanged through shared memory (64-thread named barrier), the pivot
-  // row published by its lane (second barrier). Half the per-lane rows of the single-warp panel.
-  constexpr int BAR_PANEL2 = 1, HALF = NM / 2, RPL2 = NM >= 64 ? NM / 64 : 1;
+  // Multi-warp panel (n > 32): the tile's owner (role 0) and PW - 1 helper warps (roles 1.., the
+  // other warps of the owner's aligned group of PW) factor the 8 columns together, NM / (32 PW)
+  // rows per lane. Per pivot: a 2-REDUX argmax in each warp, the candidates exchanged through
+  // shared memory (named barrier over the PW warps), the pivot row published by its lane (second
+  // barrier).
+  constexpr int PW = NT >= 16 ? 4 : 2;
+  constexpr int BAR_PANEL2 = 1, HALF = NM / PW, RPL2 = NM >= 32 * PW ? NM / (32 * PW) : 1;
   auto panel2 = [&](auto cc, int kb, int role) {
     constexpr int C = decltype(cc)::value;
     double(*Pb)[9] = sW[kb & 1];
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
 #pragma unroll
         for (int h = 0; h < 2; ++h) Pb[8 * r + g][2 * tq + h] = a[r][C][h];
     }
-    bar_sync(BAR_PANEL2, 64);
+    bar_sync(BAR_PANEL2, 32 * PW);
     double pr[RPL2][8];
     bool used[RPL2];
 #pragma unroll
@@ -385,11 +387,15 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
       const unsigned mh = __reduce_max_sync(0xffffffffu, bh);
       const unsigned ml = __reduce_max_sync(0xffffffffu, bh == mh ? bl : 0u);
       if (lane == 0) { sCand[role][0] = mh; sCand[role][1] = ml; }
-      bar_sync(BAR_PANEL2, 64);
-      const unsigned h0 = sCand[0][0], l0 = sCand[0][1], h1 = sCand[1][0], l1 = sCand[1][1];
-      const unsigned wl = (h1 > h0 || (h1 == h0 && l1 > l0)) ? l1 : l0;
+      bar_sync(BAR_PANEL2, 32 * PW);
+      unsigned wh = sCand[0][0], wl = sCand[0][1];
+#pragma unroll
+      for (int w2 = 1; w2 < PW; ++w2) {
+        const unsigned h2 = sCand[w2][0], l2 = sCand[w2][1];
+        if (h2 > wh || (h2 == wh && l2 > wl)) { wh = h2; wl = l2; }
+      }
       const int p = 127 - (int)(wl & 127u);
-      const int prole = p >= HALF, pq = p - prole * HALF, pl = pq & 31, pi = pq >> 5;
+      const int prole = p / HALF, pq = p - prole * HALF, pl = pq & 31, pi = pq >> 5;
       if (role == prole && lane == pl) {
 #pragma unroll
         for (int i = 0; i < RPL2; ++i)
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
               *reinterpret_cast<double2*>(&sRowP[t & 1][j]) = make_double2(pr[i][j], pr[i][j + 1]);
           }
       }
-      bar_sync(BAR_PANEL2, 64);
+      bar_sync(BAR_PANEL2, 32 * PW);
       double rp[8];
 #pragma unroll
       for (int j = 0; j < 8; j += 2) {
@@ -439,7 +445,7 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
 #pragma unroll
       for (int j = 0; j < 8; ++j) Pb[R][j] = pr[i][j];
     }
-    bar_sync(BAR_PANEL2, 64);
+    bar_sync(BAR_PANEL2, 32 * PW);
     if (role == 0) {
 #pragma unroll
       for (int r = 0; r < NT; ++r)
@@ -467,7 +473,7 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
   const long long p00 = clock64();
 #endif
   if constexpr (TWO) {
-    if (warp < 2) panel2(C0{}, 0, warp);
+    if (warp < PW) panel2(C0{}, 0, warp);
   } else {
     if (warp == 0) panel(C0{}, 0);
   }
@@ -542,10 +548,10 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
 #endif
         if (!keep0) update_tile(C0{}, kb);
       }
-    } else if (TWO && nx < NT && warp == (nown ^ 1)) {
+    } else if (TWO && nx < NT && (warp ^ nown) < PW) {
       // helper of the next panel: one of my tile updates, the panel, then the other update
       if (!keep0) update_tile(C0{}, kb);
-      panel2(C0{}, nx, 1);  // (the helper's tile index is unused)
+      panel2(C0{}, nx, warp ^ nown);  // (the helper's tile index is unused)
       if (!keep1) update_tile(C1{}, kb);
     } else {
       if (!keep0) update_tile(C0{}, kb);
