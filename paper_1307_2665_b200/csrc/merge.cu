@@ -492,34 +492,33 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
     const bool keep0 = warp == own && ownc == 0, keep1 = warp == own && ownc == 1;
     // stage my pivot rows of block kb, zeroing them in the tiles that take the update:
     // a_new = a + Panel A_P on non-pivot rows, a_new = Panel A_P on pivot rows (no cancellation)
+    // which of my register slots hold a pivot row of block kb (rows 8r + g), and its position t:
+    // a static loop over the slots then stages them with redirected stores (no dynamic register
+    // indexing, no indirect branches)
+    unsigned zmask = 0u;
+    unsigned long long tpos = 0ull;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const int p = sP[kb & 1][t], rp = p >> 3;
-      const bool mine = g == (p & 7);
-      // lanes not holding row p write to a dummy slot: no divergent branch
-      double* d = mine ? &sAP[warp][t][2 * tq] : sDum;
-      const bool z0 = mine && !keep0, z1 = mine && !keep1;
-      switch (rp) {  // warp-uniform
-#define HPS_GJ_STAGE(R)                                                       \
-  case R:                                                                     \
-    if constexpr (R < NT) {                                                   \
-      d[0] = a[R][0][0];                                                      \
-      d[1] = a[R][0][1];                                                      \
-      d[8] = a[R][1][0];                                                      \
-      d[9] = a[R][1][1];                                                      \
-      a[R][0][0] = z0 ? 0.0 : a[R][0][0];                                     \
-      a[R][0][1] = z0 ? 0.0 : a[R][0][1];                                     \
-      a[R][1][0] = z1 ? 0.0 : a[R][1][0];                                     \
-      a[R][1][1] = z1 ? 0.0 : a[R][1][1];                                     \
-    }                                                                         \
-    break;
-        HPS_GJ_STAGE(0) HPS_GJ_STAGE(1) HPS_GJ_STAGE(2) HPS_GJ_STAGE(3)
-        HPS_GJ_STAGE(4) HPS_GJ_STAGE(5) HPS_GJ_STAGE(6) HPS_GJ_STAGE(7)
-        HPS_GJ_STAGE(8) HPS_GJ_STAGE(9) HPS_GJ_STAGE(10) HPS_GJ_STAGE(11)
-        HPS_GJ_STAGE(12) HPS_GJ_STAGE(13) HPS_GJ_STAGE(14) HPS_GJ_STAGE(15)
-#undef HPS_GJ_STAGE
-        default: break;
+      const int p = sP[kb & 1][t];
+      if (g == (p & 7)) {
+        zmask |= 1u << (p >> 3);
+        tpos |= (unsigned long long)t << (4 * (p >> 3));
       }
+    }
+#pragma unroll
+    for (int r = 0; r < NT; ++r) {
+      const bool piv = (zmask >> r) & 1u;
+      const int t = (int)((tpos >> (4 * r)) & 15ull);
+      double* d = piv ? &sAP[warp][t][2 * tq] : sDum;
+      d[0] = a[r][0][0];
+      d[1] = a[r][0][1];
+      d[8] = a[r][1][0];
+      d[9] = a[r][1][1];
+      const bool z0 = piv && !keep0, z1 = piv && !keep1;
+      a[r][0][0] = z0 ? 0.0 : a[r][0][0];
+      a[r][0][1] = z0 ? 0.0 : a[r][0][1];
+      a[r][1][0] = z1 ? 0.0 : a[r][1][0];
+      a[r][1][1] = z1 ? 0.0 : a[r][1][1];
     }
     __syncwarp();
 #ifdef HPS_GJ_PROFILE
