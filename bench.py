@@ -324,6 +324,9 @@ def main():
     # Every step is one full problem: host sampling + grouping of the coefficients, their H2D
     # upload, the build, the H2D of the boundary data, the batched solve and the D2H of u. The
     # pipeline overlaps the host work of step i+1 with the device work of step i.
+    st = U = graph = None  # the device leg's captured state goes before the pipeline captures its own
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     pin_F = torch.from_numpy(np.ascontiguousarray(F_host)).pin_memory()
     pipe = solver.Pipeline(tree, nodes, device=dev, reuse_graphs=not args.no_graph)
     st = U = None

@@ -743,7 +743,15 @@ class Pipeline:
         if g is None:
             if len(slot) >= 4:  # bound the captured memory
                 slot.clear()
-            g = slot[key] = BuildGraph(inp, nrhs=nrhs)
+            torch = _torch()
+            try:
+                g = slot[key] = BuildGraph(inp, nrhs=nrhs)
+            except torch.OutOfMemoryError:  # two captured states do not fit: stay eager from here on
+                slot.clear()
+                self._graphs = [{}, {}]
+                self.reuse_graphs = False
+                torch.cuda.empty_cache()
+                return None
         return g
 
     @staticmethod
@@ -774,6 +782,8 @@ class BuildGraph:
     usual. Replays enqueue on the current stream. `launches` is the number of library kernel
     launches one build + solve replay performs."""
 
+    _warmed = set()
+
     def __init__(self, inp, nrhs=0):
         torch = _torch()
         lib = _native.load()
@@ -791,13 +801,17 @@ class BuildGraph:
         pool = torch.cuda.graph_pool_handle()
         self.stages = []
         n0 = lib.hps_launch_count()
+        key = (id(inp.layout), inp.ngroups, self._present, self.scalars, self.nrhs)
         with torch.cuda.stream(side):
-            st = build_device(self._inp)  # warm-up: lazy attributes and scratch sizes outside the capture
-            if self.nrhs:
-                solve_device(st, self._F)
-            del st
-            torch.cuda.synchronize()
-            torch.cuda.empty_cache()  # the warm-up state's memory (L=9: ~50 GB) back before the capture
+            if key not in BuildGraph._warmed:
+                # warm-up: lazy attributes and scratch sizes outside the capture (once per shape)
+                st = build_device(self._inp)
+                if self.nrhs:
+                    solve_device(st, self._F)
+                del st
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()  # the warm-up state's memory (L=9: ~50 GB) back before the capture
+                BuildGraph._warmed.add(key)
             n0 = lib.hps_launch_count()
 
             # thread_local: other host threads (the Pipeline's preparation thread) may sync or
@@ -809,14 +823,32 @@ class BuildGraph:
                 g.capture_begin(pool=pool, capture_error_mode="thread_local")
                 self.stages.append((name, g))
 
-            self.state = build_device(self._inp, stage_begin=begin)
-            self.stages[-1][1].capture_end()
-            self.solve_graph, self.U = None, None
-            if self.nrhs:
-                self.solve_graph = torch.cuda.CUDAGraph()
-                self.solve_graph.capture_begin(pool=pool, capture_error_mode="thread_local")
-                self.U = solve_device(self.state, self._F)
-                self.solve_graph.capture_end()
+            active = [None]
+
+            def begin_tracked(name):
+                begin(name)
+                active[0] = self.stages[-1][1]
+
+            try:
+                self.state = build_device(self._inp, stage_begin=begin_tracked)
+                self.stages[-1][1].capture_end()
+                active[0] = None
+                self.solve_graph, self.U = None, None
+                if self.nrhs:
+                    self.solve_graph = torch.cuda.CUDAGraph()
+                    self.solve_graph.capture_begin(pool=pool, capture_error_mode="thread_local")
+                    active[0] = self.solve_graph
+                    self.U = solve_device(self.state, self._F)
+                    self.solve_graph.capture_end()
+                    active[0] = None
+            except BaseException:
+                if active[0] is not None:  # leave the stream out of capture mode before re-raising
+                    try:
+                        active[0].capture_end()
+                    except BaseException:
+                        pass
+                self.stages, self.state = [], None
+                raise
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.launches = int(lib.hps_launch_count() - n0)
