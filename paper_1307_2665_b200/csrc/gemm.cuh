@@ -397,6 +397,42 @@ __global__ void __launch_bounds__(128, MINB) dgemm64_kernel(GemmParams p) {
     }
     return;
   }
+  if (p.blk_j1a) {
+    // merge update T = blkdiag + C S: gather all 32 block-diagonal addends of this lane first
+    // (maps, then the child entries, all independent loads in flight together), then store
+    const int n1 = p.M >> 1, gb = b + p.batch_offset;
+    const double* Ta = p.blk.a(gb);
+    const double* Tb = p.blk.bb(gb);
+    const double* rs[4];
+    bool rtop[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = min(m0 + arow + 8 * i, p.M - 1);
+      rtop[i] = r < n1;
+      rs[i] = rtop[i] ? Ta + (long long)p.blk_j1a[r] * p.blk.m : Tb + (long long)p.blk_j2b[r - n1] * p.blk.m;
+    }
+    int cm[2][4];
+    bool ctop[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = min(ccol0 + 16 * q + k, p.N - 1);
+        ctop[q][k] = c < n1;
+        cm[q][k] = ctop[q][k] ? p.blk_j1a[c] : p.blk_j2b[c - n1];
+      }
+    // column 16q + 4t + (2h + j) holds acc[i][q][j][h]
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double v = rtop[i] == ctop[q][k] ? __ldg(rs[i] + cm[q][k]) : 0.0;
+          acc[i][q][k & 1][k >> 1] = fma(p.alpha, acc[i][q][k & 1][k >> 1], v);
+        }
+  }
+  const double alpha = p.blk_j1a ? 1.0 : p.alpha;  // (applied above when the addend was fused)
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -409,15 +445,11 @@ __global__ void __launch_bounds__(128, MINB) dgemm64_kernel(GemmParams p) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (c + 2 * h >= p.N) continue;
-        double2 v = make_double2(p.alpha * acc[i][q][0][h], p.alpha * acc[i][q][1][h]);
+        double2 v = make_double2(alpha * acc[i][q][0][h], alpha * acc[i][q][1][h]);
         if (p.beta != 0.0) {
           const double2 o = *reinterpret_cast<const double2*>(dst + 2 * h);
           v.x += p.beta * o.x;
           v.y += p.beta * o.y;
-        }
-        if (p.blk_j1a) {
-          v.x += blk_value(p, b, r, c + 2 * h);
-          v.y += blk_value(p, b, r, c + 2 * h + 1);
         }
         bad |= !isfinite(v.x) || !isfinite(v.y);
         *reinterpret_cast<double2*>(dst + 2 * h) = v;
