@@ -70,7 +70,6 @@ __global__ void k_gather_c(ChildRef ch, const int* __restrict__ j1a, const int* 
   for (int c = lane; c < n3; c += 32) Cr[c] = src[j3[c]];
 }
 
-__device__ __forceinline__ int g_of(int lane) { return lane >> 2; }
 
 // Corner-mode projector entry (V V^T)[r][c] for an interface of n = nseg * q nodes.
 __device__ __forceinline__ double vvt(int r, int c, int q, int nseg, const double* vs, const double* ve) {
@@ -582,138 +581,6 @@ __global__ void __launch_bounds__(NT * 16) k_gj_blk(double* X, long long lda, lo
   if (s_sing && status && threadIdx.x == 0) atomicMax(status, status_base + (int)blockIdx.x);
 }
 
-// Fused merge for small interfaces (n3 <= 32, ne <= 192: the deepest depths), one CTA per merge:
-//   [X | R] gathered into shared memory -> deflate X -> Gauss-Jordan with partial pivoting on the
-//   augmented rows (so the right block becomes S = X^-1 R directly) -> S out ->
-//   T = blkdiag + C S on DMMA, with C and the blkdiag rows gathered straight from the children.
-// This replaces 6 launches per depth (gathers, deflation, inverse, two GEMMs), and their HBM round
-// trips, by one.
-template <int N3MAX, int NEMAX>
-__global__ void __launch_bounds__(128) k_merge_small(ChildRef ch, const int* __restrict__ j1a,
-                                                     const int* __restrict__ j2b, const int* __restrict__ j3a,
-                                                     const int* __restrict__ j3b, int n3, int ne, int q,
-                                                     const double* __restrict__ vs, const double* __restrict__ ve,
-                                                     double* __restrict__ S_out, double* __restrict__ T_out,
-                                                     int* status) {
-  constexpr int LDA = N3MAX + NEMAX + 1;  // odd stride: conflict-free column walks
-  extern __shared__ __align__(16) double aug[];  // N3MAX x LDA
-  __shared__ double red[32];
-  __shared__ int s_p;
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n1 = ne / 2, w = n3 + ne;
-  const double* Ta = ch.a(b);
-  const double* Tb = ch.bb(b);
-  // gather [X | R]
-  for (int e = tid; e < n3 * w; e += 128) {
-    const int r = e / w, c = e - r * w;
-    const double* ra = Ta + (long long)j3a[r] * ch.m;
-    const double* rb = Tb + (long long)j3b[r] * ch.m;
-    double v;
-    if (c < n3) v = ra[j3a[c]] - rb[j3b[c]];
-    else if (c < n3 + n1) v = -ra[j1a[c - n3]];
-    else v = rb[j2b[c - n3 - n1]];
-    aug[r * LDA + c] = v;
-  }
-  __syncthreads();
-  if (n3 > q) {  // deflate the corner null modes
-    double dm = 0.0;
-    for (int i = tid; i < n3; i += 128) dm = fmax(dm, fabs(aug[i * LDA + i]));
-    const double sigma = block_max(dm, red);
-    const int nseg = n3 / q;
-    for (int e = tid; e < n3 * n3; e += 128) {
-      const int r = e / n3, c = e - r * n3;
-      if (abs(r / q - c / q) <= 1) aug[r * LDA + c] += sigma * vvt(r, c, q, nseg, vs, ve);
-    }
-    __syncthreads();
-  }
-  bool singular = false;
-  for (int k = 0; k < n3; ++k) {
-    if (warp == 0) {
-      const double v = lane >= k && lane < n3 ? fabs(aug[lane * LDA + k]) : -1.0;
-      const unsigned long long key = v < 0 ? 0ull : (unsigned long long)__double_as_longlong(v);
-      const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-      const unsigned cand = (hi == mhi && lo == mlo && lane >= k && lane < n3) ? (unsigned)lane : 0xffffffffu;
-      const int p = (int)__reduce_min_sync(0xffffffffu, cand);
-      if (lane == 0) s_p = p < n3 ? p : k;
-    }
-    __syncthreads();
-    const int p = s_p;
-    if (p != k)
-      for (int c = tid; c < w; c += 128) {
-        const double t0 = aug[k * LDA + c];
-        aug[k * LDA + c] = aug[p * LDA + c];
-        aug[p * LDA + c] = t0;
-      }
-    __syncthreads();
-    const double piv = aug[k * LDA + k];
-    singular |= (piv == 0.0);
-    const double inv = fast_rcp(piv);
-    // eliminate column k from every other row (columns > k only; column k is never read again)
-    const int wc = w - k - 1;
-    for (int e = tid; e < n3 * wc; e += 128) {
-      const int r = e / wc, c = k + 1 + (e - r * wc);
-      if (r != k) aug[r * LDA + c] = fma(-aug[r * LDA + k] * inv, aug[k * LDA + c], aug[r * LDA + c]);
-    }
-    __syncthreads();
-    for (int c = k + 1 + tid; c < w; c += 128) aug[k * LDA + c] *= inv;
-    __syncthreads();
-  }
-  // S = right block
-  double* S = S_out + (long long)b * n3 * ne;
-  bool bad = false;
-  for (int e = tid; e < n3 * ne; e += 128) {
-    const int r = e / ne, c = e - r * ne;
-    const double v = aug[r * LDA + n3 + c];
-    bad |= !isfinite(v);
-    S[e] = v;
-  }
-  if ((singular || bad) && status) atomicMax(status, b);
-  // T = blkdiag + C S: warp = 8 output rows x 64-column chunks; C rows kept in registers
-  double* T = T_out + (long long)b * ne * ne;
-  for (int rt = warp; rt < ne / 8; rt += 4) {
-    const int r = rt * 8 + g_of(lane);
-    const bool top = r < n1;
-    const double* src = top ? Ta + (long long)j1a[r] * ch.m : Tb + (long long)j2b[r - n1] * ch.m;
-    const int* j3 = top ? j3a : j3b;
-    const int* jk = top ? j1a : j2b;
-    const int tq = lane & 3;
-    double af[N3MAX / 4];
-#pragma unroll
-    for (int ks = 0; ks < N3MAX / 4; ++ks) af[ks] = 4 * ks < n3 ? src[j3[4 * ks + tq]] : 0.0;
-    for (int cb = 0; cb < ne; cb += 64) {
-      double acc[8][2];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = cb + 8 * j + 2 * tq + h;
-          double v = 0.0;
-          if (c < ne && (c < n1) == top) v = src[jk[top ? c : c - n1]];
-          acc[j][h] = v;
-        }
-      }
-#pragma unroll
-      for (int ks = 0; ks < N3MAX / 4; ++ks)
-        if (4 * ks < n3) {
-          const double* Sr = aug + (4 * ks + tq) * LDA + n3 + cb + g_of(lane);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const double bv = (cb + 8 * j + g_of(lane) < ne) ? Sr[8 * j] : 0.0;
-            dmma_8x8x4(acc[j][0], acc[j][1], af[ks], bv);
-          }
-        }
-      double* Tr = T + (long long)r * ne;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int c = cb + 8 * j + 2 * tq;
-        if (c < ne) *reinterpret_cast<double2*>(Tr + c) = make_double2(acc[j][0], acc[j][1]);
-      }
-    }
-  }
-}
-
 // Deflation X += sigma V V^T, sigma = max |diag X| (reduced by k_gather_xr before any CTA here
 // modifies a diagonal block): one CTA per (segment row, merge).
 __global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs, const double* __restrict__ ve,
@@ -829,20 +696,6 @@ extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const d
     return HPS_ERR_ARG;
   }
   const int n1 = ne / 2;
-  static const int fuse_small = getenv("HPS_MERGE_FUSED") ? atoi(getenv("HPS_MERGE_FUSED")) : 0;  // measured slower (r01)
-  if (fuse_small && n3 <= 32 && ne <= 192 && ne % 16 == 0) {
-    ChildRef chs{T_child, child_stride, child_idx, m};
-    constexpr size_t smem = sizeof(double) * 32 * (32 + 192 + 1);
-    static bool attr = false;
-    if (!attr) {
-      HPS_CUDA_CHECK(cudaFuncSetAttribute(k_merge_small<32, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
-    k_merge_small<32, 192><<<nbatch, 128, smem, st>>>(chs, maps, maps + n1, maps + 2 * n1, maps + 2 * n1 + n3, n3, ne, q,
-                                                     vmode, vmode + q, S_out, T_out, status);
-    HPS_LAUNCH_CHECK();
-    return HPS_OK;
-  }
   const int* j1a = maps;
   const int* j2b = maps + n1;
   const int* j3a = maps + 2 * n1;
