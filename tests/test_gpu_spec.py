@@ -139,3 +139,23 @@ def test_small_trees_non_square_domain_mixed_derivative_against_oracle(L):
     u, uo = solver.solve(st, F), O.solve(ost, F)
     assert rel(O.leaf_cheb_boundary(ost, u), O.leaf_cheb_boundary(ost, uo)) < 1e-10
     assert rel(O.leaf_flux(ost, u), O.leaf_flux(ost, uo)) < 1e-10
+
+
+def test_leaf_resonance_raises_like_the_reference():
+    # c = -lambda_min of the discrete interior operator makes every leaf's A_ii singular: the build
+    # must raise LeafResonanceError for the first group in first-occurrence order (solver.py:235-239)
+    L = 1
+    tree, nodes = _tree(L)
+    geom = O.Geometry(16, tree.leaf_width, tree.leaf_height)
+    A = O.assemble_operator(geom, {"c11": 1.0, "c12": 0.0, "c22": 1.0, "c1": 0.0, "c2": 0.0, "c": 0.0})
+    Aii = A[np.ix_(geom.J_i, geom.J_i)]
+    lam = np.linalg.eigvals(Aii)
+    lam_min = float(np.min(lam[np.abs(lam.imag) < 1e-9].real))
+    co = CoefficientField(c=-lam_min)
+    with pytest.raises(P.errors.LeafResonanceError) as ei:
+        solver.build(tree, nodes, co)
+    assert ei.value.box == (4 ** L - 1)  # the first leaf: one group, first occurrence
+    assert ei.value.cond > 1e13
+    ot = O.build_tree((0.0, 1.0, 0.0, 1.0), L, 16)
+    with pytest.raises(ArithmeticError):
+        O.build(ot, coeff_dict(co))
