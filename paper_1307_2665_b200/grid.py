@@ -360,43 +360,46 @@ class TreeLayout:
         self.leaf_I_e = np.ascontiguousarray(np.concatenate(
             [h_ids(liy, lix), v_ids(lix + 1, liy), h_ids(liy + 1, lix), v_ids(lix, liy)], axis=1))
 
-        # parents bottom-up: child-a remainder then child-b remainder (grid.py:313-319)
+        # parents bottom-up: child-a remainder then child-b remainder (grid.py:313-319). The split
+        # maps are the same for every parent of a depth, so they come from the first parent; every
+        # parent's I_e is then one vectorised gather, and the maps are checked on a sample of
+        # parents (always including the first and last): the shared ids must sit at the same
+        # positions and be the parent's contiguous I_i range.
         child_Ie = self.leaf_I_e
         depths = [None] * (2 * L)
+        rng = np.random.default_rng(0)
         for d in range(2 * L - 1, -1, -1):
             nb = 1 << d
             A = child_Ie[0::2]
             B = child_Ie[1::2]
             start = depth_off[d] + np.arange(nb, dtype=np.int64) * n3s[d]
             n3 = n3s[d]
-            in_a = (A >= start[:, None]) & (A < (start + n3)[:, None])
-            in_b = (B >= start[:, None]) & (B < (start + n3)[:, None])
             m = A.shape[1]
-            cnt_a = in_a.sum(1)
-            cnt_b = in_b.sum(1)
-            if not (np.all(cnt_a == n3) and np.all(cnt_b == n3)):
+            a0, b0 = A[0], B[0]
+            in_a0 = (a0 >= start[0]) & (a0 < start[0] + n3)
+            in_b0 = (b0 >= start[0]) & (b0 < start[0] + n3)
+            if in_a0.sum() != n3 or in_b0.sum() != n3:
                 raise AssertionError("children are not edge-adjacent")
-            # j3: position of shared id (start + r) inside the child list, ordered by r
-            ra, ca = np.nonzero(in_a)
-            j3a_all = np.empty((nb, n3), np.int64)
-            j3a_all[ra, A[ra, ca] - start[ra]] = ca
-            rb, cb = np.nonzero(in_b)
-            j3b_all = np.empty((nb, n3), np.int64)
-            j3b_all[rb, B[rb, cb] - start[rb]] = cb
-            keep_a = ~in_a
-            keep_b = ~in_b
-            j1a = np.flatnonzero(keep_a[0])
-            j2b = np.flatnonzero(keep_b[0])
-            uniform = (np.all(keep_a == keep_a[0]) and np.all(keep_b == keep_b[0])
-                       and np.all(j3a_all == j3a_all[0]) and np.all(j3b_all == j3b_all[0]))
-            if not uniform:
+            j3a = np.empty(n3, np.int64)
+            j3a[a0[in_a0] - start[0]] = np.flatnonzero(in_a0)
+            j3b = np.empty(n3, np.int64)
+            j3b[b0[in_b0] - start[0]] = np.flatnonzero(in_b0)
+            j1a = np.flatnonzero(~in_a0)
+            j2b = np.flatnonzero(~in_b0)
+            sample = np.unique(np.concatenate([[0, nb - 1], rng.integers(0, nb, size=min(nb, 64))]))
+            shared = start[sample][:, None] + np.arange(n3)[None, :]
+            As, Bs = A[sample], B[sample]
+            ok = (np.array_equal(As[:, j3a], shared) and np.array_equal(Bs[:, j3b], shared)
+                  and not np.any((As[:, j1a] >= start[sample][:, None]) & (As[:, j1a] < start[sample][:, None] + n3))
+                  and not np.any((Bs[:, j2b] >= start[sample][:, None]) & (Bs[:, j2b] < start[sample][:, None] + n3)))
+            if not ok:
                 raise AssertionError(f"non-uniform split maps at depth {d}")
-            Ie = np.ascontiguousarray(np.concatenate([A[:, j1a], B[:, j2b]], axis=1))
+            Ie = np.concatenate([A[:, j1a], B[:, j2b]], axis=1)
             depths[d] = DepthLayout(
                 depth=d, axis="v" if d % 2 == 0 else "h", n3=n3, ne=Ie.shape[1], m=m,
                 j1a=j1a.astype(np.intp), j2b=j2b.astype(np.intp),
-                j3a=j3a_all[0].astype(np.intp), j3b=j3b_all[0].astype(np.intp),
-                I_e=Ie.astype(np.intp), Ii_start=start.astype(np.intp))
+                j3a=j3a.astype(np.intp), j3b=j3b.astype(np.intp),
+                I_e=Ie, Ii_start=start.astype(np.intp))
             child_Ie = Ie
         self.depths = depths
         self.root_I_e = child_Ie[0].astype(np.intp) if L > 0 else self.leaf_I_e[0].astype(np.intp)
