@@ -228,42 +228,66 @@ def _eval_field(f, xs, ys, threads=True, out=None):
     chunks in a thread pool (numpy ufuncs release the GIL). Each element is computed by the same
     SIMD code path as in a single call, since chunks are whole leaves, 256 points each.
     `out(shape)` optionally allocates the result (e.g. in pinned host memory); the chunks are then
-    written straight into it instead of being concatenated."""
+    written straight into it instead of being concatenated. Returns (values, all_finite): the
+    finiteness check runs per chunk inside the workers."""
     n = xs.shape[0]
     if not threads or n < 256:
-        return f(xs, ys)
+        v = f(xs, ys)
+        return v, bool(np.all(np.isfinite(v)))
     nchunk = max(1, min(16, n // 64))
     bounds = np.linspace(0, n, nchunk + 1).astype(int)
     first = f(xs[bounds[0]:bounds[1]], ys[bounds[0]:bounds[1]])
     if np.isscalar(first) or np.ndim(first) == 0:  # the callable returned a scalar
-        return f(xs, ys)
+        v = f(xs, ys)
+        return v, bool(np.all(np.isfinite(v)))
     res = out(xs.shape) if out is not None else np.empty(xs.shape)
     res[bounds[0]:bounds[1]] = np.broadcast_to(np.asarray(first, dtype=float), (bounds[1] - bounds[0], xs.shape[1]))
+    ok0 = bool(np.all(np.isfinite(res[bounds[0]:bounds[1]])))
 
     def run(ab):
         b0, b1 = ab
         q = f(xs[b0:b1], ys[b0:b1])
         if np.isscalar(q) or np.ndim(q) == 0:
-            return False
+            return None
         res[b0:b1] = np.broadcast_to(np.asarray(q, dtype=float), (b1 - b0, xs.shape[1]))
-        return True
+        return bool(np.all(np.isfinite(res[b0:b1])))
 
-    if not all(_pool().map(run, zip(bounds[1:-1], bounds[2:]))):
-        return f(xs, ys)
-    return res
+    flags = list(_pool().map(run, zip(bounds[1:-1], bounds[2:])))
+    if any(fl is None for fl in flags):
+        v = f(xs, ys)
+        return v, bool(np.all(np.isfinite(v)))
+    return res, ok0 and all(flags)
+
+
+_POINTS = {}
+
+
+def _leaf_points(lay, geom):
+    """Chebyshev grid points of every leaf (heap leaf order), cached per (tree, geometry)."""
+    key = (id(lay), geom.p, geom.width, geom.height)
+    v = _POINTS.get(key)
+    if v is None:
+        lc = lay.leaf_cells
+        xs = lay.xline[lc[:, 0]][:, None] + geom.grid_x[None, :]
+        ys = lay.yline[lc[:, 1]][:, None] + geom.grid_y[None, :]
+        xs.setflags(write=False)
+        ys.setflags(write=False)
+        v = _POINTS[key] = (xs, ys)
+    return v
 
 
 def _sample(coeffs, lay, geom, threads=True, out=None):
     """Coefficient samples on all leaf Chebyshev grids, heap leaf order (solver.py:196-206)."""
-    lc = lay.leaf_cells
-    xs = lay.xline[lc[:, 0]][:, None] + geom.grid_x[None, :]
-    ys = lay.yline[lc[:, 1]][:, None] + geom.grid_y[None, :]
+    xs, ys = _leaf_points(lay, geom)
     fields = {}
     for name in COEFF_NAMES:
         f = getattr(coeffs, name)
-        fields[name] = _eval_field(f, xs, ys, threads, out) if callable(f) else float(f)
-        v = np.atleast_1d(fields[name])
-        if not np.all(np.isfinite(v)):
+        if callable(f):
+            fields[name], finite = _eval_field(f, xs, ys, threads, out)
+        else:
+            fields[name] = float(f)
+            finite = bool(np.isfinite(fields[name]))
+        if not finite:
             bad = np.argwhere(~np.isfinite(np.broadcast_to(fields[name], xs.shape)))
             i, k = (bad[0] if bad.size else (0, 0))
             raise ValueError(f"coefficient {name} is not finite at node ({xs[i, k]}, {ys[i, k]})")
