@@ -563,7 +563,12 @@ int leaf16v3_grid(int ngroups) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static int per_sm = getenv("HPS_LEAF3_CTAS_PER_SM") ? atoi(getenv("HPS_LEAF3_CTAS_PER_SM")) : 2;
-  return std::max(1, std::min(ngroups, per_sm * sms));
+  // the smallest grid with the same leaves per CTA as a full one: the grid-stride loop's critical
+  // path is unchanged, and the spare CTA slots let other streams' small kernels (the next
+  // problem's grouping in solver.Pipeline) run beside the leaf stage (cfg2: 293 of 296)
+  const int full = std::max(1, std::min(ngroups, per_sm * sms));
+  const int per_cta = (ngroups + full - 1) / full;
+  return std::max(1, (ngroups + per_cta - 1) / per_cta);
 }
 
 int launch_leaf16v3(LeafArgs& a, cudaStream_t st) {

@@ -689,7 +689,11 @@ class Pipeline:
         self._jobs = 0
         self.tree, self.nodeset = tree, nodeset
         self.device = torch.device(device if device is not None else "cuda")
-        self._upload = torch.cuda.Stream(self.device)
+        # the next problem's uploads and grouping kernels run beside the current build: highest
+        # stream priority, so they take SM slots as soon as any free up
+        import os as _os
+        prio = int(_os.environ.get("HPS_UPLOAD_PRIORITY", "1"))
+        self._upload = torch.cuda.Stream(self.device, priority=-prio if prio else 0)
         self._main = torch.cuda.Stream(self.device)
         self._d2h = torch.cuda.Stream(self.device)
         import concurrent.futures
