@@ -24,13 +24,17 @@ __global__ void k_splitk_reduce(GemmParams p) {
   }
 }
 
-// Split-K scratch: one growing device buffer (builds repeat the same shapes, so it settles after
-// the first build). The library enqueues on one stream at a time. A buffer it outgrows is never
-// freed: a captured CUDA graph (solver.BuildGraph) may still reference it.
-static double* g_splitk = nullptr;
-static size_t g_splitk_n = 0;
+// Split-K scratch: two growing device buffers, one for the library's own side stream (the
+// interface inverse runs independent GEMMs there concurrently) and one for the caller's stream
+// (the library enqueues on one caller stream at a time). Builds repeat the same shapes, so they
+// settle after the first build. An outgrown buffer is never freed: a captured CUDA graph
+// (solver.BuildGraph) may still reference it.
+cudaStream_t fork_side_stream();  // merge.cu
+static double* g_splitk[2] = {nullptr, nullptr};
+static size_t g_splitk_n[2] = {0, 0};
 static double* splitk_scratch(size_t n, cudaStream_t st) {
-  if (n > g_splitk_n) {
+  const int slot = (st != nullptr && st == fork_side_stream()) ? 1 : 0;
+  if (n > g_splitk_n[slot]) {
     // no allocation inside a stream capture (it would invalidate the capture): the caller then
     // runs without split-K. BuildGraph warms up first, so captures normally find it allocated.
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -40,10 +44,10 @@ static double* splitk_scratch(size_t n, cudaStream_t st) {
       cudaGetLastError();
       return nullptr;
     }
-    g_splitk = fresh;
-    g_splitk_n = n;
+    g_splitk[slot] = fresh;
+    g_splitk_n[slot] = n;
   }
-  return g_splitk;
+  return g_splitk[slot];
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool VEC = true>

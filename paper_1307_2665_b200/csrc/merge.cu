@@ -646,6 +646,35 @@ static int gemm(int M, int N, int K, int batch, double alpha, const double* A, l
 //   A11 <- inv(A11); T12 = A11 A12; T21 = A21 A11; A22 <- A22 - A21 T12; A22 <- inv(A22)
 //   A12 <- -T12 A22; A21 <- -A22 T21; A11 <- A11 - A12 T21
 // Base blocks (<= 128) use pivoted Gauss-Jordan in shared memory.
+// Side stream + event ring of the recursive inverse: the independent GEMM pairs of each level run
+// concurrently (fork/join through events; captured CUDA graphs get parallel branches).
+struct ForkCtx {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[64];
+  int next = 0;
+  bool ok = false;
+};
+static ForkCtx& fork_ctx() {
+  static ForkCtx c;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    c.ok = cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; i < 64 && c.ok; ++i) c.ok = cudaEventCreateWithFlags(&c.ev[i], cudaEventDisableTiming) == cudaSuccess;
+    cudaGetLastError();
+  }
+  return c;
+}
+cudaStream_t fork_side_stream() { return fork_ctx().ok ? fork_ctx().side : nullptr; }
+
+static cudaEvent_t record_on(cudaStream_t st) {
+  ForkCtx& c = fork_ctx();
+  cudaEvent_t e = c.ev[c.next];
+  c.next = (c.next + 1) & 63;
+  cudaEventRecord(e, st);
+  return e;
+}
+
 static int inverse_rec(double* A, long long lda, long long strideA, int n, int batch, double* tmp, int* status,
                        int status_base, cudaStream_t st) {
   static const int base = getenv("HPS_INV_BASE") ? atoi(getenv("HPS_INV_BASE")) : 128;
@@ -659,13 +688,22 @@ static int inverse_rec(double* A, long long lda, long long strideA, int n, int b
   double* T21 = tmp + (long long)batch * h * h2;  // h2 x h
   double* deeper = T21 + (long long)batch * h * h2;
   const long long sT = (long long)h * h2;
+  static const int par = getenv("HPS_INV_FORK") ? atoi(getenv("HPS_INV_FORK")) : 1;
+  ForkCtx& fc = fork_ctx();
+  const bool fork = par && fc.ok;
+  cudaStream_t s2 = fork ? fc.side : st;
   HPS_TRY(inverse_rec(A11, lda, strideA, h, batch, deeper, status, status_base, st));
+  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(s2, record_on(st), 0));
+  // T21 = A21 inv(A11) on the side stream, T12 = inv(A11) A12 and the Schur update on the main one
+  HPS_TRY(gemm(h2, h, h, batch, 1.0, A21, lda, strideA, A11, lda, strideA, 0.0, T21, h, sT, s2));
   HPS_TRY(gemm(h, h2, h, batch, 1.0, A11, lda, strideA, A12, lda, strideA, 0.0, T12, h2, sT, st));
-  HPS_TRY(gemm(h2, h, h, batch, 1.0, A21, lda, strideA, A11, lda, strideA, 0.0, T21, h, sT, st));
   HPS_TRY(gemm(h2, h2, h, batch, -1.0, A21, lda, strideA, T12, h2, sT, 1.0, A22, lda, strideA, st));
   HPS_TRY(inverse_rec(A22, lda, strideA, h2, batch, deeper, status, status_base, st));
+  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(s2, record_on(st), 0));
+  // A21 = -inv(S) T21 on the side stream (after T21 there), A12 = -T12 inv(S) on the main one
+  HPS_TRY(gemm(h2, h, h2, batch, -1.0, A22, lda, strideA, T21, h, sT, 0.0, A21, lda, strideA, s2));
   HPS_TRY(gemm(h, h2, h2, batch, -1.0, T12, h2, sT, A22, lda, strideA, 0.0, A12, lda, strideA, st));
-  HPS_TRY(gemm(h2, h, h2, batch, -1.0, A22, lda, strideA, T21, h, sT, 0.0, A21, lda, strideA, st));
+  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(st, record_on(s2), 0));  // join: T21 and A21 done
   HPS_TRY(gemm(h, h, h2, batch, -1.0, A12, lda, strideA, T21, h, sT, 1.0, A11, lda, strideA, st));
   return HPS_OK;
 }
