@@ -10,9 +10,10 @@
 //     list of still-active rows only. They update the next panel's columns first, then signal
 //     the panel warps through a named barrier, so factor(k+1) overlaps update(k) on the
 //     remaining columns.
-// After the last panel, a blocked back substitution (DMMA off-diagonal blocks) yields
-// X = U^{-1} Y in place of Y in the pivot rows. The augmented matrix lives in a per-CTA global
-// scratch slot (200 x 260 fp64, L2-resident).
+// After the last panel, a blocked back substitution (leaf3_backsub: Y staged in shared memory,
+// precomputed inverses of the 16x16 diagonal blocks, everything on DMMA) yields X = U^{-1} Y.
+// The augmented matrix lives in a per-CTA global scratch slot (200 x 260 fp64, L2-resident),
+// followed by the 13 diagonal-block inverses.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -31,7 +32,6 @@ __device__ long long g_leaf3_prof[1024][16];
 #endif
 namespace l3 {
 constexpr int NI = 196, NB = 60, NG = 64, NCOLS = 257, LDM = 260, MROWS = 200;
-constexpr int NRHS = LDM - NI;  // 64 (61 used)
 constexpr int THREADS = 256;
 constexpr int NPW = 4;  // panel warps
 constexpr int SA = 20;  // multiplier row stride (== 4 mod 16)
@@ -42,12 +42,189 @@ constexpr int OFF_A16 = 0;                         // 2 x MROWS x SA
 constexpr int OFF_U12 = OFF_A16 + 2 * MROWS * SA;  // 16 x SB
 constexpr int OFF_LU = OFF_U12 + 16 * SB;          // 16 x 17
 constexpr int OFF_PROW = OFF_LU + 16 * 17;         // 2 x 16
-constexpr int NDBL = OFF_PROW + 32;
+constexpr int BS_OFF_U = NI * 64;                  // back substitution: Y (NI x 64), then 2 x Uinv
+constexpr int NDBL = std::max(OFF_PROW + 32, BS_OFF_U + 2 * 16 * 20);
 constexpr int NINT = 2 * MROWS + NI + NI + NB + 64;
 constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4 + 64;
 constexpr int BAR_PANEL = 1;      // panel warps only (128 threads)
 }  // namespace l3
 
+
+
+// Back substitution X = U^{-1} Y for the 13 pivot blocks, Psi = -X out, T1 = L43e + L43i Psi staged
+// in shared memory (64 x ST1 at OFF_U12) for the T epilogue. Returns this thread's max |X[:, probe]|.
+__device__ __noinline__ double leaf3_backsub(double* __restrict__ M, const int* __restrict__ sPiv, double* __restrict__ Psi,
+                                             const double* __restrict__ cL43i, const double* __restrict__ cL43e) {
+  using namespace l3;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  (void)lane;
+    // ================= back substitution (right-looking), fused with T1 = L43i Psi =================
+    // Y (the 64 right-hand-side columns of every pivot row, in pivot-step order) is staged once
+    // into shared memory (XOR-swizzled rows of 64), so the 13-block chain never waits on L2.
+    //   once:   Uinv_k = U11_k^{-1} for all 13 diagonal blocks (one column per thread), to global;
+    //   per block, from the last:
+    //     X_kp = Uinv_kp Y_kp on DMMA (warp w: columns 8w..8w+7, in place), Psi rows out;
+    //     T1 += L43i[:, blk] (-X_kp) and Y_j -= U[P_j, blk] X_kp (j < kp), all warps on DMMA, with
+    //     Uinv (cp.async) and the U / L43i fragments (registers) loaded one block ahead.
+    double* sYb = sm;                       // NI x 64 (swizzled)
+    double* sUb = sm + BS_OFF_U;            // 2 x 16 x SUI: Uinv of the block (cp.async)
+    constexpr int SUI = 20;                 // == 4 mod 16: conflict-free A fragments
+    double* UinvG = M + (long long)MROWS * LDM;  // 13 x 16 x 16 in the CTA's scratch slot
+    auto yidx = [](int r, int c) { return r * 64 + (c ^ ((r & 7) << 3)); };
+    double t1acc[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t1acc[j][0] = t1acc[j][1] = 0.0;
+    double pm = 0.0;
+    P3_T(t_st);
+    {  // U11 blocks -> smem (13 x 16 x 16, zero outside the block), then Uinv columns -> global
+      for (int e = tid; e < NPANEL * 128; e += THREADS) {
+        const int blk = e >> 7, r = (e >> 3) & 15, c = (e & 7) * 2, k0 = 16 * blk, kb = min(16, NI - k0);
+        double2 v = make_double2(0.0, 0.0);
+        if (r < kb) v = *reinterpret_cast<const double2*>(M + (long long)sPiv[k0 + r] * LDM + k0 + c);
+        if (c >= kb) v.x = 0.0;
+        if (c + 1 >= kb) v.y = 0.0;
+        *reinterpret_cast<double2*>(sm + blk * 256 + r * 16 + c) = v;
+      }
+      __syncthreads();
+      if (tid < NPANEL * 16) {
+        const int blk = tid >> 4, c = tid & 15, kb = min(16, NI - 16 * blk);
+        const double* U = sm + blk * 256;
+        double v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = r == c ? 1.0 : 0.0;
+#pragma unroll
+        for (int r = 15; r >= 0; --r) {
+          if (r <= c && r < kb) {
+            const double x = v[r] * fast_rcp(U[r * 16 + r]);
+            v[r] = x;
+#pragma unroll
+            for (int b = 0; b < r; ++b) v[b] = fma(-U[b * 16 + r], x, v[b]);
+          }
+        }
+        double* out = UinvG + blk * 256 + c;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) out[r * 16] = (c < kb && r < kb) ? v[r] : 0.0;
+      }
+      __syncthreads();  // Uinv (global) visible to the cp.async readers below; U11 staging dead
+    }
+    auto load_uinv = [&](int kp, int buf) {  // 16 rows x 16 doubles, 8 x 16 B per row (threads 0-127)
+      if (tid < 128) {
+        const int r = tid >> 3, c = (tid & 7) * 2;
+        cp_async16(sUb + buf * 16 * SUI + r * SUI + c, UinvG + kp * 256 + r * 16 + c, true);
+      }
+      cp_async_commit();
+    };
+    // A fragments loaded into registers one block ahead: U[P_j, blk] for this warp's Y-update
+    // items (it = warp + 8m) and -L43i[8w+g, blk] for its T1 rows
+    double afU[3][4], afT[4];
+    auto load_frags = [&](int kp) {
+      const int k0 = 16 * kp, kb = min(16, NI - k0);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int ri = (warp + 8 * m) * 8 + g;
+        const bool rv = ri < k0;
+        const double* Urow = M + (long long)(rv ? sPiv[ri] : 0) * LDM + k0;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) afU[m][ks] = (rv && 4 * ks < kb) ? Urow[4 * ks + tq] : 0.0;
+      }
+      const double* Arow = cL43i + (long long)(warp * 8 + g) * NI + k0;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) afT[ks] = 4 * ks < kb ? -__ldg(Arow + 4 * ks + tq) : 0.0;
+    };
+    load_uinv(NPANEL - 1, (NPANEL - 1) & 1);
+    load_frags(NPANEL - 1);
+    for (int e = tid; e < NI * 32; e += THREADS) {
+      const int r = e >> 5, c = (e & 31) * 2;
+      const double2 v = *reinterpret_cast<const double2*>(M + (long long)sPiv[r] * LDM + NI + c);
+      *reinterpret_cast<double2*>(sYb + yidx(r, c)) = v;
+    }
+    for (int kp = NPANEL - 1; kp >= 0; --kp) {
+      const int k0 = 16 * kp, kb = min(16, NI - k0), buf = kp & 1;
+      if (kp == NPANEL - 1) P3_ADD(10, t_st, tid == 0);
+      P3_T(t_w);
+      cp_async_wait<0>();
+      __syncthreads();  // Y_kp final, Uinv_kp staged, previous block's readers done
+      P3_ADD(11, t_w, tid == 0);
+      P3_T(t_s);
+      if (kp > 0) load_uinv(kp - 1, buf ^ 1);
+      {  // X_kp = Uinv_kp Y_kp: this warp's 8 columns, both 8-row halves, in place
+        const double* Ui = sUb + buf * 16 * SUI;
+        double x0[2] = {0.0, 0.0}, x1[2] = {0.0, 0.0};
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          if (4 * ks < kb) {
+            const double b = sYb[yidx(k0 + 4 * ks + tq, 8 * warp + g)];
+            dmma_8x8x4(x0[0], x0[1], Ui[g * SUI + 4 * ks + tq], b);
+            dmma_8x8x4(x1[0], x1[1], Ui[(g + 8) * SUI + 4 * ks + tq], b);
+          }
+        __syncwarp();
+        const int col = 8 * warp + 2 * tq;
+        if (g < kb) {
+          *reinterpret_cast<double2*>(sYb + yidx(k0 + g, col)) = make_double2(x0[0], x0[1]);
+          if (col < NB) __stcs(reinterpret_cast<double2*>(Psi + (long long)(k0 + g) * NB + col), make_double2(-x0[0], -x0[1]));
+        }
+        if (g + 8 < kb) {
+          *reinterpret_cast<double2*>(sYb + yidx(k0 + g + 8, col)) = make_double2(x1[0], x1[1]);
+          if (col < NB) __stcs(reinterpret_cast<double2*>(Psi + (long long)(k0 + g + 8) * NB + col), make_double2(-x1[0], -x1[1]));
+        }
+        if (col == NB) pm = fmax(pm, fmax(g < kb ? fabs(x0[0]) : 0.0, g + 8 < kb ? fabs(x1[0]) : 0.0));
+      }
+      __syncthreads();
+      P3_ADD(12, t_s, tid == 0);
+      P3_T(t_u);
+      // T1 rows 8w..8w+7 += L43i[:, blk] (-X_kp)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        if (4 * ks < kb) {
+          const int xr = k0 + 4 * ks + tq;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dmma_8x8x4(t1acc[j][0], t1acc[j][1], afT[ks], sYb[yidx(xr, 8 * j + g)]);
+        }
+      // Y_j -= U[P_j, blk] X_kp for the pivot steps j < k0 (8-row items it = warp + 8m)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int it = warp + 8 * m;
+        if (it * 8 < k0) {
+          const int yr = it * 8 + g;
+          double acc[8][2];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double2 v = *reinterpret_cast<const double2*>(sYb + yidx(yr, 8 * j + 2 * tq));
+            acc[j][0] = v.x;
+            acc[j][1] = v.y;
+          }
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            if (4 * ks < kb) {
+              const double af = -afU[m][ks];
+              const int xr = k0 + 4 * ks + tq;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], af, sYb[yidx(xr, 8 * j + g)]);
+            }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<double2*>(sYb + yidx(yr, 8 * j + 2 * tq)) = make_double2(acc[j][0], acc[j][1]);
+        }
+      }
+      if (kp > 0) load_frags(kp - 1);  // in flight across the next block's barrier + solve
+      P3_ADD(13, t_u, tid == 0);
+    }
+    __syncthreads();
+    // T1 (+ L43e) -> smem
+    double* sT1 = sm + OFF_U12;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int col = 8 * j + 2 * tq;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = col + h;
+        sT1[(warp * 8 + g) * ST1 + cc] = cc < NB ? __ldg(cL43e + (warp * 8 + g) * NB + cc) + t1acc[j][h] : 0.0;
+      }
+    }
+    return pm;
+}
 
 __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
   using namespace l3;
@@ -153,7 +330,9 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
     // ================= blocked LU with look-ahead =================
     // panel-warp state: rows r0 = tid, r1 = tid + 128
     const int r0 = tid, r1 = tid + 128;
-    bool act0 = pwarp && r0 < NI, act1 = pwarp && r1 < NI;
+    // a row is active until it becomes a pivot row (step >= 0); derived, not stored, to save registers
+#define act0 (step0 < 0 && tid < 128)
+#define act1 (step1 < 0 && tid < NI - 128)
     int step0 = -1, step1 = -1;
     int cidx0 = -1, cidx1 = -1;  // compact index of r0 / r1 in the last active list
 
@@ -216,13 +395,13 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
           }
           double* pr = sProw + (j & 1) * 16;
           if (r0 == p) {
-            act0 = false; step0 = k0 + j;
+            step0 = k0 + j;
             if (w0[j] == 0.0) s_sing = 1;
 #pragma unroll
             for (int c = 0; c < 16; ++c) sts64(pr + c, w0[c]);
           }
           if (r1 == p) {
-            act1 = false; step1 = k0 + j;
+            step1 = k0 + j;
             if (w1[j] == 0.0) s_sing = 1;
 #pragma unroll
             for (int c = 0; c < 16; ++c) sts64(pr + c, w1[c]);
@@ -295,6 +474,8 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
       if (tid == 0) s_nact[buf] = tot;
     };
 
+#undef act0
+#undef act1
     // rank-kb update of M[act rows][c0 + [cbeg, cend)] by the update warps (uw = 0..3). Work item:
     // 8 rows x CW columns whose C loads are all issued before the DMMAs (one L2 round trip).
     // uw >= 0: static round-robin over 4 update warps; uw < 0: pull items from s_next (any warp).
@@ -405,101 +586,9 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
     }
     P3_T(t_bs);
 
-    // ================= back substitution (right-looking), fused with T1 = L43i Psi =================
-    // For block kp from the last: X_blk = U11^{-1} Y[P_kp] (one RHS column per thread, into smem),
-    // Psi rows out, T1 += L43i[:, blk] (-X_blk) (each warp: 8 rows x 64 columns in registers), then
-    // Y[P_j] -= U[P_j, blk] X_blk for all earlier pivot rows (DMMA, 8-row items, parallel loads).
-    double* sX = sA16;                 // 16 x 66 : X block (B operand, SB-like padded stride)
-    constexpr int SX = 68;             // == 4 mod 16 (conflict-free B fragments)
-    double* Psi = a.Psi + (long long)grp * NI * NB;
-    double t1acc[8][2];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) t1acc[j][0] = t1acc[j][1] = 0.0;
-    double pm = 0.0;
-    double* sY = sA16 + 16 * SX;  // 16 x SX: Y rows of the block
-    double* sU = sY + 16 * SX;    // 16 x 17: U11 of the block
-    for (int kp = NPANEL - 1; kp >= 0; --kp) {
-      const int k0 = 16 * kp, kb = min(16, NI - k0);
-      // stage Y[P_kp] (16 x 64) and U11 (16 x 16) with one round of parallel loads
-      for (int e = tid; e < 16 * (NRHS + 16); e += THREADS) {
-        const int r = e / (NRHS + 16), c = e - r * (NRHS + 16);
-        const double* Urow = M + (long long)sPiv[k0 + (r < kb ? r : 0)] * LDM;
-        if (c < NRHS) sY[r * SX + c] = r < kb ? Urow[NI + c] : 0.0;
-        else sU[r * 17 + (c - NRHS)] = (r < kb && c - NRHS < kb) ? Urow[k0 + c - NRHS] : 0.0;
-      }
-      __syncthreads();
-      if (tid < NRHS) {
-        double x[16];
-#pragma unroll
-        for (int r = 15; r >= 0; --r) {
-          if (r < kb) {
-            double v = sY[r * SX + tid];
-#pragma unroll
-            for (int b = r + 1; b < 16; ++b)
-              if (b < kb) v = fma(-sU[r * 17 + b], x[b], v);
-            x[r] = v * fast_rcp(sU[r * 17 + r]);
-          } else {
-            x[r] = 0.0;
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < 16; ++r) sts64(sX + r * SX + tid, x[r]);
-        if (tid < NB) {
-#pragma unroll
-          for (int r = 0; r < 16; ++r)
-            if (r < kb) __stcs(Psi + (long long)(k0 + r) * NB + tid, -x[r]);
-        } else if (tid == NB) {
-#pragma unroll
-          for (int r = 0; r < 16; ++r)
-            if (r < kb) pm = fmax(pm, fabs(x[r]));
-        }
-      }
-      __syncthreads();
-      {  // T1 += L43i[:, k0:k0+kb] * (-X_blk): warp rows 8w..8w+7, all 64 columns
-        const double* Arow = cL43i + (long long)(warp * 8 + g) * NI + k0;
-        for (int ks = 0; ks < kb; ks += 4) {
-          const double af = -__ldg(Arow + ks + tq);
-          const double* Xr = sX + (ks + tq) * SX + g;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) dmma_8x8x4(t1acc[j][0], t1acc[j][1], af, Xr[8 * j]);
-        }
-      }
-      // Y[P_j] -= U[P_j, k0:k0+kb] X_blk for steps j < k0 (rows sPiv[0..k0))
-      const int nrt = (k0 + 7) >> 3;
-      for (int it = warp; it < nrt; it += THREADS / 32) {
-        const int ri = it * 8 + g;
-        const bool rv = ri < k0;
-        const double* Urow = M + (long long)(rv ? sPiv[ri] : 0) * LDM;
-        double af[4];
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) af[ks] = (rv && 4 * ks < kb) ? -Urow[k0 + 4 * ks + tq] : 0.0;
-        double acc[8][2];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (rv) {
-            const double2 v = *reinterpret_cast<const double2*>(Urow + NI + 8 * j + 2 * tq);
-            acc[j][0] = v.x;
-            acc[j][1] = v.y;
-          } else {
-            acc[j][0] = acc[j][1] = 0.0;
-          }
-        }
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          if (4 * ks < kb) {
-            const double* Xr = sX + (4 * ks + tq) * SX + g;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], af[ks], Xr[8 * j]);
-          }
-        if (rv) {
-          double* Yr = const_cast<double*>(Urow) + NI;
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<double2*>(Yr + 8 * j + 2 * tq) = make_double2(acc[j][0], acc[j][1]);
-        }
-      }
-      __syncthreads();
-    }
+    // back substitution + T1 in a separate (non-inlined) function: its registers do not perturb
+    // the allocation of the factorisation loop above
+    double pm = leaf3_backsub(M, sPiv, a.Psi + (long long)grp * NI * NB, cL43i, cL43e);
     P3_ADD(8, t_bs, tid == 0);
     P3_T(t_ep);
     // probe condition estimate (leafops.py:293-294)
@@ -512,17 +601,7 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
       const double cnd = anorm * mx / a.probe_max;
       a.cond[grp] = (s_sing || !isfinite(cnd)) ? INFINITY : cnd;
     }
-    // T1 (+ L43e) -> smem, then T = T1 L1
-    double* sT1 = sU12;  // 64 x ST1
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int col = 8 * j + 2 * tq;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int cc = col + h;
-        sT1[(warp * 8 + g) * ST1 + cc] = cc < NB ? __ldg(cL43e + (warp * 8 + g) * NB + cc) + t1acc[j][h] : 0.0;
-      }
-    }
+    double* sT1 = sU12;  // 64 x ST1, written by leaf3_backsub
     __syncthreads();
     {
       const int rr0 = warp * 8;
@@ -556,7 +635,7 @@ extern "C" int hps_debug_leaf3_profile(long long* out, int reset) {
 }
 #endif
 
-size_t leaf16v3_scratch_doubles() { return (size_t)l3::MROWS * l3::LDM; }
+size_t leaf16v3_scratch_doubles() { return (size_t)l3::MROWS * l3::LDM + (size_t)l3::NPANEL * 256; }
 
 int leaf16v3_grid(int ngroups) {
   int dev = 0, sms = 148;

@@ -19,7 +19,7 @@ lib.hps_debug_leaf3_profile(buf, 0)
 a = np.frombuffer(buf, dtype=np.int64).reshape(1024, 16)[:296].astype(float)
 per = inp.ngroups / 296
 names = ["assembly", "factor(0)", "U12 (13x)", "U-warps: lookahead cols", "U-warps: total update", "P-warps: wait for lookahead",
-         "P-warps: wait+factor", "panel iteration total", "back substitution", "epilogue"]
+         "P-warps: wait+factor", "panel iteration total", "back substitution", "epilogue", "BS: Y staging", "BS: wait at block barrier", "BS: tri-solve (warp 0)", "BS: update (warp 0)"]
 print("leaf ms", [round(e0.elapsed_time(e1), 3) for n, e0, e1 in tl if n == "leaf"])
 for i, n in enumerate(names):
     print(f"  {n:30s} {a[:, i].mean() / per:12.0f} cyc/leaf")
