@@ -323,7 +323,8 @@ def main():
     # ---- end-to-end through the public API (solver.Pipeline), pinned host memory ----
     # Every step is one full problem: host sampling + grouping of the coefficients, their H2D
     # upload, the build, the H2D of the boundary data, the batched solve and the D2H of u. The
-    # pipeline overlaps the host work of step i+1 with the device work of step i.
+    # pipeline overlaps the host work of step i+1 with the device work of step i, and step i's
+    # device work with step i+1's (two compute streams).
     st = U = graph = None  # the device leg's captured state goes before the pipeline captures its own
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -348,6 +349,7 @@ def main():
         for U, st in pipe.run([(co, pin_F)]):
             st = None
         lat.append(time.perf_counter() - t1)
+    n_streams = len(pipe._mains)
     pipe.close()
     inp_b = solver.prepare(tree, nodes, co, device=dev, pinned=True)
     h2d = inp_b.h2d_bytes() + pin_F.numel() * 8
@@ -358,9 +360,10 @@ def main():
            "latency_s": float(min(lat)),
            "includes": "per step: coefficient sampling on the host, H2D of the samples (pinned), leaf grouping "
                        "on the device, build, status check, H2D of the boundary data, batched solve, D2H of u "
-                       "(N x ldu); solver.Pipeline overlaps step i+1's host work with step i's device work "
-                       "(and replays build + solve from two alternating CUDA-graph captures); "
-                       "latency_s = one problem alone"}
+                       "(N x ldu); solver.Pipeline overlaps step i+1's host work with step i's device work, "
+                       "runs consecutive problems on two alternating compute streams (step i's latency-bound "
+                       "top merges beside step i+1's leaf stage; %d stream(s) here) and replays build + solve "
+                       "from two alternating CUDA-graph captures; latency_s = one problem alone" % n_streams}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

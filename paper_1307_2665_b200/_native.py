@@ -25,7 +25,8 @@ HPS_ERR_ARG = 5
 EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_launch_count", "hps_leaf_workspace_bytes",
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
            "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched", "hps_leaf_hash",
-           "hps_leaf_verify", "hps_leaf_fields", "hps_eval_points", "hps_gauge_sides", "hps_gauge_gather")
+           "hps_leaf_verify", "hps_leaf_fields", "hps_eval_points", "hps_gauge_sides", "hps_gauge_gather",
+           "hps_set_scratch_slot")
 
 _lib = None
 
@@ -48,6 +49,8 @@ def load():
     lib.hps_last_error.restype = ctypes.c_char_p
     lib.hps_version.restype = c_int
     lib.hps_launch_count.restype = c_ll
+    lib.hps_set_scratch_slot.argtypes = [c_int]
+    lib.hps_set_scratch_slot.restype = c_int
     lib.hps_device_check.argtypes = [ctypes.POINTER(c_int)] * 3
     lib.hps_device_check.restype = c_int
     lib.hps_leaf_workspace_bytes.argtypes = [c_int, c_int]

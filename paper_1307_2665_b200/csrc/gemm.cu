@@ -24,17 +24,20 @@ __global__ void k_splitk_reduce(GemmParams p) {
   }
 }
 
-// Split-K scratch: two growing device buffers, one for the library's own side stream (the
-// interface inverse runs independent GEMMs there concurrently) and one for the caller's stream
-// (the library enqueues on one caller stream at a time). Builds repeat the same shapes, so they
-// settle after the first build. An outgrown buffer is never freed: a captured CUDA graph
-// (solver.BuildGraph) may still reference it.
+// Split-K scratch: growing device buffers, one for the library's own side stream (the interface
+// inverse runs independent GEMMs there concurrently) and one for the caller's stream, in
+// HPS_SCRATCH_SLOTS independent sets. hps_set_scratch_slot(s) selects the set for the calling host
+// thread's later enqueues, so two builds in flight on two streams (solver.Pipeline(streams=2))
+// never share one. Builds repeat the same shapes, so they settle after the first build. An
+// outgrown buffer is never freed: a captured CUDA graph (solver.BuildGraph) may still reference it.
 cudaStream_t fork_side_stream();  // merge.cu
-static double* g_splitk[2] = {nullptr, nullptr};
-static size_t g_splitk_n[2] = {0, 0};
+constexpr int HPS_SCRATCH_SLOTS = 2;
+static double* g_splitk[HPS_SCRATCH_SLOTS][2] = {};
+static size_t g_splitk_n[HPS_SCRATCH_SLOTS][2] = {};
+static thread_local int t_scratch_slot = 0;
 static double* splitk_scratch(size_t n, cudaStream_t st) {
-  const int slot = (st != nullptr && st == fork_side_stream()) ? 1 : 0;
-  if (n > g_splitk_n[slot]) {
+  const int role = (st != nullptr && st == fork_side_stream()) ? 1 : 0, set = t_scratch_slot;
+  if (n > g_splitk_n[set][role]) {
     // no allocation inside a stream capture (it would invalidate the capture): the caller then
     // runs without split-K. BuildGraph warms up first, so captures normally find it allocated.
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -44,10 +47,10 @@ static double* splitk_scratch(size_t n, cudaStream_t st) {
       cudaGetLastError();
       return nullptr;
     }
-    g_splitk[slot] = fresh;
-    g_splitk_n[slot] = n;
+    g_splitk[set][role] = fresh;
+    g_splitk_n[set][role] = n;
   }
-  return g_splitk[slot];
+  return g_splitk[set][role];
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool VEC = true>
@@ -168,6 +171,15 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
 }
 
 }  // namespace hps
+
+extern "C" int hps_set_scratch_slot(int slot) {
+  if (slot < 0 || slot >= hps::HPS_SCRATCH_SLOTS) {
+    hps::set_error("hps_set_scratch_slot: slot %d not in [0, %d)", slot, hps::HPS_SCRATCH_SLOTS);
+    return HPS_ERR_ARG;
+  }
+  hps::t_scratch_slot = slot;
+  return HPS_OK;
+}
 
 extern "C" int hps_dgemm_batched(int M, int N, int K, int batch, double alpha, const double* A, long long lda,
                                  long long strideA, const double* B, long long ldb, long long strideB,

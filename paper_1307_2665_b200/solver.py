@@ -670,14 +670,16 @@ class Pipeline:
     service answering many coefficient fields / boundary data on the same tree runs that pair in a
     loop. Here, while the device builds and solves problem i on the main stream, a host thread
     samples, uploads and groups problem i+1's coefficients (`prepare`, pinned memory, its own
-    stream), and problem i-1's u and status words come back on a third stream. Every problem
-    still makes its own H2D copies and its own D2H of u; at most two states are alive at once.
+    stream), and problem i-1's u and status words come back on a third stream. With streams=2
+    (default up to L = 8) problems alternate between two compute streams, so problem i's
+    latency-bound top merges run beside problem i+1's leaf stage. Every problem still makes its
+    own H2D copies and its own D2H of u; at most three states are alive at once.
 
     `run(jobs)` takes an iterable of (coeffs, F), F a host (|Gamma|, b) or (|Gamma|,) array in
     root.I_e order, and yields (U, state) per job in order: U is a pinned host tensor (N, ldu) whose
     columns [:b] are the solutions, state the SolverState (valid until the caller drops it)."""
 
-    def __init__(self, tree, nodeset, *, device=None, overlap_results=True, reuse_graphs=False):
+    def __init__(self, tree, nodeset, *, device=None, overlap_results=True, reuse_graphs=False, streams=None):
         torch = _torch()
         _native.require_device()
         self.overlap_results = overlap_results
@@ -694,7 +696,18 @@ class Pipeline:
         import os as _os
         prio = int(_os.environ.get("HPS_UPLOAD_PRIORITY", "1"))
         self._upload = torch.cuda.Stream(self.device, priority=-prio if prio else 0)
-        self._main = torch.cuda.Stream(self.device)
+        # streams=2: consecutive problems are built and solved on two alternating compute streams,
+        # so one problem's latency-bound top merges (interface inverses on a few CTAs) overlap the
+        # next problem's leaf stage. Each problem waits for the D2H of the problem two before it
+        # (the previous user of its graph slot / workspace).
+        # Default: two streams up to L = 8 (cfg2 e2e 15.0 -> 13.2 ms/problem, cfg3 41.5 -> 37.6 ms);
+        # one at L >= 9, where two problems' operators in flight would not fit beside each other.
+        if streams is None:
+            env = _os.environ.get("HPS_PIPE_STREAMS")
+            streams = int(env) if env else (2 if getattr(getattr(tree, "layout", tree), "L", 0) <= 8 else 1)
+        self._mains = [torch.cuda.Stream(self.device) for _ in range(max(1, min(2, int(streams))))]
+        self._main = self._mains[0]
+        self._slot_done = [None, None]
         self._d2h = torch.cuda.Stream(self.device)
         import concurrent.futures
         self._host = concurrent.futures.ThreadPoolExecutor(max_workers=1)
@@ -714,31 +727,42 @@ class Pipeline:
         fut = self._host.submit(self._prepare, job[0]) if job is not None else None
         pending = None
         while fut is not None:
+            k = self._jobs  # job counter across run() calls: stream, graph slot and scratch slot
             inp, ready = fut.result()
             nxt = next(it, None)
             F = job[1]
             fut = self._host.submit(self._prepare, nxt[0]) if nxt is not None else None
+            main = self._mains[k % len(self._mains)]
             with torch.cuda.device(self.device):
-                with torch.cuda.stream(self._main):
-                    self._main.wait_event(ready)
+                with torch.cuda.stream(main):
+                    main.wait_event(ready)
+                    if len(self._mains) > 1 and self._slot_done[k & 1] is not None:
+                        main.wait_event(self._slot_done[k & 1])
                     for t in inp.device_tensors():
-                        t.record_stream(self._main)
+                        t.record_stream(main)
                     Fh = F if torch.is_tensor(F) else torch.from_numpy(np.ascontiguousarray(np.asarray(F, dtype=float)))
                     if Fh.dim() == 1:
                         Fh = Fh[:, None]
                     if not Fh.is_pinned():
                         Fh = Fh.pin_memory()
                     Fd = Fh.to(self.device, non_blocking=True)
-                    g = self._graph_for(inp, Fd.shape[1]) if self.reuse_graphs else None
-                    if g is not None:
-                        g.load(inp, Fd)
-                        st = g.replay_build()
-                        U = g.replay_solve()
-                    else:
-                        st = build_device(inp)
-                        U = solve_device(st, Fd)
+                    multi = len(self._mains) > 1
+                    if multi:  # this job's split-K scratch set (its neighbour may still be running)
+                        _native.check(_native.load().hps_set_scratch_slot(k & 1), "hps_set_scratch_slot")
+                    try:
+                        g = self._graph_for(inp, Fd.shape[1], k & 1) if self.reuse_graphs else None
+                        if g is not None:
+                            g.load(inp, Fd)
+                            st = g.replay_build()
+                            U = g.replay_solve()
+                        else:
+                            st = build_device(inp)
+                            U = solve_device(st, Fd)
+                    finally:
+                        if multi:
+                            _native.load().hps_set_scratch_slot(0)
                     solved = torch.cuda.Event()
-                    solved.record(self._main)
+                    solved.record(main)
                 # results and status words come back on their own stream, so the next job's build
                 # is enqueued on the main stream before this job's D2H is waited for
                 with torch.cuda.stream(self._d2h):
@@ -751,6 +775,8 @@ class Pipeline:
                         outs.append(h)
                     done = torch.cuda.Event()
                     done.record(self._d2h)
+                    self._slot_done[k & 1] = done
+            self._jobs += 1
             del U
             if pending is not None:
                 yield self._finish(*pending)
@@ -763,9 +789,8 @@ class Pipeline:
         if pending is not None:
             yield self._finish(*pending)
 
-    def _graph_for(self, inp, nrhs):
-        slot = self._graphs[self._jobs & 1]
-        self._jobs += 1
+    def _graph_for(self, inp, nrhs, sidx):
+        slot = self._graphs[sidx]
         key = (inp.ngroups, tuple(t is not None for t in inp.fields_dev), tuple(inp.scalars), int(nrhs))
         g = slot.get(key)
         if g is None:
@@ -773,7 +798,7 @@ class Pipeline:
                 slot.clear()
             torch = _torch()
             try:
-                g = slot[key] = BuildGraph(inp, nrhs=nrhs)
+                g = slot[key] = BuildGraph(inp, nrhs=nrhs, scratch_slot=sidx if len(self._mains) > 1 else 0)
             except torch.OutOfMemoryError:  # two captured states do not fit: stay eager from here on
                 slot.clear()
                 self._graphs = [{}, {}]
@@ -812,9 +837,13 @@ class BuildGraph:
 
     _warmed = set()
 
-    def __init__(self, inp, nrhs=0):
+    def __init__(self, inp, nrhs=0, scratch_slot=0):
         torch = _torch()
         lib = _native.load()
+        # the library's split-K scratch set this capture bakes in (two graphs replayed at once on two
+        # streams need different slots, see Pipeline(streams=2))
+        self.scratch_slot = int(scratch_slot)
+        _native.check(lib.hps_set_scratch_slot(self.scratch_slot), "hps_set_scratch_slot")
         self.torch = torch
         self.layout, self.ngroups, self.scalars = inp.layout, inp.ngroups, tuple(inp.scalars)
         self._present = tuple(t is not None for t in inp.fields_dev)
@@ -829,7 +858,7 @@ class BuildGraph:
         pool = torch.cuda.graph_pool_handle()
         self.stages = []
         n0 = lib.hps_launch_count()
-        key = (id(inp.layout), inp.ngroups, self._present, self.scalars, self.nrhs)
+        key = (id(inp.layout), inp.ngroups, self._present, self.scalars, self.nrhs, self.scratch_slot)
         with torch.cuda.stream(side):
             if key not in BuildGraph._warmed:
                 # warm-up: lazy attributes and scratch sizes outside the capture (once per shape)
@@ -877,6 +906,8 @@ class BuildGraph:
                         pass
                 self.stages, self.state = [], None
                 raise
+            finally:
+                lib.hps_set_scratch_slot(0)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.launches = int(lib.hps_launch_count() - n0)
