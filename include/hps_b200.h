@@ -43,7 +43,7 @@ int hps_device_check(int* major, int* minor, int* sms);
 /* Kernels launched by this library so far in this process (benchmark accounting). */
 long long hps_launch_count(void);
 /* Internal scratch set (split-K partial sums) used by this host thread's later enqueues: two
- * builds in flight at once on two streams must use different slots (0 or 1; default 0). */
+ * builds in flight at once on different streams must use different slots (0..3; default 0). */
 int hps_set_scratch_slot(int slot);
 
 /* Leaf stage for `ngroups` distinct coefficient groups (leaves with bitwise-equal samples share a

@@ -31,7 +31,7 @@ __global__ void k_splitk_reduce(GemmParams p) {
 // never share one. Builds repeat the same shapes, so they settle after the first build. An
 // outgrown buffer is never freed: a captured CUDA graph (solver.BuildGraph) may still reference it.
 cudaStream_t fork_side_stream();  // merge.cu
-constexpr int HPS_SCRATCH_SLOTS = 2;
+constexpr int HPS_SCRATCH_SLOTS = 4;
 static double* g_splitk[HPS_SCRATCH_SLOTS][2] = {};
 static size_t g_splitk_n[HPS_SCRATCH_SLOTS][2] = {};
 static thread_local int t_scratch_slot = 0;

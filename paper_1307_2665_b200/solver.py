@@ -687,7 +687,7 @@ class Pipeline:
         # group count, coefficient structure and batch width; other jobs run eagerly). A yielded
         # state then lives in graph memory and is valid until the next item is requested.
         self.reuse_graphs = reuse_graphs
-        self._graphs = [{}, {}]
+        self._graphs = [{} for _ in range(4)]
         self._jobs = 0
         self.tree, self.nodeset = tree, nodeset
         self.device = torch.device(device if device is not None else "cuda")
@@ -705,9 +705,10 @@ class Pipeline:
         if streams is None:
             env = _os.environ.get("HPS_PIPE_STREAMS")
             streams = int(env) if env else (2 if getattr(getattr(tree, "layout", tree), "L", 0) <= 8 else 1)
-        self._mains = [torch.cuda.Stream(self.device) for _ in range(max(1, min(2, int(streams))))]
+        self._mains = [torch.cuda.Stream(self.device) for _ in range(max(1, min(4, int(streams))))]
+        self._nslots = max(2, len(self._mains))  # graph / scratch / workspace slots, used round robin
         self._main = self._mains[0]
-        self._slot_done = [None, None]
+        self._slot_done = [None] * 4
         self._d2h = torch.cuda.Stream(self.device)
         import concurrent.futures
         self._host = concurrent.futures.ThreadPoolExecutor(max_workers=1)
@@ -736,8 +737,9 @@ class Pipeline:
             with torch.cuda.device(self.device):
                 with torch.cuda.stream(main):
                     main.wait_event(ready)
-                    if len(self._mains) > 1 and self._slot_done[k & 1] is not None:
-                        main.wait_event(self._slot_done[k & 1])
+                    sl = k % self._nslots
+                    if len(self._mains) > 1 and self._slot_done[sl] is not None:
+                        main.wait_event(self._slot_done[sl])
                     for t in inp.device_tensors():
                         t.record_stream(main)
                     Fh = F if torch.is_tensor(F) else torch.from_numpy(np.ascontiguousarray(np.asarray(F, dtype=float)))
@@ -748,9 +750,9 @@ class Pipeline:
                     Fd = Fh.to(self.device, non_blocking=True)
                     multi = len(self._mains) > 1
                     if multi:  # this job's split-K scratch set (its neighbour may still be running)
-                        _native.check(_native.load().hps_set_scratch_slot(k & 1), "hps_set_scratch_slot")
+                        _native.check(_native.load().hps_set_scratch_slot(sl), "hps_set_scratch_slot")
                     try:
-                        g = self._graph_for(inp, Fd.shape[1], k & 1) if self.reuse_graphs else None
+                        g = self._graph_for(inp, Fd.shape[1], sl) if self.reuse_graphs else None
                         if g is not None:
                             g.load(inp, Fd)
                             st = g.replay_build()
@@ -775,7 +777,7 @@ class Pipeline:
                         outs.append(h)
                     done = torch.cuda.Event()
                     done.record(self._d2h)
-                    self._slot_done[k & 1] = done
+                    self._slot_done[sl] = done
             self._jobs += 1
             del U
             if pending is not None:
@@ -801,7 +803,7 @@ class Pipeline:
                 g = slot[key] = BuildGraph(inp, nrhs=nrhs, scratch_slot=sidx if len(self._mains) > 1 else 0)
             except torch.OutOfMemoryError:  # two captured states do not fit: stay eager from here on
                 slot.clear()
-                self._graphs = [{}, {}]
+                self._graphs = [{} for _ in range(4)]
                 self.reuse_graphs = False
                 torch.cuda.empty_cache()
                 return None

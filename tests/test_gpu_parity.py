@@ -309,8 +309,8 @@ def test_pipeline_matches_sequential_build_and_solve():
     tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), 4, 16)
     pts = nodes.points[tree.root.I_e]
     jobs = [(problems.coefficients(cfg), problems.boundary_data(2, pts, seed=cfg, batch=3)) for cfg in (2, 4, 3, 2)]
-    # streams=2: consecutive jobs on two compute streams, split-K scratch in separate slots
-    for graphs, streams in ((False, 1), (True, 1), (False, 2), (True, 2)):
+    # streams>1: consecutive jobs on alternating compute streams, split-K scratch in separate slots
+    for graphs, streams in ((False, 1), (True, 1), (False, 2), (True, 2), (True, 3)):
         pipe = solver.Pipeline(tree, nodes, reuse_graphs=graphs, streams=streams)
         got = [(U[:, :3].numpy().copy(), st.n_leaf_groups) for U, st in pipe.run(jobs)]
         got += [(U[:, :3].numpy().copy(), st.n_leaf_groups) for U, st in pipe.run(jobs)]  # counters carry over
