@@ -163,6 +163,10 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
   // latency-bound on the index-then-row loads) measured 7-12 us per depth faster on the LDS.64
   // 64 x 64 kernel below; at b = 256 the paired kernel wins (cfg5 solve 97.8 vs 104.3 ms).
   static const int v64 = getenv("HPS_GEMM64") ? atoi(getenv("HPS_GEMM64")) : 1;
+  // K <= 32 (the bottom merge depths: K = n3 = 16 or 32, one or two k tiles): two stages are enough
+  // and the smaller footprint fits 4 CTAs per SM, more tiles in flight for these memory-bound shapes
+  static const int smallk = getenv("HPS_SMALLK") ? atoi(getenv("HPS_SMALLK")) : 1;
+  if (v64 && !(p.Bidx && p.N <= 64) && smallk && p.K <= 32) return launch_cfg64<16, 2, 4>(p, stream);
   if (v64 && !(p.Bidx && p.N <= 64)) return launch_cfg64<16, 3, 3>(p, stream);
   double tiles128 = double((p.M + 127) / 128) * double((p.N + 127) / 128) * p.batch;
   // HPS_GEMM64=0: the previous tiling (128 x 128 x 16, 8 warps of 64 x 32, one CTA per SM)
