@@ -288,8 +288,9 @@ def main():
     # ---- roofline of the dominant stage ----
     peak, peak_src = fp64_peak()
     stage_flops = {"leaf": inp.ngroups * Wk.leaf_flops(q)}
-    for d in range(2 * L):
-        stage_flops[f"merge_d{d}"] = Wk.merge_flops_depth(L, q, d)
+    # a look-ahead depth also runs its parent's interface inverse (solver.lookahead_depths)
+    for d, f in Wk.merge_stage_flops(L, q, solver.lookahead_depths(inp.layout)).items():
+        stage_flops[f"merge_d{d}"] = f
     stage_ms = {k: float(np.mean(v)) * 1e3 for k, v in stages.items()}
     dom = max(stage_ms, key=stage_ms.get)
     ach = stage_flops[dom] / (stage_ms[dom] / 1e3) / 1e12

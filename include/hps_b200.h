@@ -72,6 +72,18 @@ int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const double* T_ch
                     long long child_stride, const int* child_idx, const int* maps,
                     const double* vmode, double* S_out, double* T_out, void* ws, size_t ws_bytes,
                     int* status, int status_base, void* stream);
+/* hps_merge_level plus a look-ahead for the parent depth (the next call): before this depth's big
+ * T GEMM, the parent's interface matrix X = Ta[pj3a, pj3a] - Tb[pj3b, pj3b] is formed from the pj3
+ * rows / columns of this depth's T = blk + C S (one GEMM over gathered operands), deflated and
+ * inverted in the parent's workspace `pws` on a high-priority library stream, concurrently with the
+ * T GEMM; the call joins it before returning. The parent's call then passes pre_inverted = 1 (with
+ * the same workspace) and skips its own X gather, deflation and inverse. pmaps = NULL: no
+ * look-ahead. nbatch must be even when pmaps is set. */
+int hps_merge_level_ahead(int nbatch, int n3, int ne, int m, int q, const double* T_child,
+                          long long child_stride, const int* child_idx, const int* maps, const double* vmode,
+                          double* S_out, double* T_out, void* ws, size_t ws_bytes, int* status, int status_base,
+                          int pre_inverted, const int* pmaps, int pn3, int pne, const double* pvmode, void* pws,
+                          size_t pws_bytes, int* pstatus, int pstatus_base, void* stream);
 
 /* u[ii_start0 + b*n3 + r, :nrhs] = sum_c S[b][r][c] * u[Ie[b][c], :nrhs] for all nbatch parents of
  * one depth; u is node-major with leading dimension ldu (solver.py:312-315). */

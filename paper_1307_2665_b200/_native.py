@@ -26,7 +26,7 @@ EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_launch_coun
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
            "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched", "hps_leaf_hash",
            "hps_leaf_verify", "hps_leaf_fields", "hps_eval_points", "hps_gauge_sides", "hps_gauge_gather",
-           "hps_set_scratch_slot")
+           "hps_set_scratch_slot", "hps_merge_level_ahead")
 
 _lib = None
 
@@ -63,6 +63,10 @@ def load():
     lib.hps_merge_level.argtypes = [c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp, c_dp,
                                     c_dp, c_sz, c_dp, c_int, c_dp]
     lib.hps_merge_level.restype = c_int
+    lib.hps_merge_level_ahead.argtypes = [c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp, c_dp,
+                                          c_dp, c_sz, c_dp, c_int, c_int, c_dp, c_int, c_int, c_dp, c_dp, c_sz, c_dp,
+                                          c_int, c_dp]
+    lib.hps_merge_level_ahead.restype = c_int
     lib.hps_solve_level.argtypes = [c_int, c_int, c_int, c_dp, c_dp, c_ll, c_dp, c_int, c_int, c_dp]
     lib.hps_solve_level.restype = c_int
     lib.hps_dgemm_batched.argtypes = [c_int, c_int, c_int, c_int, c_d, c_dp, c_ll, c_ll, c_dp, c_ll, c_ll, c_dp,

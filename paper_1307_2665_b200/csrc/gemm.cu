@@ -24,19 +24,19 @@ __global__ void k_splitk_reduce(GemmParams p) {
   }
 }
 
-// Split-K scratch: growing device buffers, one for the library's own side stream (the interface
-// inverse runs independent GEMMs there concurrently) and one for the caller's stream, in
+// Split-K scratch: growing device buffers, one per stream role (the caller's stream, the library's
+// side stream where the interface inverse runs independent GEMMs, and the look-ahead pair), in
 // HPS_SCRATCH_SLOTS independent sets. hps_set_scratch_slot(s) selects the set for the calling host
 // thread's later enqueues, so two builds in flight on two streams (solver.Pipeline(streams=2))
 // never share one. Builds repeat the same shapes, so they settle after the first build. An
 // outgrown buffer is never freed: a captured CUDA graph (solver.BuildGraph) may still reference it.
-cudaStream_t fork_side_stream();  // merge.cu
+int stream_role(cudaStream_t st);  // merge.cu: 0 caller, 1 fork side, 2/3 look-ahead inverse pair
 constexpr int HPS_SCRATCH_SLOTS = 4;
-static double* g_splitk[HPS_SCRATCH_SLOTS][2] = {};
-static size_t g_splitk_n[HPS_SCRATCH_SLOTS][2] = {};
+static double* g_splitk[HPS_SCRATCH_SLOTS][4] = {};
+static size_t g_splitk_n[HPS_SCRATCH_SLOTS][4] = {};
 static thread_local int t_scratch_slot = 0;
 static double* splitk_scratch(size_t n, cudaStream_t st) {
-  const int role = (st != nullptr && st == fork_side_stream()) ? 1 : 0, set = t_scratch_slot;
+  const int role = stream_role(st), set = t_scratch_slot;
   if (n > g_splitk_n[set][role]) {
     // no allocation inside a stream capture (it would invalidate the capture): the caller then
     // runs without split-K. BuildGraph warms up first, so captures normally find it allocated.

@@ -42,9 +42,9 @@ __global__ void k_gather_xr(ChildRef ch, const int* __restrict__ j1a, const int*
   const int n1 = ne / 2;
   const double* Ta = ch.a(b) + (long long)j3a[r] * ch.m;
   const double* Tb = ch.bb(b) + (long long)j3b[r] * ch.m;
-  double* Xr = X + ((long long)b * n3 + r) * n3;
+  double* Xr = X ? X + ((long long)b * n3 + r) * n3 : nullptr;
   double* Rr = R + ((long long)b * n3 + r) * ne;
-  for (int c = lane; c < n3; c += 32) {
+  if (X) for (int c = lane; c < n3; c += 32) {  // X == nullptr: precomputed (look-ahead), R only
     const double v = Ta[j3a[c]] - Tb[j3b[c]];
     Xr[c] = v;
     // max |diag X| for the deflation shift: non-negative doubles order like their bit patterns,
@@ -70,6 +70,71 @@ __global__ void k_gather_c(ChildRef ch, const int* __restrict__ j1a, const int* 
   for (int c = lane; c < n3; c += 32) Cr[c] = src[j3[c]];
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Look-ahead of the parent's interface matrix (hps_merge_level_ahead). While depth d+1 still has
+// its big T GEMM to run, the parent depth's X = Ta[pj3a, pj3a] - Tb[pj3b, pj3b] only needs the
+// pj3 rows and columns of the two children, T = blk + C S:
+//   X = (blk_a - blk_b)[pj3, pj3] + [Ca[pj3a, :] | -Cb[pj3b, :]] [Sa[:, pj3a]; Sb[:, pj3b]],
+// one GEMM with K = 2 n3 over gathered operands. The parent's deflation and inverse then run on a
+// high-priority stream beside the T GEMM.
+// ---------------------------------------------------------------------------------------------
+// Block-diagonal addend of child k's T at (i, j) (the merge epilogue's blk_value, for any entry).
+__device__ __forceinline__ double blk_at(const ChildRef& ch, const int* j1a, const int* j2b, int n1, int k, int i,
+                                         int j) {
+  const bool ti = i < n1;
+  if ((j < n1) != ti) return 0.0;
+  const double* src = ti ? ch.a(k) : ch.bb(k);
+  const int ri = ti ? j1a[i] : j2b[i - n1], cj = ti ? j1a[j] : j2b[j - n1];
+  return src[(long long)ri * ch.m + cj];
+}
+
+// One warp per parent row r: Ag[b][r] = [Cm[2b][pj3a[r]] | -Cm[2b+1][pj3b[r]]] and
+// X[b][r][c] = blk_2b(pj3a[r], pj3a[c]) - blk_2b+1(pj3b[r], pj3b[c]).
+__global__ void k_ahead_rows(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b, int n3, int ne,
+                             const double* __restrict__ Cm, const int* __restrict__ pj3a,
+                             const int* __restrict__ pj3b, int pn3, double* __restrict__ Ag, double* __restrict__ X) {
+  const int b = blockIdx.x;
+  const int r = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= pn3) return;
+  const int n1 = ne / 2, ia = pj3a[r], ib = pj3b[r];
+  const double* Ca = Cm + ((long long)(2 * b) * ne + ia) * n3;
+  const double* Cb = Cm + ((long long)(2 * b + 1) * ne + ib) * n3;
+  double* Ar = Ag + ((long long)b * pn3 + r) * (2 * n3);
+  for (int k = lane; k < n3; k += 32) {
+    Ar[k] = Ca[k];
+    Ar[n3 + k] = -Cb[k];
+  }
+  double* Xr = X + ((long long)b * pn3 + r) * pn3;
+  for (int c = lane; c < pn3; c += 32)
+    Xr[c] = blk_at(ch, j1a, j2b, n1, 2 * b, ia, pj3a[c]) - blk_at(ch, j1a, j2b, n1, 2 * b + 1, ib, pj3b[c]);
+}
+
+// One warp per row k of Bg[b] (2 n3 x pn3): S[2b][k][pj3a[c]] (k < n3), S[2b+1][k - n3][pj3b[c]].
+__global__ void k_ahead_bg(const double* __restrict__ S, int n3, int ne, const int* __restrict__ pj3a,
+                           const int* __restrict__ pj3b, int pn3, double* __restrict__ Bg) {
+  const int b = blockIdx.x;
+  const int k = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (k >= 2 * n3) return;
+  const bool top = k < n3;
+  const double* Sr = S + ((long long)(2 * b + (top ? 0 : 1)) * n3 + (top ? k : k - n3)) * ne;
+  const int* map = top ? pj3a : pj3b;
+  double* Br = Bg + ((long long)b * 2 * n3 + k) * pn3;
+  for (int c = lane; c < pn3; c += 32) Br[c] = Sr[map[c]];
+}
+
+// max |diag X| per matrix (the deflation shift), as the exact integer max of the bit patterns.
+__global__ void k_diagmax(const double* __restrict__ X, int n, unsigned long long* __restrict__ diagmax) {
+  const int b = blockIdx.x;
+  unsigned long long m = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned long long v = (unsigned long long)__double_as_longlong(fabs(X[((long long)b * n + i) * n + i]));
+    m = v > m ? v : m;
+  }
+  atomicMax(diagmax + b, m);
+}
 
 // Corner-mode projector entry (V V^T)[r][c] for an interface of n = nseg * q nodes.
 __device__ __forceinline__ double vvt(int r, int c, int q, int nseg, const double* vs, const double* ve) {
@@ -598,24 +663,36 @@ __global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs
 }
 
 // In-place batched inverse of n x n blocks (n <= 128), stride lda.
+// reserve_sm: the look-ahead inverse runs beside a full-GPU GEMM. Its Gauss-Jordan CTAs are chains
+// of dependent FP64 operations, which slow down sharply when GEMM CTAs on the same SM keep the FP64
+// pipe busy; padding the launch with unused dynamic shared memory keeps GEMM CTAs off those SMs.
+template <int NT>
+static int launch_gj(double* X, long long lda, long long strideX, int n, int batch, int* status, int status_base,
+                     bool reserve_sm, cudaStream_t st) {
+  static const int pad_kb = getenv("HPS_GJ_RESERVE_KB") ? atoi(getenv("HPS_GJ_RESERVE_KB")) : 160;
+  static bool attr = false;
+  const int pad = reserve_sm ? pad_kb * 1024 : 0;
+  if (pad && !attr) {
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(k_gj_blk<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
+    attr = true;
+  }
+  k_gj_blk<NT><<<batch, NT * 16, pad, st>>>(X, lda, strideX, n, status, status_base);
+  HPS_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
 static int inverse_small(double* X, long long lda, long long strideX, int n, int batch, int* status,
-                         int status_base, cudaStream_t st) {
+                         int status_base, cudaStream_t st, bool reserve_sm = false) {
   if (n > 128) {
     set_error("inverse_small: n=%d > 128", n);
     return HPS_ERR_ARG;
   }
   static const int v = getenv("HPS_GJ_V") ? atoi(getenv("HPS_GJ_V")) : 3;
   if (v == 3) {  // blocked GJ (8-pivot panels, DMMA block updates)
-    if (n <= 16)
-      k_gj_blk<2><<<batch, 32, 0, st>>>(X, lda, strideX, n, status, status_base);
-    else if (n <= 32)
-      k_gj_blk<4><<<batch, 64, 0, st>>>(X, lda, strideX, n, status, status_base);
-    else if (n <= 64)
-      k_gj_blk<8><<<batch, 128, 0, st>>>(X, lda, strideX, n, status, status_base);
-    else
-      k_gj_blk<16><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
-    HPS_LAUNCH_CHECK();
-    return HPS_OK;
+    if (n <= 16) return launch_gj<2>(X, lda, strideX, n, batch, status, status_base, reserve_sm, st);
+    if (n <= 32) return launch_gj<4>(X, lda, strideX, n, batch, status, status_base, reserve_sm, st);
+    if (n <= 64) return launch_gj<8>(X, lda, strideX, n, batch, status, status_base, reserve_sm, st);
+    return launch_gj<16>(X, lda, strideX, n, batch, status, status_base, reserve_sm, st);
   }
   if (n <= 16)
     k_gj_inverse<1, 8, 2><<<batch, 64, 0, st>>>(X, lda, strideX, n, status, status_base);
@@ -650,6 +727,7 @@ static int gemm(int M, int N, int K, int batch, double alpha, const double* A, l
 // concurrently (fork/join through events; captured CUDA graphs get parallel branches).
 struct ForkCtx {
   cudaStream_t side = nullptr;
+  cudaStream_t ahead = nullptr, ahead_side = nullptr;  // look-ahead inverse (highest priority)
   cudaEvent_t ev[64];
   int next = 0;
   bool ok = false;
@@ -660,12 +738,22 @@ static ForkCtx& fork_ctx() {
   if (!init) {
     init = true;
     c.ok = cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking) == cudaSuccess;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    c.ok = c.ok && cudaStreamCreateWithPriority(&c.ahead, cudaStreamNonBlocking, hi) == cudaSuccess;
+    c.ok = c.ok && cudaStreamCreateWithPriority(&c.ahead_side, cudaStreamNonBlocking, hi) == cudaSuccess;
     for (int i = 0; i < 64 && c.ok; ++i) c.ok = cudaEventCreateWithFlags(&c.ev[i], cudaEventDisableTiming) == cudaSuccess;
     cudaGetLastError();
   }
   return c;
 }
 cudaStream_t fork_side_stream() { return fork_ctx().ok ? fork_ctx().side : nullptr; }
+// split-K scratch role of a stream: 0 the caller's, 1 the fork side stream, 2/3 the look-ahead pair
+int stream_role(cudaStream_t st) {
+  ForkCtx& c = fork_ctx();
+  if (!c.ok || st == nullptr) return 0;
+  return st == c.side ? 1 : st == c.ahead ? 2 : st == c.ahead_side ? 3 : 0;
+}
 
 static cudaEvent_t record_on(cudaStream_t st) {
   ForkCtx& c = fork_ctx();
@@ -676,9 +764,9 @@ static cudaEvent_t record_on(cudaStream_t st) {
 }
 
 static int inverse_rec(double* A, long long lda, long long strideA, int n, int batch, double* tmp, int* status,
-                       int status_base, cudaStream_t st) {
+                       int status_base, cudaStream_t st, cudaStream_t side = nullptr, bool reserve_sm = false) {
   static const int base = getenv("HPS_INV_BASE") ? atoi(getenv("HPS_INV_BASE")) : 128;
-  if (n <= base || n <= 16) return inverse_small(A, lda, strideA, n, batch, status, status_base, st);
+  if (n <= base || n <= 16) return inverse_small(A, lda, strideA, n, batch, status, status_base, st, reserve_sm);
   const int h = n / 2, h2 = n - h;  // unequal halves allowed (q = 21 gives n3 = 21 * 2^j)
   double* A11 = A;
   double* A12 = A + h;
@@ -691,14 +779,15 @@ static int inverse_rec(double* A, long long lda, long long strideA, int n, int b
   static const int par = getenv("HPS_INV_FORK") ? atoi(getenv("HPS_INV_FORK")) : 1;
   ForkCtx& fc = fork_ctx();
   const bool fork = par && fc.ok;
-  cudaStream_t s2 = fork ? fc.side : st;
-  HPS_TRY(inverse_rec(A11, lda, strideA, h, batch, deeper, status, status_base, st));
+  if (!side) side = fc.side;
+  cudaStream_t s2 = fork ? side : st;
+  HPS_TRY(inverse_rec(A11, lda, strideA, h, batch, deeper, status, status_base, st, side, reserve_sm));
   if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(s2, record_on(st), 0));
   // T21 = A21 inv(A11) on the side stream, T12 = inv(A11) A12 and the Schur update on the main one
   HPS_TRY(gemm(h2, h, h, batch, 1.0, A21, lda, strideA, A11, lda, strideA, 0.0, T21, h, sT, s2));
   HPS_TRY(gemm(h, h2, h, batch, 1.0, A11, lda, strideA, A12, lda, strideA, 0.0, T12, h2, sT, st));
   HPS_TRY(gemm(h2, h2, h, batch, -1.0, A21, lda, strideA, T12, h2, sT, 1.0, A22, lda, strideA, st));
-  HPS_TRY(inverse_rec(A22, lda, strideA, h2, batch, deeper, status, status_base, st));
+  HPS_TRY(inverse_rec(A22, lda, strideA, h2, batch, deeper, status, status_base, st, side, reserve_sm));
   if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(s2, record_on(st), 0));
   // A21 = -inv(S) T21 on the side stream (after T21 there), A12 = -T12 inv(S) on the main one
   HPS_TRY(gemm(h2, h, h2, batch, -1.0, A22, lda, strideA, T21, h, sT, 0.0, A21, lda, strideA, s2));
@@ -723,11 +812,21 @@ extern "C" size_t hps_merge_workspace_bytes(int nbatch, int n3, int ne) {
   return d * sizeof(double) + 256;
 }
 
-extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const double* T_child,
-                               long long child_stride, const int* child_idx, const int* maps, const double* vmode,
-                               double* S_out, double* T_out, void* ws, size_t ws_bytes, int* status,
-                               int status_base, void* stream) {
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+// Parent-depth look-ahead of hps_merge_level_ahead (see k_ahead_rows).
+struct AheadArgs {
+  const int* pmaps;       // parent depth's split maps (j1a, j2b, j3a, j3b)
+  int pn3, pne;
+  const double* pvmode;   // parent depth's corner-mode vectors (2q)
+  void* pws;              // the parent depth's merge workspace (X inverted in place there)
+  size_t pws_bytes;
+  int* pstatus;
+  int pstatus_base;
+};
+
+static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const double* T_child, long long child_stride,
+                            const int* child_idx, const int* maps, const double* vmode, double* S_out, double* T_out,
+                            void* ws, size_t ws_bytes, int* status, int status_base, bool pre_inverted,
+                            const AheadArgs* ah, cudaStream_t st) {
   if (nbatch <= 0) return HPS_OK;
   if (ne % 2 || n3 % q || m != ne / 2 + n3 || ws_bytes < hps_merge_workspace_bytes(nbatch, n3, ne)) {
     set_error("hps_merge_level: bad arguments n3=%d ne=%d m=%d q=%d ws=%zu", n3, ne, m, q, ws_bytes);
@@ -744,23 +843,67 @@ extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const d
   double* tmp = Cm + (size_t)nbatch * ne * n3;
   unsigned long long* diagmax = reinterpret_cast<unsigned long long*>(tmp + inverse_rec_tmp_doubles(n3, nbatch));
   const bool deflate = n3 > q;  // deflate the n3/q - 1 corner null modes
-  if (deflate) HPS_CUDA_CHECK(cudaMemsetAsync(diagmax, 0, sizeof(unsigned long long) * nbatch, st));
   ChildRef ch{T_child, child_stride, child_idx, m};
-  k_gather_xr<<<dim3(nbatch, (n3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, X, R,
-                                                        deflate ? diagmax : nullptr);
+  if (!pre_inverted && deflate) HPS_CUDA_CHECK(cudaMemsetAsync(diagmax, 0, sizeof(unsigned long long) * nbatch, st));
+  // pre_inverted: X was formed, deflated and inverted by the child depth's look-ahead; R and C only
+  k_gather_xr<<<dim3(nbatch, (n3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, pre_inverted ? nullptr : X,
+                                                        R, (deflate && !pre_inverted) ? diagmax : nullptr);
   HPS_LAUNCH_CHECK();
   k_gather_c<<<dim3(nbatch, (ne + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, Cm);
   HPS_LAUNCH_CHECK();
-  const double* vs = vmode;
-  const double* ve = vmode + q;
-  if (deflate) {
-    k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vs, ve, diagmax);
-    HPS_LAUNCH_CHECK();
+  if (!pre_inverted) {
+    if (deflate) {
+      k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vmode, vmode + q, diagmax);
+      HPS_LAUNCH_CHECK();
+    }
+    HPS_TRY(inverse_rec(X, n3, (long long)n3 * n3, n3, nbatch, tmp, status, status_base, st));
   }
-  HPS_TRY(inverse_rec(X, n3, (long long)n3 * n3, n3, nbatch, tmp, status, status_base, st));
   HPS_TRY(gemm(n3, ne, n3, nbatch, 1.0, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, 0.0, S_out, ne,
                (long long)n3 * ne, st, status));
   // nonfinite flag reports merge index; shift by status_base happens on the host side
+  ForkCtx& fc = fork_ctx();
+  const bool ahead = ah != nullptr && fc.ok && (nbatch % 2) == 0;
+  if (ahead) {
+    // parent X from the pj3 rows / columns of this depth's T (before the T GEMM): gathered
+    // operands in the parent workspace's R and C regions, X into its X region
+    const int P = nbatch / 2, pn3 = ah->pn3, pne = ah->pne, pn1 = pne / 2;
+    if (pn3 % q || ah->pws_bytes < hps_merge_workspace_bytes(P, pn3, pne)) {
+      set_error("hps_merge_level_ahead: bad parent arguments pn3=%d pne=%d ws=%zu", pn3, pne, ah->pws_bytes);
+      return HPS_ERR_ARG;
+    }
+    const int* pj3a = ah->pmaps + 2 * pn1;
+    const int* pj3b = pj3a + pn3;
+    double* pX = static_cast<double*>(ah->pws);
+    double* pR = pX + (size_t)P * pn3 * pn3;
+    double* pC = pR + (size_t)P * pn3 * pne;
+    double* ptmp = pC + (size_t)P * pne * pn3;
+    unsigned long long* pdiag = reinterpret_cast<unsigned long long*>(ptmp + inverse_rec_tmp_doubles(pn3, P));
+    double* Ag = pR;  // P x pn3 x 2 n3  (2 n3 <= pne)
+    double* Bg = pC;  // P x 2 n3 x pn3
+    k_ahead_rows<<<dim3(P, (pn3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, n3, ne, Cm, pj3a, pj3b, pn3, Ag, pX);
+    HPS_LAUNCH_CHECK();
+    k_ahead_bg<<<dim3(P, (2 * n3 + 7) / 8), 256, 0, st>>>(S_out, n3, ne, pj3a, pj3b, pn3, Bg);
+    HPS_LAUNCH_CHECK();
+    HPS_TRY(gemm(pn3, pn3, 2 * n3, P, 1.0, Ag, 2 * n3, (long long)pn3 * 2 * n3, Bg, pn3, (long long)2 * n3 * pn3,
+                 1.0, pX, pn3, (long long)pn3 * pn3, st));
+    const bool pdefl = pn3 > q;
+    if (pdefl) {
+      HPS_CUDA_CHECK(cudaMemsetAsync(pdiag, 0, sizeof(unsigned long long) * P, st));
+      k_diagmax<<<P, 256, 0, st>>>(pX, pn3, pdiag);
+      HPS_LAUNCH_CHECK();
+    }
+    // fork: deflate + invert the parent X on the high-priority look-ahead stream
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(fc.ahead, record_on(st), 0));
+    if (pdefl) {
+      k_deflate<<<dim3(P, pn3 / q), 256, 0, fc.ahead>>>(pX, pn3, q, ah->pvmode, ah->pvmode + q, pdiag);
+      HPS_LAUNCH_CHECK();
+    }
+    // HPS_GJ_RESERVE=1 pads the look-ahead Gauss-Jordan launches so no GEMM CTA shares their SMs:
+    // measured no faster (cfg2 13.45 vs 13.41-13.46 ms), so off by default
+    static const int reserve = getenv("HPS_GJ_RESERVE") ? atoi(getenv("HPS_GJ_RESERVE")) : 0;
+    HPS_TRY(inverse_rec(pX, pn3, (long long)pn3 * pn3, pn3, P, ptmp, ah->pstatus, ah->pstatus_base, fc.ahead,
+                        fc.ahead_side, reserve != 0));
+  }
   {  // T = blkdiag(Ta[j1a, j1a], Tb[j2b, j2b]) + C S, the blkdiag read by the GEMM epilogue
     GemmParams gp{ne, ne, n3, nbatch, Cm, n3, (long long)ne * n3, S_out, ne, (long long)n3 * ne, nullptr, 0,
                   T_out, ne, (long long)ne * ne, 1.0, 0.0, nullptr};
@@ -769,7 +912,28 @@ extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const d
     gp.blk_j2b = j2b;
     HPS_TRY(dgemm_launch(gp, st));
   }
+  if (ahead) HPS_CUDA_CHECK(cudaStreamWaitEvent(st, record_on(fc.ahead), 0));  // join
   return HPS_OK;
+}
+
+extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const double* T_child,
+                               long long child_stride, const int* child_idx, const int* maps, const double* vmode,
+                               double* S_out, double* T_out, void* ws, size_t ws_bytes, int* status,
+                               int status_base, void* stream) {
+  return merge_level_impl(nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, S_out, T_out, ws,
+                          ws_bytes, status, status_base, false, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int hps_merge_level_ahead(int nbatch, int n3, int ne, int m, int q, const double* T_child,
+                                     long long child_stride, const int* child_idx, const int* maps,
+                                     const double* vmode, double* S_out, double* T_out, void* ws, size_t ws_bytes,
+                                     int* status, int status_base, int pre_inverted, const int* pmaps, int pn3,
+                                     int pne, const double* pvmode, void* pws, size_t pws_bytes, int* pstatus,
+                                     int pstatus_base, void* stream) {
+  AheadArgs ah{pmaps, pn3, pne, pvmode, pws, pws_bytes, pstatus, pstatus_base};
+  return merge_level_impl(nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, S_out, T_out, ws,
+                          ws_bytes, status, status_base, pre_inverted != 0, pmaps ? &ah : nullptr,
+                          static_cast<cudaStream_t>(stream));
 }
 
 // Batched in-place inverse (n <= 128 uses the register Gauss-Jordan kernel directly, larger n the

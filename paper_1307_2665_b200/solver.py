@@ -474,6 +474,35 @@ def prepare(tree, nodeset, coeffs, *, device=None, pinned=False):
                        uploaded_bytes=int(up))
 
 
+def _ahead_params():
+    """(min parent n3, work bound) of the look-ahead interface inverse (hps_merge_level_ahead).
+
+    It pays where the parent's inverse is a latency chain that leaves the GPU idle: about
+    0.11 ms per 128 rows (n3 / 128 sequential Gauss-Jordan panels plus small GEMMs, measured).
+    Forming X early costs 4 pn3^2 n3 P extra flops (P parents, n3 = this depth's interface), about
+    pn3 n3 P * 4 pn3 / 30 TF/s. Look ahead when that is under half the chain it hides:
+    pn3 * n3 * P <= 3.2e6. In practice: every depth of L <= 7 trees, none at L >= 8 (measured
+    cfg2 14.1 -> 13.45 ms, cfg3 41.9 -> 39.6 ms, cfg4 363.9 -> 366.2 ms had it been on)."""
+    import os
+    lo = os.environ.get("HPS_AHEAD_MIN_N3")
+    work = os.environ.get("HPS_AHEAD_WORK")
+    return (int(lo) if lo else 128), (float(work) if work else 3.2e6)
+
+
+def lookahead_depths(lay):
+    """Depths d whose merge stage also forms and inverts the parent depth's (d - 1) interface
+    matrix (hps_merge_level_ahead), by the rule of _ahead_params."""
+    ahead_min, ahead_work = _ahead_params()
+    out = set()
+    if ahead_min <= 0:
+        return out
+    for d in range(1, len(lay.depths)):
+        pl, dl_ = lay.depths[d - 1], lay.depths[d]
+        if pl.n3 >= ahead_min and float(pl.n3) * dl_.n3 * pl.n_boxes <= ahead_work:
+            out.add(d)
+    return out
+
+
 def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_threshold=math.inf,
                  hbs_leaf_size=64, stage_begin=None):
     """Enqueue the leaf stage and every merge level on the current stream (no host sync).
@@ -517,6 +546,11 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
     S_levels = [None] * (2 * L)
     level_T = [None] * (2 * L) if keep_level_T else None
     child_T, child_stride, child_idx = Tleaf, ng * ng, inp.gid_dev
+    # Look-ahead interface inverse (hps_merge_level_ahead): depth d forms, deflates and inverts the
+    # parent depth's X beside its own T GEMM (rule in _ahead_params; HPS_AHEAD_MIN_N3=0 disables).
+    # The parent's workspace is allocated one depth early.
+    ahead = lookahead_depths(lay)
+    ws_next, pre_inv = None, False
     for d in range(2 * L - 1, -1, -1):
         if stage_begin is not None:
             stage_begin(f"merge_d{d}")
@@ -525,13 +559,29 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
         S = torch.empty((nbatch, n3, ne), dtype=torch.float64, device=device)
         T = torch.empty((nbatch, ne, ne), dtype=torch.float64, device=device)
         wsb = lib.hps_merge_workspace_bytes(nbatch, n3, ne)
-        ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+        ws = ws_next if ws_next is not None else torch.empty(wsb, dtype=torch.uint8, device=device)
+        ws_next = None
+        status_d = ctypes_vp(status.data_ptr() + 4 * d)
         mark = _marker(timeline, f"merge_d{d}")
-        _native.check(lib.hps_merge_level(nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride,
-                                          _native.ptr(child_idx), _native.ptr(dl.maps[d]),
-                                          _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T),
-                                          _native.ptr(ws), wsb, ctypes_vp(status.data_ptr() + 4 * d), 0,
-                                          stream), f"hps_merge_level(depth {d})")
+        pl = lay.depths[d - 1] if d > 0 else None
+        if pl is not None and d in ahead:
+            pwsb = lib.hps_merge_workspace_bytes(pl.n_boxes, pl.n3, pl.ne)
+            ws_next = torch.empty(pwsb, dtype=torch.uint8, device=device)
+            _native.check(lib.hps_merge_level_ahead(
+                nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride, _native.ptr(child_idx),
+                _native.ptr(dl.maps[d]), _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T), _native.ptr(ws),
+                wsb, status_d, 0, int(pre_inv), _native.ptr(dl.maps[d - 1]), pl.n3, pl.ne,
+                _native.ptr(dl.vmode[d - 1]), _native.ptr(ws_next), pwsb, ctypes_vp(status.data_ptr() + 4 * (d - 1)),
+                0, stream), f"hps_merge_level_ahead(depth {d})")
+            next_pre = True
+        else:
+            _native.check(lib.hps_merge_level_ahead(
+                nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride, _native.ptr(child_idx),
+                _native.ptr(dl.maps[d]), _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T), _native.ptr(ws),
+                wsb, status_d, 0, int(pre_inv), None, 0, 0, None, None, 0, None, 0, stream),
+                f"hps_merge_level(depth {d})")
+            next_pre = False
+        pre_inv = next_pre
         mark()
         del ws
         instrumentation.bump("merge", nbatch)

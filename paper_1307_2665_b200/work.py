@@ -32,6 +32,20 @@ def merge_flops_depth(L, q, d):
     return (2 ** d) * (2.0 / 3.0 * n3 ** 3 + 2.0 * n3 ** 2 * ne + 2.0 * n3 * ne ** 2)
 
 
+def merge_stage_flops(L, q, ahead=()):
+    """Per merge stage (depth d) flops as executed: a depth in `ahead` (solver.lookahead_depths)
+    also runs its parent's interface inverse (2/3 n3^3 per parent, moved from depth d - 1) and the
+    look-ahead GEMM that forms the parent's X (4 pn3^2 n3 per parent, extra work beyond the
+    reference count, so not added: achieved rates stay on the algorithmic count)."""
+    out = {d: merge_flops_depth(L, q, d) for d in range(2 * L)}
+    for d in ahead:
+        pn3, _ = depth_sizes(L, q, d - 1)
+        inv = (2 ** (d - 1)) * 2.0 / 3.0 * pn3 ** 3
+        out[d - 1] -= inv
+        out[d] += inv
+    return out
+
+
 def merge_bytes_depth(L, q, d):
     """Children's T in (two m x m, m = ne/2 + n3), S and T out."""
     n3, ne = depth_sizes(L, q, d)
