@@ -67,6 +67,10 @@ def load():
                                           c_dp, c_sz, c_dp, c_int, c_int, c_dp, c_int, c_int, c_dp, c_dp, c_sz, c_dp,
                                           c_int, c_dp]
     lib.hps_merge_level_ahead.restype = c_int
+    lib.hps_debug_ahead_times.argtypes = [c_int, ctypes.POINTER(ctypes.c_float)]
+    lib.hps_debug_ahead_times.restype = c_int
+    lib.hps_debug_ahead_depth.argtypes = [c_int]
+    lib.hps_debug_ahead_depth.restype = None
     lib.hps_solve_level.argtypes = [c_int, c_int, c_int, c_dp, c_dp, c_ll, c_dp, c_int, c_int, c_dp]
     lib.hps_solve_level.restype = c_int
     lib.hps_dgemm_batched.argtypes = [c_int, c_int, c_int, c_int, c_d, c_dp, c_ll, c_ll, c_dp, c_ll, c_ll, c_dp,

@@ -812,6 +812,25 @@ extern "C" size_t hps_merge_workspace_bytes(int nbatch, int n3, int ne) {
   return d * sizeof(double) + 256;
 }
 
+// HPS_AHEAD_PROFILE=1 (eager builds only, dev tool): timing events at the look-ahead fork (0), the
+// end of the parent inverse on the look-ahead stream (1), the end of the T GEMM (2) and the join
+// (3), per depth; hps_debug_ahead_times reads the elapsed times relative to event 0.
+static cudaEvent_t g_probe_ev[32][4];
+static int g_probe_depth = -1;
+static void ahead_probe(int k, cudaStream_t s) {
+  static const int on = getenv("HPS_AHEAD_PROFILE") ? atoi(getenv("HPS_AHEAD_PROFILE")) : 0;
+  if (!on || g_probe_depth < 0 || g_probe_depth >= 32) return;
+  cudaEvent_t& e = g_probe_ev[g_probe_depth][k];
+  if (!e) cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+}
+extern "C" int hps_debug_ahead_times(int depth, float* out) {  // ms since the fork: inv end, T end, join
+  if (depth < 0 || depth >= 32 || !g_probe_ev[depth][0]) return 1;
+  for (int k = 1; k < 4; ++k) cudaEventElapsedTime(out + k - 1, g_probe_ev[depth][0], g_probe_ev[depth][k]);
+  return 0;
+}
+extern "C" void hps_debug_ahead_depth(int depth) { g_probe_depth = depth; }
+
 // Parent-depth look-ahead of hps_merge_level_ahead (see k_ahead_rows).
 struct AheadArgs {
   const int* pmaps;       // parent depth's split maps (j1a, j2b, j3a, j3b)
@@ -893,6 +912,7 @@ static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const doub
       HPS_LAUNCH_CHECK();
     }
     // fork: deflate + invert the parent X on the high-priority look-ahead stream
+    ahead_probe(0, st);
     HPS_CUDA_CHECK(cudaStreamWaitEvent(fc.ahead, record_on(st), 0));
     if (pdefl) {
       k_deflate<<<dim3(P, pn3 / q), 256, 0, fc.ahead>>>(pX, pn3, q, ah->pvmode, ah->pvmode + q, pdiag);
@@ -903,6 +923,7 @@ static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const doub
     static const int reserve = getenv("HPS_GJ_RESERVE") ? atoi(getenv("HPS_GJ_RESERVE")) : 0;
     HPS_TRY(inverse_rec(pX, pn3, (long long)pn3 * pn3, pn3, P, ptmp, ah->pstatus, ah->pstatus_base, fc.ahead,
                         fc.ahead_side, reserve != 0));
+    ahead_probe(1, fc.ahead);
   }
   {  // T = blkdiag(Ta[j1a, j1a], Tb[j2b, j2b]) + C S, the blkdiag read by the GEMM epilogue
     GemmParams gp{ne, ne, n3, nbatch, Cm, n3, (long long)ne * n3, S_out, ne, (long long)n3 * ne, nullptr, 0,
@@ -912,7 +933,9 @@ static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const doub
     gp.blk_j2b = j2b;
     HPS_TRY(dgemm_launch(gp, st));
   }
+  if (ahead) ahead_probe(2, st);
   if (ahead) HPS_CUDA_CHECK(cudaStreamWaitEvent(st, record_on(fc.ahead), 0));  // join
+  if (ahead) ahead_probe(3, st);
   return HPS_OK;
 }
 
