@@ -303,12 +303,12 @@ def main():
     hpeak, hsrc = hbm_peak()
     t_roof = Wk.build_roofline_seconds(L, q, inp.ngroups, peak, hpeak)
     traffic, traffic_src = None, None  # DRAM bytes per launch of the dominant kernel (committed ncu capture)
-    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "leaf16v3_ncu_r01c.json")
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "leaf16v3_ncu_r01d.json")
     if dom == "leaf" and leaf_kernel == "hps::k_leaf16v3" and os.path.exists(prof):
         pj = json.load(open(prof))
         if pj.get("workload") == workload:
             traffic = float(pj["dram_bytes_per_launch"])
-            traffic_src = (f"profiles/leaf16v3_ncu_r01c.json: dram read+write per launch (ncu --set full); "
+            traffic_src = (f"profiles/leaf16v3_ncu_r01d.json: dram read+write per launch (ncu --set full); "
                            f"algorithmic {pj['algorithmic_bytes_per_launch']:.3g} B")
     roofline = {
         "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
