@@ -31,6 +31,22 @@ namespace hps {
 // ---------------------------------------------------------------------------------------------
 // ChildRef (children of merge b) lives in gemm.cuh: the T GEMM epilogue reads the blkdiag through it.
 
+// dst[c] = sign * src[map[c]] for c < n by one warp: 4 elements per lane per step, all index loads
+// before the value loads (independent loads in flight together instead of load -> load chains)
+__device__ __forceinline__ void warp_gather(double* __restrict__ dst, const double* __restrict__ src,
+                                            const int* __restrict__ map, int n, double sign, int lane) {
+  int c = lane;
+  for (; c + 96 < n; c += 128) {
+    const int i0 = __ldg(map + c), i1 = __ldg(map + c + 32), i2 = __ldg(map + c + 64), i3 = __ldg(map + c + 96);
+    const double v0 = src[i0], v1 = src[i1], v2 = src[i2], v3 = src[i3];
+    dst[c] = sign * v0;
+    dst[c + 32] = sign * v1;
+    dst[c + 64] = sign * v2;
+    dst[c + 96] = sign * v3;
+  }
+  for (; c < n; c += 32) dst[c] = sign * src[__ldg(map + c)];
+}
+
 __global__ void k_gather_xr(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b,
                             const int* __restrict__ j3a, const int* __restrict__ j3b, int n3, int ne,
                             double* __restrict__ X, double* __restrict__ R,
@@ -51,13 +67,14 @@ __global__ void k_gather_xr(ChildRef ch, const int* __restrict__ j1a, const int*
     // so an integer atomicMax is exact and independent of the CTA order
     if (c == r && diagmax) atomicMax(diagmax + b, (unsigned long long)__double_as_longlong(fabs(v)));
   }
-  for (int c = lane; c < n1; c += 32) Rr[c] = -Ta[j1a[c]];
-  for (int c = lane; c < n1; c += 32) Rr[n1 + c] = Tb[j2b[c]];
+  warp_gather(Rr, Ta, j1a, n1, -1.0, lane);
+  warp_gather(Rr + n1, Tb, j2b, n1, 1.0, lane);
 }
 
-__global__ void k_gather_c(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b,
-                           const int* __restrict__ j3a, const int* __restrict__ j3b, int n3, int ne,
-                           double* __restrict__ Cm) {
+// C[b] (ne x n3), one warp per row (n3 >= 32)
+__global__ void k_gather_c_rows(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b,
+                                const int* __restrict__ j3a, const int* __restrict__ j3b, int n3, int ne,
+                                double* __restrict__ Cm) {
   const int b = blockIdx.x;
   const int r = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -65,9 +82,43 @@ __global__ void k_gather_c(ChildRef ch, const int* __restrict__ j1a, const int* 
   const int n1 = ne / 2;
   const bool top = r < n1;
   const double* src = top ? ch.a(b) + (long long)j1a[r] * ch.m : ch.bb(b) + (long long)j2b[r - n1] * ch.m;
-  const int* j3 = top ? j3a : j3b;
-  double* Cr = Cm + ((long long)b * ne + r) * n3;
-  for (int c = lane; c < n3; c += 32) Cr[c] = src[j3[c]];
+  warp_gather(Cm + ((long long)b * ne + r) * n3, src, top ? j3a : j3b, n3, 1.0, lane);
+}
+
+// C[b] (ne x n3), element-parallel (one thread per 4 entries, 256-entry strides), for narrow rows
+// (n3 = 16 at the leaf pairs would leave half of every row warp idle); measured faster below 32
+// columns, slower above
+__global__ void k_gather_c(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b,
+                           const int* __restrict__ j3a, const int* __restrict__ j3b, int n3, int ne,
+                           double* __restrict__ Cm) {
+  const int b = blockIdx.x;
+  const int n1 = ne / 2;
+  const long long total = (long long)ne * n3;
+  const double* Ta = ch.a(b);
+  const double* Tb = ch.bb(b);
+  double* Cb = Cm + (long long)b * total;
+  for (long long e0 = (long long)blockIdx.y * 1024 + threadIdx.x; e0 < total; e0 += (long long)gridDim.y * 1024) {
+    long long src[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // all index loads first
+      const long long e = e0 + 256 * k;
+      src[k] = -1;
+      if (e < total) {
+        const int r = (int)(e / n3), c = (int)(e - (long long)r * n3);
+        src[k] = r < n1 ? (long long)__ldg(j1a + r) * ch.m + __ldg(j3a + c)
+                        : (long long)__ldg(j2b + r - n1) * ch.m + __ldg(j3b + c);
+      }
+    }
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const long long e = e0 + 256 * k;
+      v[k] = src[k] >= 0 ? ((int)(e / n3) < n1 ? Ta : Tb)[src[k]] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (src[k] >= 0) Cb[e0 + 256 * k] = v[k];
+  }
 }
 
 
@@ -79,16 +130,6 @@ __global__ void k_gather_c(ChildRef ch, const int* __restrict__ j1a, const int* 
 // one GEMM with K = 2 n3 over gathered operands. The parent's deflation and inverse then run on a
 // high-priority stream beside the T GEMM.
 // ---------------------------------------------------------------------------------------------
-// Block-diagonal addend of child k's T at (i, j) (the merge epilogue's blk_value, for any entry).
-__device__ __forceinline__ double blk_at(const ChildRef& ch, const int* j1a, const int* j2b, int n1, int k, int i,
-                                         int j) {
-  const bool ti = i < n1;
-  if ((j < n1) != ti) return 0.0;
-  const double* src = ti ? ch.a(k) : ch.bb(k);
-  const int ri = ti ? j1a[i] : j2b[i - n1], cj = ti ? j1a[j] : j2b[j - n1];
-  return src[(long long)ri * ch.m + cj];
-}
-
 // One warp per parent row r: Ag[b][r] = [Cm[2b][pj3a[r]] | -Cm[2b+1][pj3b[r]]] and
 // X[b][r][c] = blk_2b(pj3a[r], pj3a[c]) - blk_2b+1(pj3b[r], pj3b[c]).
 __global__ void k_ahead_rows(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b, int n3, int ne,
@@ -106,9 +147,26 @@ __global__ void k_ahead_rows(ChildRef ch, const int* __restrict__ j1a, const int
     Ar[k] = Ca[k];
     Ar[n3 + k] = -Cb[k];
   }
+  // X row: the block-diagonal addends of the two children (zero off their diagonal blocks). The
+  // row half (j1a / j2b side) of ia and ib is fixed per row, so only the column maps vary.
   double* Xr = X + ((long long)b * pn3 + r) * pn3;
-  for (int c = lane; c < pn3; c += 32)
-    Xr[c] = blk_at(ch, j1a, j2b, n1, 2 * b, ia, pj3a[c]) - blk_at(ch, j1a, j2b, n1, 2 * b + 1, ib, pj3b[c]);
+  const bool ta = ia < n1, tb = ib < n1;
+  const double* rowa = (ta ? ch.a(2 * b) : ch.bb(2 * b)) + (long long)(ta ? j1a[ia] : j2b[ia - n1]) * ch.m;
+  const double* rowb = (tb ? ch.a(2 * b + 1) : ch.bb(2 * b + 1)) + (long long)(tb ? j1a[ib] : j2b[ib - n1]) * ch.m;
+  auto colmap = [&](int j, bool top) { return (j < n1) == top ? (top ? j1a[j] : j2b[j - n1]) : -1; };
+  int c = lane;
+  for (; c + 32 < pn3; c += 64) {
+    const int ja0 = __ldg(pj3a + c), jb0 = __ldg(pj3b + c), ja1 = __ldg(pj3a + c + 32), jb1 = __ldg(pj3b + c + 32);
+    const int ma0 = colmap(ja0, ta), mb0 = colmap(jb0, tb), ma1 = colmap(ja1, ta), mb1 = colmap(jb1, tb);
+    const double a0 = ma0 >= 0 ? rowa[ma0] : 0.0, b0 = mb0 >= 0 ? rowb[mb0] : 0.0;
+    const double a1 = ma1 >= 0 ? rowa[ma1] : 0.0, b1 = mb1 >= 0 ? rowb[mb1] : 0.0;
+    Xr[c] = a0 - b0;
+    Xr[c + 32] = a1 - b1;
+  }
+  for (; c < pn3; c += 32) {
+    const int ma = colmap(pj3a[c], ta), mb = colmap(pj3b[c], tb);
+    Xr[c] = (ma >= 0 ? rowa[ma] : 0.0) - (mb >= 0 ? rowb[mb] : 0.0);
+  }
 }
 
 // One warp per row k of Bg[b] (2 n3 x pn3): S[2b][k][pj3a[c]] (k < n3), S[2b+1][k - n3][pj3b[c]].
@@ -868,7 +926,11 @@ static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const doub
   k_gather_xr<<<dim3(nbatch, (n3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, pre_inverted ? nullptr : X,
                                                         R, (deflate && !pre_inverted) ? diagmax : nullptr);
   HPS_LAUNCH_CHECK();
-  k_gather_c<<<dim3(nbatch, (ne + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, Cm);
+  if (n3 < 32)
+    k_gather_c<<<dim3(nbatch, (unsigned)std::min<long long>(((long long)ne * n3 + 1023) / 1024, 65535)), 256, 0,
+                 st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, Cm);
+  else
+    k_gather_c_rows<<<dim3(nbatch, (ne + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, Cm);
   HPS_LAUNCH_CHECK();
   if (!pre_inverted) {
     if (deflate) {
