@@ -642,6 +642,10 @@ int leaf16v3_grid(int ngroups) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static int per_sm = getenv("HPS_LEAF3_CTAS_PER_SM") ? atoi(getenv("HPS_LEAF3_CTAS_PER_SM")) : 2;
+  // HPS_LEAF_FREE_SMS: size the grid for that many fewer SMs (experiment: SMs left to a concurrent
+  // stream's merges in solver.Pipeline)
+  static int free_sms = getenv("HPS_LEAF_FREE_SMS") ? atoi(getenv("HPS_LEAF_FREE_SMS")) : 0;
+  sms = std::max(1, sms - free_sms);
   // the smallest grid with the same leaves per CTA as a full one: the grid-stride loop's critical
   // path is unchanged, and the spare CTA slots let other streams' small kernels (the next
   // problem's grouping in solver.Pipeline) run beside the leaf stage (cfg2: 293 of 296)
