@@ -296,7 +296,16 @@ def main():
     ach = stage_flops[dom] / (stage_ms[dom] / 1e3) / 1e12
     leaf_kernel = "hps::k_leaf16v3" if q == 16 and os.environ.get("HPS_LEAF_V", "3") != "2" else (
         "hps::k_leaf16" if q == 16 else "hps::k_leaf")
-    kernels = {"leaf": leaf_kernel}.get(dom, "hps_merge_level (gather, deflate, k_gj_inverse, dgemm_dmma)")
+    if dom == "leaf":
+        kernels = leaf_kernel
+    else:
+        dd = int(dom.split("_d")[-1])
+        ahead_set = solver.lookahead_depths(inp.layout)
+        kernels = ("hps_merge_level_ahead: R/C gathers, S GEMM, T GEMM (hps::dgemm64_kernel)"
+                   + ("; its interface inverse ran in depth %d's look-ahead" % (dd + 1) if dd + 1 in ahead_set
+                      else "; deflation + interface inverse (k_gj_blk / recursive block inverse)")
+                   + ("; forms and inverts depth %d's interface matrix beside its T GEMM" % (dd - 1)
+                      if dd in ahead_set else ""))
     build_flops = sum(stage_flops.values())
     solve_flops = Wk.solve_flops(L, q, b)
     S_bytes = Wk.solve_S_bytes(L, q)
@@ -304,11 +313,21 @@ def main():
     t_roof = Wk.build_roofline_seconds(L, q, inp.ngroups, peak, hpeak)
     traffic, traffic_src = None, None  # DRAM bytes per launch of the dominant kernel (committed ncu capture)
     prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "leaf16v3_ncu_r01d.json")
+    gprof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "dgemm64_cfg3_d0_ncu_r01d.json")
     if dom == "leaf" and leaf_kernel == "hps::k_leaf16v3" and os.path.exists(prof):
         pj = json.load(open(prof))
         if pj.get("workload") == workload:
             traffic = float(pj["dram_bytes_per_launch"])
             traffic_src = (f"profiles/leaf16v3_ncu_r01d.json: dram read+write per launch (ncu --set full); "
+                           f"algorithmic {pj['algorithmic_bytes_per_launch']:.3g} B")
+    elif dom == "merge_d0" and os.path.exists(gprof):
+        pj = json.load(open(gprof))
+        if pj.get("workload") == workload:  # the stage's dominant kernel: its T GEMM
+            g = pj["grouped_rasterisation"]
+            traffic = float(g["dram_bytes_per_launch"])
+            traffic_src = (f"profiles/dgemm64_cfg3_d0_ncu_r01d.json: dram read+write of the depth-0 T GEMM "
+                           f"({g['gpu_time_ms']:.2f} ms of the stage; DMMA pipe active "
+                           f"{pj['raw']['sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active']}); "
                            f"algorithmic {pj['algorithmic_bytes_per_launch']:.3g} B")
     roofline = {
         "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,

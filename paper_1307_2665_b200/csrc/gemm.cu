@@ -120,6 +120,8 @@ static int launch_cfg64(const GemmParams& p, cudaStream_t stream) {
     q.partial = splitk_scratch((size_t)split * p.batch * (size_t)p.M * p.N, stream);
     if (!q.partial) q.split = 1;
   }
+  static const int group_m = getenv("HPS_GEMM_GROUP_M") ? atoi(getenv("HPS_GEMM_GROUP_M")) : 16;
+  q.group_m = group_m;
   dim3 grid((p.N + 63) / 64, (p.M + 63) / 64, p.batch * q.split);
   kern<<<grid, 128, Cfg::kSmem, stream>>>(q);
   HPS_LAUNCH_CHECK();

@@ -46,6 +46,7 @@ struct GemmParams {
   ChildRef blk{nullptr, 0, nullptr, 0};
   const int* blk_j1a = nullptr;
   const int* blk_j2b = nullptr;
+  int group_m = 0;  // 64 x 64 kernel: grouped tile rasterisation (0 = row-major)
 };
 
 __device__ __forceinline__ double blk_value(const GemmParams& p, int b, int r, int c) {
@@ -271,7 +272,18 @@ __global__ void __launch_bounds__(128, MINB) dgemm64_kernel(GemmParams p) {
   double* sB = smem + STAGES * Cfg::kStageA;
   const int b = blockIdx.z / p.split;
   const int ks_idx = blockIdx.z - b * p.split;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  // Grouped rasterisation (p.group_m > 0, large grids): consecutive CTAs walk down group_m tile rows
+  // before moving right, so the ~444 CTAs of a wave share ~sqrt(444) row and column panels of A and
+  // B in L2 instead of streaming all of B once per wave of tile rows.
+  int tile_m = blockIdx.y, tile_n = blockIdx.x;
+  if (p.group_m > 0 && (int)gridDim.y > p.group_m) {
+    const int pid = blockIdx.y * gridDim.x + blockIdx.x, per_group = p.group_m * gridDim.x;
+    const int first_m = (pid / per_group) * p.group_m;
+    const int gsize = min((int)gridDim.y - first_m, p.group_m);
+    tile_m = first_m + (pid % per_group) % gsize;
+    tile_n = (pid % per_group) / gsize;
+  }
+  const int m0 = tile_m * BM, n0 = tile_n * BN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t = lane & 3;
