@@ -108,3 +108,27 @@ def test_work_model_matches_oracle_counts():
     # SURVEY.md §8d build totals: cfg2 1.79e11 flop
     tot = 4096 * W.leaf_flops(16) + sum(W.merge_flops_depth(6, 16, d) for d in range(12))
     assert abs(tot - 1.79e11) / 1.79e11 < 0.01
+
+
+def test_lookahead_rule_and_stage_flop_accounting(monkeypatch):
+    # hps_merge_level_ahead is used where the parent's interface inverse is a latency chain worth
+    # hiding: pn3 >= 128 and pn3 * n3 * P <= 3.2e6 (every depth of L <= 7, none at L >= 8). The
+    # bench attributes the moved inverse flops to the depth that runs them; totals are unchanged.
+    from paper_1307_2665_b200 import work as W
+    monkeypatch.delenv("HPS_AHEAD_MIN_N3", raising=False)
+    monkeypatch.delenv("HPS_AHEAD_WORK", raising=False)
+    for L, want in ((4, {1, 2, 3}), (6, set(range(1, 8))), (7, set(range(1, 10))), (8, set()), (9, set())):
+        tree, _ = P.build_tree(P.Rectangle(0, 1, 0, 1), L, 16)
+        lay = layout_of(tree)
+        got = solver.lookahead_depths(lay)
+        assert got == want, (L, got)
+        f = W.merge_stage_flops(L, 16, got)
+        ref = {d: W.merge_flops_depth(L, 16, d) for d in range(2 * L)}
+        assert abs(sum(f.values()) - sum(ref.values())) < 1e-6 * sum(ref.values())
+        inv = {d: 2 ** d * 2.0 / 3.0 * W.depth_sizes(L, 16, d)[0] ** 3 for d in range(2 * L)}
+        for d in range(2 * L):  # depth d's inverse runs in depth d + 1 when d + 1 looks ahead
+            want_d = ref[d] - (inv[d] if d + 1 in got else 0.0) + (inv[d - 1] if d in got else 0.0)
+            assert f[d] == pytest.approx(want_d)
+    monkeypatch.setenv("HPS_AHEAD_MIN_N3", "0")
+    tree, _ = P.build_tree(P.Rectangle(0, 1, 0, 1), 6, 16)
+    assert solver.lookahead_depths(layout_of(tree)) == set()
