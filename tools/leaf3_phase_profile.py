@@ -1,6 +1,6 @@
 """Per-phase cycle breakdown of k_leaf16v3 (tools/libhps_b200_prof.so built with -DHPS_LEAF_PROFILE)."""
 import os, sys, ctypes
-os.environ["HPS_LIB"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhps_b200_prof.so")
+os.environ.setdefault("HPS_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhps_b200_prof.so"))
 sys.path.insert(0, ".")
 import numpy as np, torch
 import paper_1307_2665_b200 as P
