@@ -170,6 +170,11 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
   static const int smallk = getenv("HPS_SMALLK") ? atoi(getenv("HPS_SMALLK")) : 1;
   if (v64 && !(p.Bidx && p.N <= 64) && smallk && p.K <= 32) return launch_cfg64<16, 2, 4>(p, stream);
   if (v64 && !(p.Bidx && p.N <= 64)) return launch_cfg64<16, 3, 3>(p, stream);
+  // narrow row-gather GEMMs with few rows (the batched solve's bottom depths: M = n3 = 16 or 32):
+  // tiles as tall as the problem instead of 64-row tiles that are 50-75% padding
+  static const int smallm = getenv("HPS_SMALLM") ? atoi(getenv("HPS_SMALLM")) : 1;
+  if (smallm && p.Bidx && p.N <= 64 && p.M <= 16) return launch_cfg<16, 64, 16, 1, 2, 3>(p, stream);
+  if (smallm && p.Bidx && p.N <= 64 && p.M <= 32) return launch_cfg<32, 64, 16, 1, 2, 3>(p, stream);
   double tiles128 = double((p.M + 127) / 128) * double((p.N + 127) / 128) * p.batch;
   // HPS_GEMM64=0: the previous tiling (128 x 128 x 16, 8 warps of 64 x 32, one CTA per SM)
   if (p.M >= 128 && p.N >= 128 && tiles128 >= 148.0) return launch_cfg<128, 128, 16, 2, 4, 4>(p, stream);
