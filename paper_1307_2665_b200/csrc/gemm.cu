@@ -168,6 +168,10 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
   // K <= 32 (the bottom merge depths: K = n3 = 16 or 32, one or two k tiles): two stages are enough
   // and the smaller footprint fits 4 CTAs per SM, more tiles in flight for these memory-bound shapes
   static const int smallk = getenv("HPS_SMALLK") ? atoi(getenv("HPS_SMALLK")) : 1;
+  // M <= 32 (the merge S = X^-1 R GEMMs of the bottom depths, n3 = 16 or 32): row tiles of 16/32
+  static const int smallm_s = getenv("HPS_SMALLM_S") ? atoi(getenv("HPS_SMALLM_S")) : 1;
+  if (smallm_s && !p.Bidx && p.M <= 16 && p.N >= 64) return launch_cfg<16, 64, 16, 1, 2, 3>(p, stream);
+  if (smallm_s && !p.Bidx && p.M <= 32 && p.N >= 64) return launch_cfg<32, 64, 16, 1, 2, 3>(p, stream);
   if (v64 && !(p.Bidx && p.N <= 64) && smallk && p.K <= 32) return launch_cfg64<16, 2, 4>(p, stream);
   if (v64 && !(p.Bidx && p.N <= 64)) return launch_cfg64<16, 3, 3>(p, stream);
   // narrow row-gather GEMMs with few rows (the batched solve's bottom depths: M = n3 = 16 or 32):
