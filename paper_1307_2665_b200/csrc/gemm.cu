@@ -172,6 +172,9 @@ int dgemm_launch(const GemmParams& p, cudaStream_t stream) {
   static const int smallm_s = getenv("HPS_SMALLM_S") ? atoi(getenv("HPS_SMALLM_S")) : 1;
   if (smallm_s && !p.Bidx && p.M <= 16 && p.N >= 64) return launch_cfg<16, 64, 16, 1, 2, 3>(p, stream);
   if (smallm_s && !p.Bidx && p.M <= 32 && p.N >= 64) return launch_cfg<32, 64, 16, 1, 2, 3>(p, stream);
+  // 96 x 96 (the leaf-pair merges' T GEMM): 48 x 48 tiles cover it exactly (64 x 64 tiles: 56%)
+  static const int t96 = getenv("HPS_T96") ? atoi(getenv("HPS_T96")) : 1;
+  if (t96 && !p.Bidx && p.M == 96 && p.N == 96) return launch_cfg<48, 48, 16, 2, 2, 2>(p, stream);
   if (v64 && !(p.Bidx && p.N <= 64) && smallk && p.K <= 32) return launch_cfg64<16, 2, 4>(p, stream);
   if (v64 && !(p.Bidx && p.N <= 64)) return launch_cfg64<16, 3, 3>(p, stream);
   // narrow row-gather GEMMs with few rows (the batched solve's bottom depths: M = n3 = 16 or 32):
