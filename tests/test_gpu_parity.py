@@ -271,10 +271,11 @@ def test_distributed_path_single_rank_cuda_backend():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("q,L,cfg", [(21, 2, 2), (12, 3, 1), (10, 2, 3), (7, 3, 5)])
+@pytest.mark.parametrize("q,L,cfg", [(21, 2, 2), (12, 3, 1), (10, 2, 3), (7, 3, 5), (21, 4, 2), (12, 5, 2)])
 def test_general_q_against_oracle(q, L, cfg):
     """Any q >= 3 (the paper uses q = 21): generic leaf kernel, unaligned GEMM path, unequal
-    recursive-inverse halves."""
+    recursive-inverse halves; at (21, 4) and (12, 5) the look-ahead interface inverse runs too
+    (parent interfaces of 168..336 and 192..384 nodes)."""
     tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), L, q)
     st = solver.build(tree, nodes, problems.coefficients(cfg), keep_level_T=True)
     ot = O.build_tree((0, 1, 0, 1), L, q)
