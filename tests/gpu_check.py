@@ -3,7 +3,7 @@ import sys, time
 import numpy as np
 import torch
 
-sys.path.insert(0, ".")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from oracle import hps_oracle as O
 import paper_1307_2665_b200 as P
 from paper_1307_2665_b200 import _native, problems, solver

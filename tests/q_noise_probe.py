@@ -1,5 +1,5 @@
 import sys, os
-sys.path.insert(0, "."); sys.path.insert(0, "tests")
+import os; _here = os.path.dirname(os.path.abspath(__file__)); sys.path.insert(0, os.path.dirname(_here)); sys.path.insert(0, _here)
 import numpy as np
 import paper_1307_2665_b200 as P
 from paper_1307_2665_b200 import solver, problems
