@@ -94,7 +94,7 @@ def test_full_size_cfg2_against_oracle():
     assert rel(O.leaf_cheb_boundary(ost, u), O.leaf_cheb_boundary(ost, O.solve(ost, F))) < 1e-10
 
 
-@pytest.mark.parametrize("cfg,L", [(1, 6), (2, 6), (5, 7), (5, 9)])
+@pytest.mark.parametrize("cfg,L", [(1, 6), (2, 6), (5, 7), (5, 9), (4, 8)])
 def test_full_size_properties(cfg, L):
     """Size-independent properties at BASELINE sizes (config 5 at L = 9: 6.7e7 unknowns, 8.6 GB
     root DtN): constants are in the DtN null space for operators with no
@@ -102,7 +102,8 @@ def test_full_size_properties(cfg, L):
     tree, nodes, st = gpu_build(cfg, L)
     T = st.root_T.device_tensor
     one = torch.ones(T.shape[0], dtype=torch.float64, device=T.device)
-    assert float((T @ one).abs().max() / T.abs().max()) < 1e-10
+    if cfg != 4:  # config 4 (variable Helmholtz) has a zeroth-order term: linearity only
+        assert float((T @ one).abs().max() / T.abs().max()) < 1e-10
     F = problems.boundary_data(2, nodes.points[tree.root.I_e], seed=9, batch=2)
     u = solver.solve(st, F)
     uc = solver.solve(st, 2.0 * F[:, 0] - 3.0 * F[:, 1])
