@@ -127,18 +127,36 @@ class CudaBackend:
                                          _native.stream_ptr()), "hps_leaf_stage")
         return Psi, T, cond
 
-    def merge_level(self, d, nbatch, child_T, child_idx, status):
+    def merge_level(self, d, nbatch, child_T, child_idx, status, parent_status=None):
+        """One depth's merges for this rank's slots. With `parent_status` (the next call merges
+        these boxes' parents on this rank), the look-ahead inverse of solver.build_device runs too
+        (hps_merge_level_ahead, where solver.lookahead_depths applies); the next call then starts
+        from the pre-inverted interface matrices."""
+        from .solver import lookahead_depths
+
         lib, torch = self.lib, self.torch
         dl = self.lay.depths[d]
         S = self.empty((nbatch, dl.n3, dl.ne))
         T = self.empty((nbatch, dl.ne, dl.ne))
         wsb = lib.hps_merge_workspace_bytes(nbatch, dl.n3, dl.ne)
-        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        pre = getattr(self, "_ahead_ws", None) is not None and self._ahead_ws[0] == (d, nbatch)
+        ws = self._ahead_ws[1] if pre else torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        self._ahead_ws = None
         idx = None if child_idx is None else self.torch.from_numpy(np.asarray(child_idx, np.int32)).to(self.device)
-        _native.check(lib.hps_merge_level(nbatch, dl.n3, dl.ne, dl.m, self.lay.q, _native.ptr(child_T),
-                                          dl.m * dl.m, _native.ptr(idx), _native.ptr(self.dl.maps[d]),
-                                          _native.ptr(self.dl.vmode[d]), _native.ptr(S), _native.ptr(T),
-                                          _native.ptr(ws), wsb, _native.ptr(status), 0, _native.stream_ptr()),
+        if parent_status is not None and nbatch % 2 == 0 and d in lookahead_depths(self.lay):
+            pl = self.lay.depths[d - 1]
+            pwsb = lib.hps_merge_workspace_bytes(nbatch // 2, pl.n3, pl.ne)
+            pws = torch.empty(pwsb, dtype=torch.uint8, device=self.device)
+            pargs = (_native.ptr(self.dl.maps[d - 1]), pl.n3, pl.ne, _native.ptr(self.dl.vmode[d - 1]),
+                     _native.ptr(pws), pwsb, _native.ptr(parent_status), 0)
+            self._ahead_ws = ((d - 1, nbatch // 2), pws)
+        else:
+            pargs = (None, 0, 0, None, None, 0, None, 0)
+        _native.check(lib.hps_merge_level_ahead(nbatch, dl.n3, dl.ne, dl.m, self.lay.q, _native.ptr(child_T),
+                                                dl.m * dl.m, _native.ptr(idx), _native.ptr(self.dl.maps[d]),
+                                                _native.ptr(self.dl.vmode[d]), _native.ptr(S), _native.ptr(T),
+                                                _native.ptr(ws), wsb, _native.ptr(status), 0, int(pre), *pargs,
+                                                _native.stream_ptr()),
                       f"hps_merge_level(depth {d})")
         return S, T
 
@@ -253,13 +271,20 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None):
     Psi, Tleaf, cond = backend.leaf_stage(inputs.fields, inputs.scalars, int(inputs.reps.size))
     st.psi_groups, st.T_leaf_groups, st.leaf_group, st.cond = Psi, Tleaf, gid, cond
 
-    # ---- local merges, depths 2L-1 .. s ----
+    # ---- local merges, depths 2L-1 .. s (the parents of a local depth above s are local too, so
+    # their status words exist one call early for the look-ahead inverse) ----
     child_T, child_idx = Tleaf, gid
+    ahead_status = {}
     for d in range(2 * L - 1, s - 1, -1):
         a, b = plan.local_slots(rank, d)
-        status = backend.status_word()
+        status = ahead_status.pop(d, None)
+        if status is None:
+            status = backend.status_word()
         st.statuses.append((d, a, status))
-        S, T = backend.merge_level(d, b - a, child_T, child_idx, status)
+        pstatus = None
+        if d - 1 >= s:
+            pstatus = ahead_status[d - 1] = backend.status_word()
+        S, T = backend.merge_level(d, b - a, child_T, child_idx, status, parent_status=pstatus)
         st.S_local[d] = S
         child_T, child_idx = T, None
     if s == 2 * L:  # one leaf per rank

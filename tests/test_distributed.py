@@ -55,7 +55,7 @@ class NumpyBackend:
         Psi, T, cond = O.leaf_operators(self.geom, fields, np.arange(ngroups))
         return torch.from_numpy(Psi), torch.from_numpy(T), torch.from_numpy(cond)
 
-    def merge_level(self, d, nbatch, child_T, child_idx, status):
+    def merge_level(self, d, nbatch, child_T, child_idx, status, parent_status=None):
         dl = self.lay.depths[d]
         Tc = child_T.numpy()
         S, T = [], []
