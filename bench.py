@@ -438,6 +438,7 @@ def bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, w
         u = parallel.solve_distributed(st, F, comm)
         return st, u
 
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -446,18 +447,24 @@ def bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, w
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clocks.start()
     l0 = lib.hps_launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
+    times = []
     for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flushed between steps, outside the step events
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
         step()
-    e1.record()
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
     launches = lib.hps_launch_count() - l0
-    t = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=dev)
+    t = torch.tensor([float(np.mean(times))], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t.item())
     if rank == 0:
@@ -467,7 +474,8 @@ def bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, w
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload, "unknowns": unknowns, "batch": b,
                        "parallelism": f"subtree split at depth {int(np.log2(world))}, NCCL send/recv for the top merges",
-                       "timing": "CUDA events around K steps, max over ranks; inputs resident (sampled + uploaded once per rank)"},
+                       "timing": "CUDA events around each step (ranks start together after a barrier), mean over K steps, max over ranks; inputs resident (sampled + uploaded once per rank)",
+                       "l2": "flushed (256 MB write) between timed steps, outside the step events"},
             "gpu_launches": int(launches), "clocks": clk,
             "note": "e2e, roofline and cpu_baseline are reported on the N=1 line"}))
     dist.destroy_process_group()
