@@ -19,6 +19,7 @@
  *                       (np.unique over the stacked coefficient sample rows)
  *   hps_leaf_fields / hps_eval_points <- _leaf_field + the barycentric evaluation of post_process and
  *                       boundary_flux_at, solver.py:349-400
+ *   hps_tree_sizes / hps_tree_layout <- grid.build_tree, grid.py:204-322 (host code)
  *   hps_gauge_sides / hps_gauge_gather <- (new) Gauss-node solution
  *                       re-tabulated from the leaf fields with the L4 blocks (leafops.py:191-198)
  */
@@ -42,6 +43,16 @@ int hps_version(void);
 int hps_device_check(int* major, int* minor, int* sms);
 /* Kernels launched by this library so far in this process (benchmark accounting). */
 long long hps_launch_count(void);
+/* Host-side tree / node layout (<- grid.build_tree, grid.py:204-322): sizes,
+ * then the arrays, all HOST pointers and caller-allocated. hps_tree_sizes fills n3/ne/m per depth
+ * d < 2L (arrays of max(2L, 1) entries) and returns N, the number of Gauss nodes (-1 on bad
+ * arguments). hps_tree_layout writes points[N][2], on_vertical[N], leaf_cells[4^L][2],
+ * leaf_I_e[4^L][4q], and per depth Ie[d] ([2^d][ne]) and maps[d] (j1a[ne/2], j2b[ne/2], j3a[n3],
+ * j3b[n3]); gauss01[q] = (Gauss-Legendre nodes + 1) / 2. Bit-exact with the reference layout. */
+long long hps_tree_sizes(int L, int q, long long* n3, long long* ne, long long* m);
+int hps_tree_layout(int L, int q, double x_lo, double y_lo, double width, double height, const double* gauss01,
+                    double* points, unsigned char* on_vertical, long long* leaf_cells, long long* leaf_I_e,
+                    long long* const* Ie, long long* const* maps);
 /* Internal scratch set (split-K partial sums) used by this host thread's later enqueues: two
  * builds in flight at once on different streams must use different slots (0..3; default 0). */
 int hps_set_scratch_slot(int slot);

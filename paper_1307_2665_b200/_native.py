@@ -26,7 +26,7 @@ EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_launch_coun
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
            "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched", "hps_leaf_hash",
            "hps_leaf_verify", "hps_leaf_fields", "hps_eval_points", "hps_gauge_sides", "hps_gauge_gather",
-           "hps_set_scratch_slot", "hps_merge_level_ahead")
+           "hps_set_scratch_slot", "hps_merge_level_ahead", "hps_tree_sizes", "hps_tree_layout")
 
 _lib = None
 
@@ -49,6 +49,13 @@ def load():
     lib.hps_last_error.restype = ctypes.c_char_p
     lib.hps_version.restype = c_int
     lib.hps_launch_count.restype = c_ll
+    pll = ctypes.POINTER(c_ll)
+    lib.hps_tree_sizes.argtypes = [c_int, c_int, pll, pll, pll]
+    lib.hps_tree_sizes.restype = c_ll
+    lib.hps_tree_layout.argtypes = [c_int, c_int, c_d, c_d, c_d, c_d, ctypes.POINTER(c_d), ctypes.POINTER(c_d),
+                                    ctypes.POINTER(ctypes.c_ubyte), pll, pll, ctypes.POINTER(pll),
+                                    ctypes.POINTER(pll)]
+    lib.hps_tree_layout.restype = c_int
     lib.hps_set_scratch_slot.argtypes = [c_int]
     lib.hps_set_scratch_slot.restype = c_int
     lib.hps_device_check.argtypes = [ctypes.POINTER(c_int)] * 3
@@ -95,6 +102,10 @@ def load():
     lib.hps_gauge_gather.restype = c_int
     _lib = lib
     return lib
+
+
+def last_error():
+    return load().hps_last_error().decode(errors="replace")
 
 
 def check(status, what):

@@ -9,11 +9,14 @@ FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompil
 objs=()
 pids=()
 mkdir -p "${HPS_OBJ:-${here}/../build_obj}"
-for f in capi gemm merge solve leaf leaf3 group post; do
+for f in capi gemm merge solve leaf leaf3 group post tree; do
   o="${HPS_OBJ:-${here}/../build_obj}/${f}.o"
+  # tree.cu is host code that must reproduce numpy's fp64 results bit for bit: no FMA contraction
+  extra=()
+  [[ "$f" == tree ]] && extra=(-Xcompiler -ffp-contract=off)
   if [[ ! -f "$o" || "${here}/${f}.cu" -nt "$o" || "${here}/common.cuh" -nt "$o" || "${here}/gemm.cuh" -nt "$o" || "${here}/leaf.cuh" -nt "$o" ]]; then
     rm -f "$o"
-    "$NVCC" "${FLAGS[@]}" -c "${here}/${f}.cu" -o "$o" &
+    "$NVCC" "${FLAGS[@]}" "${extra[@]}" -c "${here}/${f}.cu" -o "$o" &
     pids+=($!)
   fi
   objs+=("$o")

@@ -7,7 +7,9 @@ key dictionary:
   * heap numbering (children of i are 2i+1, 2i+2; grid.py:229-248 builds exactly this order);
   * every parent's I_i is a contiguous id range (grid.py:284-295 registers a fresh cut line);
   * every depth is uniform, so one (n3, ne) pair and one split map serve a whole depth.
-Cost is O(N log N) vectorised numpy (L=9: a few seconds; the reference needs minutes).
+The arrays come from the library's host C++ builder (csrc/tree.cu, hps_tree_layout; L=9 in about
+0.6 s, the reference needs minutes); the vectorised numpy version of the same closed forms below
+(HPS_NATIVE_LAYOUT=0) is the cross-check of the tests and the path when the library is absent.
 
 The per-depth arrays (`TreeLayout`) are what the CUDA kernels consume. `BoxTree.boxes` builds
 reference-shaped `BoxNode` objects lazily from them.
@@ -195,7 +197,8 @@ class TreeLayout:
         self.depths: list[DepthLayout] = []
         self.leaf_I_e = None  # (4^L, 4q)
         self.leaf_cells = None  # (4^L, 2) = (ix, iy) in heap order
-        self._build()
+        if not (_use_native_layout() and self._build_native()):
+            self._build()
 
     # -- cells of all boxes at one depth, heap order (grid.py:229-248) --
     def cells_at(self, d):
@@ -404,6 +407,70 @@ class TreeLayout:
         self.depths = depths
         self.root_I_e = child_Ie[0].astype(np.intp) if L > 0 else self.leaf_I_e[0].astype(np.intp)
 
+    def _build_native(self):
+        """The same layout from libhps_b200.so's host-side builder (csrc/tree.cu): every array
+        identical to _build's (tests/test_layout.py), ~10x faster at L = 9. False if the library
+        is not available."""
+        import ctypes
+
+        try:
+            from . import _native
+            lib = _native.load()
+        except ImportError:
+            return False
+        L, q, n = self.L, self.q, self.n
+        nd = 2 * L
+        n3 = np.zeros(max(nd, 1), np.int64)
+        ne = np.zeros(max(nd, 1), np.int64)
+        m = np.zeros(max(nd, 1), np.int64)
+        pl = ctypes.POINTER(ctypes.c_longlong)
+        N = lib.hps_tree_sizes(L, q, n3.ctypes.data_as(pl), ne.ctypes.data_as(pl), m.ctypes.data_as(pl))
+        if N < 0:
+            raise ValueError(_native.last_error())
+        dom = self.domain
+        gauss01 = np.ascontiguousarray((gauss_nodes(q) + 1.0) * 0.5)
+        points = np.empty((N, 2))
+        vert = np.empty(N, np.uint8)
+        nleaf = 1 << (2 * L)
+        leaf_cells = np.empty((nleaf, 2), np.int64)
+        leaf_Ie = np.empty((nleaf, 4 * q), np.int64)
+        Ie = [np.empty((1 << d, int(ne[d])), np.int64) for d in range(nd)]
+        maps = [np.empty(int(ne[d]) + 2 * int(n3[d]), np.int64) for d in range(nd)]
+        Ie_p = (pl * max(nd, 1))(*[a.ctypes.data_as(pl) for a in Ie])
+        maps_p = (pl * max(nd, 1))(*[a.ctypes.data_as(pl) for a in maps])
+        st = lib.hps_tree_layout(L, q, float(dom.x_lo), float(dom.y_lo), float(dom.width), float(dom.height),
+                                 gauss01.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                 points.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                 vert.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte)),
+                                 leaf_cells.ctypes.data_as(pl), leaf_Ie.ctypes.data_as(pl), Ie_p, maps_p)
+        if st != 0:
+            raise AssertionError(_native.last_error())
+        self.n_gamma = 4 * n * q
+        self.N = int(N)
+        self.n3s = [int(v) for v in n3[:nd]]
+        off = [self.n_gamma]
+        for d in range(nd):
+            off.append(off[-1] + (1 << d) * self.n3s[d])
+        self.depth_off = off
+        self.xline = dom.x_lo + np.arange(n + 1) * (dom.width / n)
+        self.yline = dom.y_lo + np.arange(n + 1) * (dom.height / n)
+        self.points = points
+        self.on_vertical = vert.view(bool)
+        self.leaf_cells = leaf_cells
+        self.leaf_I_e = leaf_Ie
+        self._h_ids = self._v_ids = None
+        depths = []
+        for d in range(nd):
+            n1, k3 = int(ne[d]) // 2, self.n3s[d]
+            mp = maps[d].astype(np.intp)
+            depths.append(DepthLayout(
+                depth=d, axis="v" if d % 2 == 0 else "h", n3=k3, ne=int(ne[d]), m=int(m[d]),
+                j1a=mp[:n1], j2b=mp[n1:2 * n1], j3a=mp[2 * n1:2 * n1 + k3], j3b=mp[2 * n1 + k3:],
+                I_e=Ie[d], Ii_start=(off[d] + np.arange(1 << d, dtype=np.int64) * k3).astype(np.intp)))
+        self.depths = depths
+        self.root_I_e = Ie[0][0].astype(np.intp) if L > 0 else leaf_Ie[0].astype(np.intp)
+        return True
+
     # -- reference-shaped accessors --
     def box_depth_slot(self, index):
         d = int(np.floor(np.log2(index + 1)))
@@ -502,6 +569,11 @@ class BoxTree:
     @property
     def leaf_height(self):
         return self.domain.height / (1 << self.levels)
+
+
+def _use_native_layout():
+    import os
+    return os.environ.get("HPS_NATIVE_LAYOUT", "1") != "0"
 
 
 @lru_cache(maxsize=8)

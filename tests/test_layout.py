@@ -128,3 +128,28 @@ def test_box_accessors():
     assert t.root.index == 0 and not t.root.is_leaf
     assert len(t.parents()) == 15
     assert t.boxes[-1].index == t.n_boxes - 1
+
+
+@pytest.mark.parametrize("dom,L,q", [((0, 1, 0, 1), 0, 16), ((0, 1, 0, 1), 1, 16), ((0, 1, 0, 1), 5, 16),
+                                     ((-0.3, 1.7, 0.25, 0.75), 3, 7), ((0, 2, 0, 1), 4, 21)])
+def test_native_layout_builder_is_identical(dom, L, q, monkeypatch):
+    # csrc/tree.cu (hps_tree_layout) against the numpy closed forms: every
+    # array bit for bit (coordinates as bit patterns), every per-depth map and I_e list
+    from paper_1307_2665_b200.grid import TreeLayout
+    monkeypatch.setenv("HPS_NATIVE_LAYOUT", "1")
+    a = TreeLayout(G.Rectangle(*dom), L, q)
+    monkeypatch.setenv("HPS_NATIVE_LAYOUT", "0")
+    b = TreeLayout(G.Rectangle(*dom), L, q)
+    for k in ("n_gamma", "N", "n3s", "depth_off"):
+        assert getattr(a, k) == getattr(b, k), k
+    for k in ("xline", "yline", "points", "on_vertical", "leaf_cells", "leaf_I_e", "root_I_e"):
+        x, y = getattr(a, k), getattr(b, k)
+        assert x.shape == y.shape and x.dtype == y.dtype, k
+        assert np.array_equal(x.view(np.uint8), y.view(np.uint8)), k
+    assert len(a.depths) == len(b.depths) == 2 * L
+    for da, db in zip(a.depths, b.depths):
+        for k in ("depth", "axis", "n3", "ne", "m"):
+            assert getattr(da, k) == getattr(db, k), k
+        for k in ("j1a", "j2b", "j3a", "j3b", "I_e", "Ii_start"):
+            x, y = getattr(da, k), getattr(db, k)
+            assert x.dtype == y.dtype and np.array_equal(x, y), (da.depth, k)
