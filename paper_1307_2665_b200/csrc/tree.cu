@@ -5,8 +5,10 @@
 // split maps per depth, and Gauss-node coordinates evaluated with the reference's fp64 expression
 // order (compiled with -ffp-contract=off: no fused multiply-adds). The caller (grid.py) allocates
 // every output; sizes follow from (L, q) alone. Every parent's split maps are checked, not a sample.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -70,6 +72,25 @@ struct Tree {
     }
   }
 };
+
+// body(lo, hi) over [0, n) split across up to 16 host threads (the big loops of a deep tree touch
+// hundreds of MB for the first time; the page faults dominate and spread across cores)
+template <class F>
+void parallel_for(long long n, F body) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const long long nt = std::min<long long>(hw, std::max<long long>(1, n / 4096));
+  if (nt <= 1) {
+    body(0LL, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const long long chunk = (n + nt - 1) / nt;
+  for (long long t = 0; t < nt; ++t) {
+    const long long lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo < hi) pool.emplace_back([=] { body(lo, hi); });
+  }
+  for (auto& th : pool) th.join();
+}
 
 }  // namespace
 
@@ -142,36 +163,40 @@ extern "C" int hps_tree_layout(int L, int q, double x_lo, double y_lo, double wi
     long long nx, ny;
     t.shape(d, nx, ny);
     const long long n3 = t.n3s[d], nseg = n3 / q;
-    for (long long k = 0; k < (1LL << d); ++k) {
-      long long ix, iy;
-      t.cells(d, k, ix, iy);
-      long long id = t.depth_off[d] + k * n3;
-      for (long long sg = 0; sg < nseg; ++sg)
-        for (int g = 0; g < q; ++g, ++id) {
-          if (d % 2 == 0)  // vertical cut line x = ix + nx / 2, segments along y
-            put(id, xline[ix + nx / 2], yline[iy + sg] + gy[g], true);
-          else
-            put(id, xline[ix + sg] + gx[g], yline[iy + ny / 2], false);
-        }
-    }
+    parallel_for(1LL << d, [&, d, nx, ny, n3, nseg](long long k0, long long k1) {
+      for (long long k = k0; k < k1; ++k) {
+        long long ix, iy;
+        t.cells(d, k, ix, iy);
+        long long id = t.depth_off[d] + k * n3;
+        for (long long sg = 0; sg < nseg; ++sg)
+          for (int g = 0; g < q; ++g, ++id) {
+            if (d % 2 == 0)  // vertical cut line x = ix + nx / 2, segments along y
+              put(id, xline[ix + nx / 2], yline[iy + sg] + gy[g], true);
+            else
+              put(id, xline[ix + sg] + gx[g], yline[iy + ny / 2], false);
+          }
+      }
+    });
   }
 
   // leaf boundary lists: S, E, N, W sides, increasing coordinate (grid.py:305-312)
   const long long nleaf = 1LL << (2 * L), m4 = 4LL * q;
-  for (long long k = 0; k < nleaf; ++k) {
-    long long ix, iy;
-    t.cells(2 * L, k, ix, iy);
-    leaf_cells[2 * k] = ix;
-    leaf_cells[2 * k + 1] = iy;
-    long long* out = leaf_I_e + k * m4;
-    const long long s0 = t.h_id(iy, ix), e0 = t.v_id(ix + 1, iy), n0 = t.h_id(iy + 1, ix), w0 = t.v_id(ix, iy);
-    for (int g = 0; g < q; ++g) {
-      out[g] = s0 + g;
-      out[q + g] = e0 + g;
-      out[2 * q + g] = n0 + g;
-      out[3 * q + g] = w0 + g;
+  parallel_for(nleaf, [&](long long k0, long long k1) {
+    for (long long k = k0; k < k1; ++k) {
+      long long ix, iy;
+      t.cells(2 * L, k, ix, iy);
+      leaf_cells[2 * k] = ix;
+      leaf_cells[2 * k + 1] = iy;
+      long long* out = leaf_I_e + k * m4;
+      const long long s0 = t.h_id(iy, ix), e0 = t.v_id(ix + 1, iy), n0 = t.h_id(iy + 1, ix), w0 = t.v_id(ix, iy);
+      for (int g = 0; g < q; ++g) {
+        out[g] = s0 + g;
+        out[q + g] = e0 + g;
+        out[2 * q + g] = n0 + g;
+        out[3 * q + g] = w0 + g;
+      }
     }
-  }
+  });
 
   // parents bottom-up: child-a remainder then child-b remainder (grid.py:313-319)
   const long long* child = leaf_I_e;
@@ -216,19 +241,24 @@ extern "C" int hps_tree_layout(int L, int q, double x_lo, double y_lo, double wi
       }
     }
     long long* Id = Ie[d];
-    for (long long k = 0; k < nb; ++k) {
-      const long long* A = child + (2 * k) * mchild;
-      const long long* B = child + (2 * k + 1) * mchild;
-      const long long s0 = t.depth_off[d] + k * n3;
-      for (long long i = 0; i < n3; ++i)  // every parent: the shared nodes are its I_i range
-        if (A[j3a[i]] != s0 + i || B[j3b[i]] != s0 + i) {
-          hps::set_error("hps_tree_layout: non-uniform split maps at depth %d (parent %lld)", d, k);
-          return HPS_ERR_ARG;
-        }
-      long long* out = Id + k * ned;
-      for (long long i = 0; i < n1; ++i) out[i] = A[j1a[i]];
-      for (long long i = 0; i < n1; ++i) out[n1 + i] = B[j2b[i]];
-    }
+    std::vector<char> badflag(std::max<long long>(1, nb), 0);
+    parallel_for(nb, [&](long long k0, long long k1) {
+      for (long long k = k0; k < k1; ++k) {
+        const long long* A = child + (2 * k) * mchild;
+        const long long* B = child + (2 * k + 1) * mchild;
+        const long long s0 = t.depth_off[d] + k * n3;
+        for (long long i = 0; i < n3; ++i)  // every parent: the shared nodes are its I_i range
+          if (A[j3a[i]] != s0 + i || B[j3b[i]] != s0 + i) badflag[k] = 1;
+        long long* out = Id + k * ned;
+        for (long long i = 0; i < n1; ++i) out[i] = A[j1a[i]];
+        for (long long i = 0; i < n1; ++i) out[n1 + i] = B[j2b[i]];
+      }
+    });
+    for (long long k = 0; k < nb; ++k)
+      if (badflag[k]) {
+        hps::set_error("hps_tree_layout: non-uniform split maps at depth %d (parent %lld)", d, k);
+        return HPS_ERR_ARG;
+      }
     child = Id;
     mchild = ned;
   }
