@@ -8,7 +8,7 @@ key dictionary:
   * every parent's I_i is a contiguous id range (grid.py:284-295 registers a fresh cut line);
   * every depth is uniform, so one (n3, ne) pair and one split map serve a whole depth.
 The arrays come from the library's host C++ builder (csrc/tree.cu, hps_tree_layout; L=9 in about
-0.6 s, the reference needs minutes); the vectorised numpy version of the same closed forms below
+0.2 s, the reference needs minutes); the vectorised numpy version of the same closed forms below
 (HPS_NATIVE_LAYOUT=0) is the cross-check of the tests and the path when the library is absent.
 
 The per-depth arrays (`TreeLayout`) are what the CUDA kernels consume. `BoxTree.boxes` builds
