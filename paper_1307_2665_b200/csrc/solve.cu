@@ -22,19 +22,19 @@ __global__ void __launch_bounds__(256) k_solve_small(const double* __restrict__ 
   double acc[NR];
 #pragma unroll
   for (int j = 0; j < NR; ++j) acc[j] = 0.0;
-  // 4 columns per lane per step, every S value and index loaded before the dependent u gathers:
+  // 8 columns per lane per step, every S value and index loaded before the dependent u gathers:
   // more loads in flight per warp on the HBM-bound S stream (the loop was load -> load chained)
   int c = lane;
-  for (; c + 96 < ne; c += 128) {
-    double sv[4];
-    int iv[4];
+  for (; c + 224 < ne; c += 256) {
+    double sv[8];
+    int iv[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 8; ++k) {
       sv[k] = __ldcs(Sr + c + 32 * k);  // S is read once per solve: stream it past L2
       iv[k] = __ldg(ie + c + 32 * k);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 8; ++k) {
       const double* uc = u + (long long)iv[k] * ldu;
 #pragma unroll
       for (int j = 0; j < NR; ++j) acc[j] = fma(sv[k], uc[j], acc[j]);
