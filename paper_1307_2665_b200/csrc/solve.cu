@@ -24,27 +24,23 @@ __global__ void __launch_bounds__(256) k_solve_small(const double* __restrict__ 
   for (int j = 0; j < NR; ++j) acc[j] = 0.0;
   // 8 columns per lane per step, every S value and index loaded before the dependent u gathers:
   // more loads in flight per warp on the HBM-bound S stream (the loop was load -> load chained)
-  int c = lane;
-  for (; c + 224 < ne; c += 256) {
+  for (int c = lane; c < ne; c += 256) {  // predicated: short rows (ne < 256) take one pass
     double sv[8];
     int iv[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      sv[k] = __ldcs(Sr + c + 32 * k);  // S is read once per solve: stream it past L2
-      iv[k] = __ldg(ie + c + 32 * k);
+      const bool ok = c + 32 * k < ne;
+      sv[k] = ok ? __ldcs(Sr + c + 32 * k) : 0.0;  // S is read once per solve: stream it past L2
+      iv[k] = ok ? __ldg(ie + c + 32 * k) : -1;
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const double* uc = u + (long long)iv[k] * ldu;
+      if (iv[k] >= 0) {
+        const double* uc = u + (long long)iv[k] * ldu;
 #pragma unroll
-      for (int j = 0; j < NR; ++j) acc[j] = fma(sv[k], uc[j], acc[j]);
+        for (int j = 0; j < NR; ++j) acc[j] = fma(sv[k], uc[j], acc[j]);
+      }
     }
-  }
-  for (; c < ne; c += 32) {
-    const double s = __ldcs(Sr + c);
-    const double* uc = u + (long long)__ldg(ie + c) * ldu;
-#pragma unroll
-    for (int j = 0; j < NR; ++j) acc[j] = fma(s, uc[j], acc[j]);
   }
 #pragma unroll
   for (int j = 0; j < NR; ++j) acc[j] = warp_sum(acc[j]);
