@@ -2,9 +2,9 @@
 
 Contract (driver-facing): `python bench.py --gpus N --steps K --warmup W [--impl reference]` prints
 ONE JSON line on rank 0. A "step" is one pass of the hot path: leaf stage -> every merge level ->
-one batched downward solve of b boundary vectors, on BASELINE.json configs[1] (config 2:
-variable-coefficient diffusion, 64x64 leaves, p = 16, b = 64). Other configs are available via
---config for exploration; the default line is config 2.
+one batched downward solve of b boundary vectors. The default workload is the largest BASELINE
+configuration that fits one B200: config 5 (convection-diffusion beta = 1000, 512 x 512 leaves,
+p = 16, 6.7e7 unknowns, b = 256; the north_star target problem). Other configs via --config.
 
 `value`    unknowns / (t_build + t_solve), inputs resident in HBM (coefficient samples of the
            leaf groups, boundary batch), CUDA events per step, L2 flushed (256 MB write)
@@ -14,10 +14,11 @@ variable-coefficient diffusion, 64x64 leaves, p = 16, b = 64). Other configs are
 `roofline` the dominant stage, measured live (CUDA events): achieved FP64 TFLOP/s vs the
            measured cuBLAS DGEMM peak (profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has no
            fp64 entry).
-`cpu_baseline` / --impl reference: the oracle port (numpy/scipy, LAPACK) of the reference
-           algorithm on this host, on a bounded sample: leaf stage on <=256 groups, one merge per
-           depth, one RHS solve sweep. Each is extrapolated to the full step exactly (every
-           depth is uniform).
+`cpu_baseline` / --impl reference: the reference's dense CPU path (the oracle port, numpy/scipy
+           LAPACK, all host cores; oracle/cpu_model.py). Configs 1-2 time whole steps
+           (`full_run`); larger ones a bounded sample extrapolated per depth (`Model`, labelled
+           "extrapolated": true; validated against whole runs by --validate-reference-model,
+           profiles/reference_model_validation_*.json).
 """
 
 from __future__ import annotations
@@ -30,7 +31,11 @@ import sys
 import threading
 import time
 
-import numpy as np
+# BLAS threads must be pinned before numpy is imported (OpenBLAS reads them once, at load time)
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+    os.environ.setdefault(_v, str(os.cpu_count()))
+
+import numpy as np  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
@@ -46,11 +51,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--levels", type=int, default=None, help="override L (exploration only)")
     ap.add_argument("--batch", type=int, default=None, help="override solve batch b")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="enqueue the build eagerly instead of replaying CUDA graphs")
+    ap.add_argument("--validate-reference-model", action="store_true",
+                    help="time whole oracle-port steps at configs 2 (L=6) and 3 (L=7) against the sampled model")
+    ap.add_argument("--full-reference", action="store_true",
+                    help="reference arm: time whole steps even above the default size limit")
     ap.add_argument("--force-distributed", action="store_true",
                     help="run the subtree/NCCL path even at world size 1 (plumbing check)")
     return ap.parse_args()
@@ -63,6 +72,27 @@ def fp64_peak():
         return float(d["fp64_tflops_burst"]), "measured cuBLAS DGEMM 8192^3 (profiles/fp64_peak_r01.json)"
     except Exception:
         return FP64_PEAK_FALLBACK, "measured cuBLAS DGEMM 8192^3, round 1 (constant in bench.py)"
+
+
+def traffic_from_profiles(workload, stage):
+    """DRAM read+write bytes per launch of a stage's dominant kernel, from the committed ncu
+    captures (profiles/*_ncu_*.json carrying "workload", "stage", "dram_bytes_per_launch"; the
+    latest file name wins). Returns (bytes or None, source)."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(HERE, "profiles", "*_ncu_*.json"))):
+        try:
+            pj = json.load(open(path))
+        except Exception:
+            continue
+        if pj.get("workload") == workload and pj.get("stage") == stage and "dram_bytes_per_launch" in pj:
+            best = (path, pj)
+    if best is None:
+        return None, None
+    path, pj = best
+    src = (f"profiles/{os.path.basename(path)}: dram read+write per launch of {pj.get('kernel')} (ncu --set full; "
+           f"{pj.get('gpu_time_ms', float('nan')):.3f} ms); algorithmic {pj.get('algorithmic_bytes_per_launch', 0):.3g} B")
+    return float(pj["dram_bytes_per_launch"]), src
 
 
 def hbm_peak():
@@ -115,61 +145,42 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------------
-# CPU reference port (oracle) on a bounded sample
+# The reference's CPU path (oracle port) timed on this host: whole steps where they fit, else a
+# bounded sample extrapolated per depth (oracle/cpu_model.py)
 # ----------------------------------------------------------------------------------------------
-def cpu_reference_sample(cfg, L, b, q=16, max_groups=256):
-    """Seconds for one full step (build + b solves) of the oracle port, extrapolated from a
-    bounded sample. Returns (seconds, description)."""
-    from oracle import hps_oracle as O
-    from paper_1307_2665_b200 import problems
-    import scipy.linalg as sla
+L2_NOTE = ("GPU arm: 256 MB L2 flush between timed steps, outside the step events; "
+           "the same workload on both arms")
+FULL_STEP_MAX_L = 6  # configs 1-2 (<= ~45 s per step on 16 cores): whole steps are timed
 
-    co = problems.coefficients(cfg)
-    coeffs = {n: getattr(co, n) for n in O.COEFF_NAMES}
-    tree = O.build_tree((0.0, 1.0, 0.0, 1.0), L, q)
-    geom = O.Geometry(q, tree.leaf_width, tree.leaf_height)
-    fields = O.sample_coefficients(coeffs, tree, geom)
-    reps, gid = O.group_leaves(fields, len(tree.leaves))
-    ng = len(reps)
-    k = min(ng, max_groups)
-    t0 = time.perf_counter()
-    Psi, Tg, cond = O.leaf_operators(geom, fields, reps[:k])
-    t_leaf = (time.perf_counter() - t0) * ng / k
-    # one merge per depth on congruent children (flop- and shape-identical to every merge there)
-    T_child = Tg[0]
-    t_merge = 0.0
-    S_depth = {}
-    for d in range(2 * L - 1, -1, -1):
-        box = (1 << d) - 1
-        a, c = tree.child_a[box], tree.child_b[box]
-        j1a, j2b, j3a, j3b = O.split_indices(tree.I_e[a], tree.I_e[c], tree.I_i[box])
-        t0 = time.perf_counter()
-        X = T_child[np.ix_(j3a, j3a)] - T_child[np.ix_(j3b, j3b)]
-        R = np.concatenate([-T_child[np.ix_(j3a, j1a)], T_child[np.ix_(j3b, j2b)]], axis=1)
-        lu = sla.lu_factor(X, check_finite=False)
-        S = sla.lu_solve(lu, R, check_finite=False)
-        n1 = j1a.size
-        T = np.zeros((n1 + j2b.size,) * 2)
-        T[:n1, :n1] = T_child[np.ix_(j1a, j1a)]
-        T[n1:, n1:] = T_child[np.ix_(j2b, j2b)]
-        T += np.concatenate([T_child[np.ix_(j1a, j3a)], T_child[np.ix_(j2b, j3b)]]) @ S
-        t_merge += (time.perf_counter() - t0) * (1 << d)
-        S_depth[d] = S
-        T_child = T
-    # one RHS sweep over every box (the reference solve is single-RHS, solver.py:298-299)
-    u = np.zeros(tree.points.shape[0])
-    u[tree.I_e[0]] = 1.0
-    t0 = time.perf_counter()
-    for bx in range(tree.n_boxes):
-        if tree.child_a[bx] < 0:
-            continue
-        d = int(np.floor(np.log2(bx + 1)))
-        u[tree.I_i[bx]] = S_depth[d] @ u[tree.I_e[bx]]
-    t_solve = (time.perf_counter() - t0) * b
-    desc = (f"oracle port (numpy/scipy LAPACK, {os.environ.get('OMP_NUM_THREADS', 'all')} BLAS threads): "
-            f"leaf stage on {k}/{ng} groups, 1 merge per depth x 2^d, 1-RHS sweep x {b}; "
-            f"extrapolated t_leaf={t_leaf:.2f}s t_merge={t_merge:.2f}s t_solve={t_solve:.2f}s")
-    return t_leaf + t_merge + t_solve, desc
+
+class CpuReference:
+    def __init__(self, cfg, L, b, q=16, full=None):
+        from oracle import cpu_model as M
+        self.M, self.cfg, self.L, self.b, self.q = M, cfg, L, b, q
+        self.full = (L <= FULL_STEP_MAX_L) if full is None else full
+        self.model = None if self.full else M.Model(cfg, L, b, q)
+
+    def step(self):
+        """Seconds of one reference step (build + b single-RHS solves), and its breakdown."""
+        if self.full:
+            return self.M.full_run(self.cfg, self.L, self.b, self.q)
+        return self.model.measure()
+
+    def describe(self, brk):
+        info = self.M.host_info()
+        cores = int(info["openblas_threads"] or os.cpu_count())
+        if self.full:
+            desc = (f"whole steps of the oracle port (numpy/scipy LAPACK, reference solver.py:250-316): leaf stage, "
+                    f"every merge, {self.b} single-RHS sweeps; t_leaf={brk['t_leaf_s']:.2f}s "
+                    f"t_merge={brk['t_merge_s']:.2f}s t_solve={brk['t_solve_s']:.2f}s")
+        else:
+            scaled = [d for d, h in brk["per_depth_how"].items() if h != "measured"]
+            desc = (f"bounded sample of the oracle port (numpy/scipy LAPACK), extrapolated per depth "
+                    f"(oracle/cpu_model.py): leaf stage on {brk['leaf_groups_timed']} groups; merges at every depth "
+                    f"measured (median of 3) except depths {','.join(scaled) or 'none'} (scaled by flops from two "
+                    f"depths below); 1-RHS sweep per depth over streaming S, x {self.b}; t_leaf={brk['t_leaf_s']:.2f}s "
+                    f"t_merge={brk['t_merge_s']:.2f}s t_solve={brk['t_solve_s']:.2f}s")
+        return cores, desc, info
 
 
 # ----------------------------------------------------------------------------------------------
@@ -188,25 +199,32 @@ def main():
     workload = f"cfg{cfg}_{c.name}_L{L}_p{q}_b{b}"
     metric = "HPS build and solve unknowns/s (fp64)"
 
+    if args.validate_reference_model:
+        from oracle import cpu_model as M
+        res = {"host": M.host_info(), "cases": M.validate()}
+        print(json.dumps(res))
+        return
+
     if args.impl == "reference":
         if rank != 0:
             return
-        cores = os.cpu_count()
-        os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-        times = []
-        desc = ""
+        ref = CpuReference(cfg, L, b, q, full=True if args.full_reference else None)
+        times, brk = [], {}
         for it in range(args.warmup + args.steps):
-            t, desc = cpu_reference_sample(cfg, L, b, q)
+            t, brk = ref.step()
             if it >= args.warmup:
                 times.append(t)
-        t = float(np.mean(times))
+        t = float(np.median(times))
         v = unknowns / t
+        cores, desc, info = ref.describe(brk)
         print(json.dumps({
             "impl": "reference", "metric": metric, "value": v, "unit": "unknowns/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "unknowns": unknowns, "batch": b},
-            "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": cores, "kind": "port", "sample": desc},
+            "config": {"workload": workload, "l2": L2_NOTE},
+            "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": cores, "kind": "port", "sample": desc,
+                             "extrapolated": not ref.full, "host": info,
+                             "steps_s": [float(x) for x in times], "breakdown": brk},
             "e2e": {"value": v, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
@@ -294,8 +312,7 @@ def main():
     stage_ms = {k: float(np.mean(v)) * 1e3 for k, v in stages.items()}
     dom = max(stage_ms, key=stage_ms.get)
     ach = stage_flops[dom] / (stage_ms[dom] / 1e3) / 1e12
-    leaf_kernel = "hps::k_leaf16v3" if q == 16 and os.environ.get("HPS_LEAF_V", "3") != "2" else (
-        "hps::k_leaf16" if q == 16 else "hps::k_leaf")
+    leaf_kernel = "hps::k_leaf16v3" if q == 16 else "hps::k_leaf"
     if dom == "leaf":
         kernels = leaf_kernel
     else:
@@ -311,24 +328,7 @@ def main():
     S_bytes = Wk.solve_S_bytes(L, q)
     hpeak, hsrc = hbm_peak()
     t_roof = Wk.build_roofline_seconds(L, q, inp.ngroups, peak, hpeak)
-    traffic, traffic_src = None, None  # DRAM bytes per launch of the dominant kernel (committed ncu capture)
-    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "leaf16v3_ncu_r01d.json")
-    gprof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "dgemm64_cfg3_d0_ncu_r01d.json")
-    if dom == "leaf" and leaf_kernel == "hps::k_leaf16v3" and os.path.exists(prof):
-        pj = json.load(open(prof))
-        if pj.get("workload") == workload:
-            traffic = float(pj["dram_bytes_per_launch"])
-            traffic_src = (f"profiles/leaf16v3_ncu_r01d.json: dram read+write per launch (ncu --set full); "
-                           f"algorithmic {pj['algorithmic_bytes_per_launch']:.3g} B")
-    elif dom == "merge_d0" and os.path.exists(gprof):
-        pj = json.load(open(gprof))
-        if pj.get("workload") == workload:  # the stage's dominant kernel: its T GEMM
-            g = pj["grouped_rasterisation"]
-            traffic = float(g["dram_bytes_per_launch"])
-            traffic_src = (f"profiles/dgemm64_cfg3_d0_ncu_r01d.json: dram read+write of the depth-0 T GEMM "
-                           f"({g['gpu_time_ms']:.2f} ms of the stage; DMMA pipe active "
-                           f"{pj['raw']['sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active']}); "
-                           f"algorithmic {pj['algorithmic_bytes_per_launch']:.3g} B")
+    traffic, traffic_src = traffic_from_profiles(workload, dom)
     roofline = {
         "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
         "traffic_source": traffic_src,
@@ -345,6 +345,8 @@ def main():
     # upload, the build, the H2D of the boundary data, the batched solve and the D2H of u. The
     # pipeline overlaps the host work of step i+1 with the device work of step i, and step i's
     # device work with step i+1's (two compute streams).
+    launch_mode = ("CUDA graphs (solver.BuildGraph: one per build stage + one for the solve)"
+                   if graph is not None else "eager")
     st = U = graph = None  # the device leg's captured state goes before the pipeline captures its own
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -353,7 +355,7 @@ def main():
     st = U = None
     # a stream of problems (about 2 s of device time, 4..20 problems): pipeline fill and drain are
     # inside the total; latency_s below is one problem alone
-    n_e2e = max(args.steps, min(20, max(4, int(2.0 / max(t_step, 1e-6)))))
+    n_e2e = min(20, max(3, int(2.0 / max(t_step, 1e-6))))
     for U, st in pipe.run([(co, pin_F)] * n_e2e):
         st = None
     st = U = None
@@ -393,21 +395,24 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
-        t_ref, desc = cpu_reference_sample(cfg, L, b, q)
-        cpu = {"value": unknowns / t_ref, "unit": "unknowns/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": desc}
+        ref = CpuReference(cfg, L, b, q, full=False)  # one bounded sample (whole steps are the reference arm's)
+        t_ref, brk = ref.step()
+        cores, desc, info = ref.describe(brk)
+        cpu = {"value": unknowns / t_ref, "unit": "unknowns/s", "cores": cores, "kind": "port", "sample": desc,
+               "extrapolated": True, "host": info}
     if rank == 0:
         print(json.dumps({
             "metric": metric, "value": value, "unit": "unknowns/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "unknowns": unknowns, "batch": b, "leaf_groups": inp.ngroups,
-                       "l2": "flushed (256 MB write) between timed steps, outside the step events",
-                       "launch": ("CUDA graphs (solver.BuildGraph: one per build stage + one for the solve)"
-                                  if graph is not None else "eager"),
+            "config": {"workload": workload, "l2": L2_NOTE},
+            "launch": launch_mode,
+            "stages": {"unknowns": unknowns, "batch": b, "leaf_groups": inp.ngroups,
                        "build_ms": tb * 1e3, "solve_ms": ts * 1e3,
-                       "build_unknowns_per_s": unknowns / tb, "solve_unknowns_per_s": unknowns * b / ts},
+                       "build_unknowns_per_s": unknowns / tb, "solve_unknowns_per_s": unknowns * b / ts,
+                       "build_fp64_tflops": roofline["build_tflops"], "build_fp64_frac": roofline["build_frac"],
+                       "solve_fp64_tflops": roofline["solve"]["tflops"], "solve_fp64_frac": roofline["solve"]["frac_fp64"],
+                       "solve_hbm_gbs": roofline["solve"]["gbs_S_stream"], "solve_hbm_frac": roofline["solve"]["frac_hbm"]},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_step": int(launches // args.steps), "clocks": clk}))
 
@@ -472,10 +477,9 @@ def bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, w
             "metric": metric, "value": unknowns / t_step, "unit": "unknowns/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "unknowns": unknowns, "batch": b,
-                       "parallelism": f"subtree split at depth {int(np.log2(world))}, NCCL send/recv for the top merges",
-                       "timing": "CUDA events around each step (ranks start together after a barrier), mean over K steps, max over ranks; inputs resident (sampled + uploaded once per rank)",
-                       "l2": "flushed (256 MB write) between timed steps, outside the step events"},
+            "config": {"workload": workload, "l2": L2_NOTE},
+            "parallelism": f"subtree split at depth {int(np.log2(world))}, NCCL send/recv for the top merges",
+            "timing": "CUDA events around each step (ranks start together after a barrier), mean over K steps, max over ranks; inputs resident (sampled + uploaded once per rank)",
             "gpu_launches": int(launches), "clocks": clk,
             "note": "e2e, roofline and cpu_baseline are reported on the N=1 line"}))
     dist.destroy_process_group()

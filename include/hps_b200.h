@@ -38,6 +38,25 @@ extern "C" {
 #define HPS_ERR_NCCL 4
 #define HPS_ERR_ARG 5
 
+/* Library context: owns the library's side streams (interface-inverse fork stream, look-ahead
+ * pair), their events, the split-K scratch and the tuning options of one device. Create one per
+ * device and per build in flight (two concurrent builds on two streams use two contexts). Calls
+ * taking a context are thread-compatible per context; the context's device must be current.
+ * hps_ctx_destroy synchronises its device and frees everything the context allocated. */
+typedef struct hps_ctx_s* hps_ctx_t;
+#define HPS_OPT_SPLITK 0            /* split-K of under-filled GEMMs (1); 0: every GEMM batch-invariant */
+#define HPS_OPT_GEMM_GROUP_M 1      /* grouped tile rasterisation of the 64x64 GEMM (16; 0 row-major) */
+#define HPS_OPT_INV_FORK 2          /* block-inverse GEMM pairs on the fork stream (1) */
+#define HPS_OPT_LEAF_CTAS_PER_SM 3  /* leaf kernel CTAs per SM (2) */
+#define HPS_OPT_LEAF_FREE_SMS 4     /* leaf grid sized for this many fewer SMs (0) */
+#define HPS_OPT_PROFILE_AHEAD 5     /* timing events around the look-ahead inverse (0; dev tool) */
+#define HPS_OPT_COUNT 6
+int hps_ctx_create(int device, hps_ctx_t* out);
+int hps_ctx_destroy(hps_ctx_t ctx);
+int hps_ctx_set_option(hps_ctx_t ctx, int option, long long value);
+long long hps_ctx_get_option(hps_ctx_t ctx, int option); /* -1 on a bad context or option */
+int hps_ctx_device(hps_ctx_t ctx);
+
 const char* hps_last_error(void);
 int hps_version(void);
 int hps_device_check(int* major, int* minor, int* sms);
@@ -53,9 +72,6 @@ long long hps_tree_sizes(int L, int q, long long* n3, long long* ne, long long* 
 int hps_tree_layout(int L, int q, double x_lo, double y_lo, double width, double height, const double* gauss01,
                     double* points, unsigned char* on_vertical, long long* leaf_cells, long long* leaf_I_e,
                     long long* const* Ie, long long* const* maps);
-/* Internal scratch set (split-K partial sums) used by this host thread's later enqueues: two
- * builds in flight at once on different streams must use different slots (0..3; default 0). */
-int hps_set_scratch_slot(int slot);
 
 /* Leaf stage for `ngroups` distinct coefficient groups (leaves with bitwise-equal samples share a
  * group, solver.py:208-222).
@@ -66,8 +82,8 @@ int hps_set_scratch_slot(int slot);
  *   idx        int32 J_i (ni), J_e (nb)
  * Outputs: Psi (ngroups x ni x nb), T (ngroups x 4p x 4p), cond (ngroups, probe estimate of
  * leafops.py:293-294; the caller raises LeafResonanceError if cond > 1e13). */
-size_t hps_leaf_workspace_bytes(int p, int ngroups);
-int hps_leaf_stage(int p, int ngroups, const double* const* fields, const double* scalars,
+size_t hps_leaf_workspace_bytes(hps_ctx_t ctx, int p, int ngroups); /* ctx NULL: default 148-SM context */
+int hps_leaf_stage(hps_ctx_t ctx, int p, int ngroups, const double* const* fields, const double* scalars,
                    const double* consts, const int* idx, double probe_max, double* Psi, double* T,
                    double* cond, void* ws, size_t ws_bytes, void* stream);
 
@@ -79,7 +95,7 @@ int hps_leaf_stage(int p, int ngroups, const double* const* fields, const double
  * the largest merge index whose interface system is singular or whose S is non-finite
  * (MergeResonanceError, merge.py:106-112). */
 size_t hps_merge_workspace_bytes(int nbatch, int n3, int ne);
-int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const double* T_child,
+int hps_merge_level(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, const double* T_child,
                     long long child_stride, const int* child_idx, const int* maps,
                     const double* vmode, double* S_out, double* T_out, void* ws, size_t ws_bytes,
                     int* status, int status_base, void* stream);
@@ -90,7 +106,7 @@ int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const double* T_ch
  * T GEMM; the call joins it before returning. The parent's call then passes pre_inverted = 1 (with
  * the same workspace) and skips its own X gather, deflation and inverse. pmaps = NULL: no
  * look-ahead. nbatch must be even when pmaps is set. */
-int hps_merge_level_ahead(int nbatch, int n3, int ne, int m, int q, const double* T_child,
+int hps_merge_level_ahead(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, const double* T_child,
                           long long child_stride, const int* child_idx, const int* maps, const double* vmode,
                           double* S_out, double* T_out, void* ws, size_t ws_bytes, int* status, int status_base,
                           int pre_inverted, const int* pmaps, int pn3, int pne, const double* pvmode, void* pws,
@@ -98,17 +114,17 @@ int hps_merge_level_ahead(int nbatch, int n3, int ne, int m, int q, const double
 
 /* u[ii_start0 + b*n3 + r, :nrhs] = sum_c S[b][r][c] * u[Ie[b][c], :nrhs] for all nbatch parents of
  * one depth; u is node-major with leading dimension ldu (solver.py:312-315). */
-int hps_solve_level(int nbatch, int n3, int ne, const double* S, const int* Ie, long long ii_start0,
+int hps_solve_level(hps_ctx_t ctx, int nbatch, int n3, int ne, const double* S, const int* Ie, long long ii_start0,
                     double* u, int ldu, int nrhs, void* stream);
 
 /* In-place inverse of `batch` n x n matrices (partial-pivoting Gauss-Jordan for n <= 128, recursive
  * 2x2 block inverse on the DMMA GEMM above that; n % 32 == 0 when n > 128). *status as above. */
 size_t hps_inverse_workspace_bytes(int n, int batch);
-int hps_inverse_batched(int n, int batch, double* X, long long lda, long long strideX, void* ws,
+int hps_inverse_batched(hps_ctx_t ctx, int n, int batch, double* X, long long lda, long long strideX, void* ws,
                         size_t ws_bytes, int* status, void* stream);
 
 /* C[b] = alpha A[b] B[b] + beta C[b]; optional B-row gather Bidx (NULL = none). K % 16 == 0. */
-int hps_dgemm_batched(int M, int N, int K, int batch, double alpha, const double* A, long long lda,
+int hps_dgemm_batched(hps_ctx_t ctx, int M, int N, int K, int batch, double alpha, const double* A, long long lda,
                       long long strideA, const double* B, long long ldb, long long strideB,
                       const int* Bidx, long long strideBidx, double beta, double* C, long long ldc,
                       long long strideC, void* stream);

@@ -22,11 +22,19 @@ HPS_ERR_NCCL = 4
 HPS_ERR_ARG = 5
 
 #: every symbol include/hps_b200.h declares (tests check the .so exports all of them)
-EXPORTS = ("hps_last_error", "hps_version", "hps_device_check", "hps_launch_count", "hps_leaf_workspace_bytes",
+EXPORTS = ("hps_ctx_create", "hps_ctx_destroy", "hps_ctx_set_option", "hps_ctx_get_option", "hps_ctx_device",
+           "hps_last_error", "hps_version", "hps_device_check", "hps_launch_count", "hps_leaf_workspace_bytes",
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
            "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched", "hps_leaf_hash",
            "hps_leaf_verify", "hps_leaf_fields", "hps_eval_points", "hps_gauge_sides", "hps_gauge_gather",
-           "hps_set_scratch_slot", "hps_merge_level_ahead", "hps_tree_sizes", "hps_tree_layout")
+           "hps_merge_level_ahead", "hps_tree_sizes", "hps_tree_layout")
+
+HPS_OPT_SPLITK = 0
+HPS_OPT_GEMM_GROUP_M = 1
+HPS_OPT_INV_FORK = 2
+HPS_OPT_LEAF_CTAS_PER_SM = 3
+HPS_OPT_LEAF_FREE_SMS = 4
+HPS_OPT_PROFILE_AHEAD = 5
 
 _lib = None
 
@@ -56,36 +64,44 @@ def load():
                                     ctypes.POINTER(ctypes.c_ubyte), pll, pll, ctypes.POINTER(pll),
                                     ctypes.POINTER(pll)]
     lib.hps_tree_layout.restype = c_int
-    lib.hps_set_scratch_slot.argtypes = [c_int]
-    lib.hps_set_scratch_slot.restype = c_int
+    lib.hps_ctx_create.argtypes = [c_int, ctypes.POINTER(c_dp)]
+    lib.hps_ctx_create.restype = c_int
+    lib.hps_ctx_destroy.argtypes = [c_dp]
+    lib.hps_ctx_destroy.restype = c_int
+    lib.hps_ctx_set_option.argtypes = [c_dp, c_int, c_ll]
+    lib.hps_ctx_set_option.restype = c_int
+    lib.hps_ctx_get_option.argtypes = [c_dp, c_int]
+    lib.hps_ctx_get_option.restype = c_ll
+    lib.hps_ctx_device.argtypes = [c_dp]
+    lib.hps_ctx_device.restype = c_int
     lib.hps_device_check.argtypes = [ctypes.POINTER(c_int)] * 3
     lib.hps_device_check.restype = c_int
-    lib.hps_leaf_workspace_bytes.argtypes = [c_int, c_int]
+    lib.hps_leaf_workspace_bytes.argtypes = [c_dp, c_int, c_int]
     lib.hps_leaf_workspace_bytes.restype = c_sz
-    lib.hps_leaf_stage.argtypes = [c_int, c_int, ctypes.POINTER(c_dp), ctypes.POINTER(c_d), c_dp, c_dp, c_d,
+    lib.hps_leaf_stage.argtypes = [c_dp, c_int, c_int, ctypes.POINTER(c_dp), ctypes.POINTER(c_d), c_dp, c_dp, c_d,
                                    c_dp, c_dp, c_dp, c_dp, c_sz, c_dp]
     lib.hps_leaf_stage.restype = c_int
     lib.hps_merge_workspace_bytes.argtypes = [c_int, c_int, c_int]
     lib.hps_merge_workspace_bytes.restype = c_sz
-    lib.hps_merge_level.argtypes = [c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp, c_dp,
+    lib.hps_merge_level.argtypes = [c_dp, c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp, c_dp,
                                     c_dp, c_sz, c_dp, c_int, c_dp]
     lib.hps_merge_level.restype = c_int
-    lib.hps_merge_level_ahead.argtypes = [c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp, c_dp,
+    lib.hps_merge_level_ahead.argtypes = [c_dp, c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp, c_dp,
                                           c_dp, c_sz, c_dp, c_int, c_int, c_dp, c_int, c_int, c_dp, c_dp, c_sz, c_dp,
                                           c_int, c_dp]
     lib.hps_merge_level_ahead.restype = c_int
-    lib.hps_debug_ahead_times.argtypes = [c_int, ctypes.POINTER(ctypes.c_float)]
+    lib.hps_debug_ahead_times.argtypes = [c_dp, c_int, ctypes.POINTER(ctypes.c_float)]
     lib.hps_debug_ahead_times.restype = c_int
-    lib.hps_debug_ahead_depth.argtypes = [c_int]
+    lib.hps_debug_ahead_depth.argtypes = [c_dp, c_int]
     lib.hps_debug_ahead_depth.restype = None
-    lib.hps_solve_level.argtypes = [c_int, c_int, c_int, c_dp, c_dp, c_ll, c_dp, c_int, c_int, c_dp]
+    lib.hps_solve_level.argtypes = [c_dp, c_int, c_int, c_int, c_dp, c_dp, c_ll, c_dp, c_int, c_int, c_dp]
     lib.hps_solve_level.restype = c_int
-    lib.hps_dgemm_batched.argtypes = [c_int, c_int, c_int, c_int, c_d, c_dp, c_ll, c_ll, c_dp, c_ll, c_ll, c_dp,
+    lib.hps_dgemm_batched.argtypes = [c_dp, c_int, c_int, c_int, c_int, c_d, c_dp, c_ll, c_ll, c_dp, c_ll, c_ll, c_dp,
                                       c_ll, c_d, c_dp, c_ll, c_ll, c_dp]
     lib.hps_dgemm_batched.restype = c_int
     lib.hps_inverse_workspace_bytes.argtypes = [c_int, c_int]
     lib.hps_inverse_workspace_bytes.restype = c_sz
-    lib.hps_inverse_batched.argtypes = [c_int, c_int, c_dp, c_ll, c_ll, c_dp, c_sz, c_dp, c_dp]
+    lib.hps_inverse_batched.argtypes = [c_dp, c_int, c_int, c_dp, c_ll, c_ll, c_dp, c_sz, c_dp, c_dp]
     lib.hps_inverse_batched.restype = c_int
     lib.hps_leaf_hash.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_dp), c_dp, c_dp]
     lib.hps_leaf_hash.restype = c_int
@@ -102,6 +118,53 @@ def load():
     lib.hps_gauge_gather.restype = c_int
     _lib = lib
     return lib
+
+
+class Context:
+    """An hps_ctx_t (include/hps_b200.h): the library's side streams, split-K scratch and options
+    for one device. Two builds in flight at once use two contexts."""
+
+    def __init__(self, device_index, **options):
+        lib = load()
+        h = c_dp()
+        check(lib.hps_ctx_create(int(device_index), ctypes.byref(h)), "hps_ctx_create")
+        self.handle = h
+        self.device_index = int(device_index)
+        for k, v in options.items():
+            self.set(k, v)
+
+    def set(self, name, value):
+        opt = globals()["HPS_OPT_" + name.upper()]
+        check(load().hps_ctx_set_option(self.handle, opt, int(value)), "hps_ctx_set_option")
+
+    def get(self, name):
+        return int(load().hps_ctx_get_option(self.handle, globals()["HPS_OPT_" + name.upper()]))
+
+    def close(self):
+        if self.handle is not None and self.handle.value:
+            load().hps_ctx_destroy(self.handle)
+        self.handle = None
+
+    _as_parameter_ = property(lambda self: self.handle)
+
+
+_contexts = {}
+
+
+def context(slot=0, device=None):
+    """The shared context `slot` of a device (default: the current CUDA device). Slot k is what a
+    k-th concurrent build stream uses (solver.Pipeline); created on first use, kept for the
+    process lifetime."""
+    import torch
+
+    dev = None if device is None else torch.device(device).index
+    dev = torch.cuda.current_device() if dev is None else dev
+    key = (dev, slot)
+    c = _contexts.get(key)
+    if c is None:
+        require_device()
+        c = _contexts[key] = Context(dev)
+    return c
 
 
 def last_error():

@@ -474,7 +474,9 @@ __global__ void __launch_bounds__(128, MINB) dgemm64_kernel(GemmParams p) {
 // C[b] = alpha * sum_s P[b][s] + beta * C[b], deterministic summation order.
 __global__ void k_splitk_reduce(GemmParams p);
 
-// Launch with a tile shape picked from the problem size. Returns HPS_OK or an error code.
-int dgemm_launch(const GemmParams& p, cudaStream_t stream);
+// Launch with a tile shape picked from the problem size (split-K scratch and options from the
+// context). Returns HPS_OK or an error code.
+struct Ctx;
+int dgemm_launch(const GemmParams& p, Ctx& cx, cudaStream_t stream);
 
 }  // namespace hps

@@ -1,5 +1,4 @@
-// Shared declarations of the leaf-stage kernels (leaf.cu: generic p and the v2 p=16 kernel;
-// leaf3.cu: the v3 p=16 kernel).
+// Shared declarations of the leaf-stage kernels (leaf.cu: generic p; leaf3.cu: the p = 16 kernel).
 #pragma once
 #include "common.cuh"
 
@@ -21,9 +20,10 @@ struct LeafArgs {
   long long scratch_stride;  // doubles per CTA slot
 };
 
-// p = 16, v3: GE with look-ahead (leaf3.cu). scratch_stride is set by the launcher.
+// p = 16: blocked LU with warp-specialised panels (leaf3.cu). scratch_stride is set by the launcher.
+struct Ctx;
 size_t leaf16v3_scratch_doubles();
-int leaf16v3_grid(int ngroups);
-int launch_leaf16v3(LeafArgs& a, cudaStream_t st);
+int leaf16v3_grid(const Ctx& cx, int ngroups);
+int launch_leaf16v3(LeafArgs& a, Ctx& cx, cudaStream_t st);
 
 }  // namespace hps

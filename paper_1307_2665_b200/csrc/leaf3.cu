@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "ctx.cuh"
 #include "leaf.cuh"
 
 namespace hps {
@@ -637,15 +638,11 @@ extern "C" int hps_debug_leaf3_profile(long long* out, int reset) {
 
 size_t leaf16v3_scratch_doubles() { return (size_t)l3::MROWS * l3::LDM + (size_t)l3::NPANEL * 256; }
 
-int leaf16v3_grid(int ngroups) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  static int per_sm = getenv("HPS_LEAF3_CTAS_PER_SM") ? atoi(getenv("HPS_LEAF3_CTAS_PER_SM")) : 2;
-  // HPS_LEAF_FREE_SMS: size the grid for that many fewer SMs (experiment: SMs left to a concurrent
-  // stream's merges in solver.Pipeline)
-  static int free_sms = getenv("HPS_LEAF_FREE_SMS") ? atoi(getenv("HPS_LEAF_FREE_SMS")) : 0;
-  sms = std::max(1, sms - free_sms);
+int leaf16v3_grid(const Ctx& cx, int ngroups) {
+  // HPS_OPT_LEAF_FREE_SMS: size the grid for that many fewer SMs (experiment: SMs left to a
+  // concurrent stream's merges in solver.Pipeline)
+  const int per_sm = (int)std::max(1LL, cx.opt[HPS_OPT_LEAF_CTAS_PER_SM]);
+  const int sms = std::max(1, cx.sms - (int)cx.opt[HPS_OPT_LEAF_FREE_SMS]);
   // the smallest grid with the same leaves per CTA as a full one: the grid-stride loop's critical
   // path is unchanged, and the spare CTA slots let other streams' small kernels (the next
   // problem's grouping in solver.Pipeline) run beside the leaf stage (cfg2: 293 of 296)
@@ -654,14 +651,11 @@ int leaf16v3_grid(int ngroups) {
   return std::max(1, (ngroups + per_cta - 1) / per_cta);
 }
 
-int launch_leaf16v3(LeafArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(k_leaf16v3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l3::SMEM));
-    attr = true;
-  }
+int launch_leaf16v3(LeafArgs& a, Ctx& cx, cudaStream_t st) {
+  const int as = ensure_smem_attr((const void*)k_leaf16v3, cx.device, (int)l3::SMEM);
+  if (as != HPS_OK) return as;
   a.scratch_stride = (long long)leaf16v3_scratch_doubles();
-  k_leaf16v3<<<leaf16v3_grid(a.ngroups), l3::THREADS, l3::SMEM, st>>>(a);
+  k_leaf16v3<<<leaf16v3_grid(cx, a.ngroups), l3::THREADS, l3::SMEM, st>>>(a);
   HPS_LAUNCH_CHECK();
   return HPS_OK;
 }

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "ctx.cuh"
 #include "gemm.cuh"
 
 namespace hps {
@@ -208,134 +209,9 @@ __device__ __forceinline__ double vvt(int r, int c, int q, int nseg, const doubl
   return 0.0;
 }
 
-// Gauss-Jordan inverse with partial pivoting for n <= 32*RPL (one CTA of W warps per matrix).
-// Layout: warp w owns columns [w*CPW, (w+1)*CPW); lane l owns rows l + 32*i (i < RPL). The whole
-// matrix lives in registers. One __syncthreads per pivot step:
-//   * column k (already updated) sits in a double-buffered shared vector; EVERY warp computes the
-//     same argmax over the unused rows from it, so no broadcast barrier is needed;
-//   * the pivot row reaches the lanes of each warp by shuffles, since it holds that warp's columns;
-//   * after its rank-1 update, the warp that owns column k+1 publishes it for the next step.
-// Pivoting is implicit (no row swaps): row p_k is eliminated at step k and the in-place result B
-// satisfies inv(X)[k][p_j] = B[p_k][j]; the write-out applies that permutation.
-template <int RPL, int CPW, int W>
-__global__ void __launch_bounds__(W * 32) k_gj_inverse(double* X, long long lda, long long strideX, int n,
-                                                      int* status, int status_base) {
-  constexpr int NMAX = 32 * RPL;
-  __shared__ double colbuf[2][NMAX];
-  __shared__ int pivrow[NMAX];
-  __shared__ int rowstep[NMAX];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b = blockIdx.x;
-  double* Xb = X + (long long)b * strideX;
-  const int cbase = warp * CPW;
-  double a[RPL][CPW];
-  bool used[RPL];
-#pragma unroll
-  for (int i = 0; i < RPL; ++i) {
-    const int r = lane + 32 * i;
-    used[i] = r >= n;
-#pragma unroll
-    for (int j = 0; j < CPW; ++j) {
-      const int c = cbase + j;
-      a[i][j] = (r < n && c < n) ? Xb[(long long)r * lda + c] : 0.0;
-    }
-  }
-  // publish column 0
-  if (warp == 0) {
-#pragma unroll
-    for (int i = 0; i < RPL; ++i) colbuf[0][lane + 32 * i] = a[i][0];
-  }
-  __syncthreads();
-  bool singular = false;
-  for (int k = 0; k < n; ++k) {
-    const double* ck = colbuf[k & 1];
-    // argmax |col k| over the unused rows. Non-negative doubles order like their bit patterns, so
-    // three 32-bit warp reductions (REDUX) give the exact argmax with ties to the smallest row.
-    double cv[RPL];
-    unsigned long long bestkey = 0ull;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      cv[i] = ck[lane + 32 * i];
-      const unsigned long long key = used[i] ? 0ull : (unsigned long long)__double_as_longlong(fabs(cv[i]));
-      const int idx = used[i] ? 0x7fffffff : lane + 32 * i;
-      if (key > bestkey || (key == bestkey && idx < bi)) { bestkey = key; bi = idx; }
-    }
-    const unsigned hi = (unsigned)(bestkey >> 32), lo = (unsigned)bestkey;
-    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-    const int p = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)bi : 0xffffffffu);
-    const int pl = p & 31, pi = p >> 5;
-    const double piv = ck[p];
-    singular |= (piv == 0.0);
-    const double inv = fast_rcp(piv);
-    if (threadIdx.x == 0) { pivrow[k] = p; rowstep[p] = k; }
-    // pivot row for this warp's columns (pi is warp-uniform: a uniform branch, no selects)
-    double rp[CPW];
-#pragma unroll
-    for (int i = 0; i < RPL; ++i)
-      if (pi == i) {
-        if (lane == pl) used[i] = true;
-#pragma unroll
-        for (int j = 0; j < CPW; ++j) rp[j] = __shfl_sync(0xffffffffu, a[i][j], pl) * inv;
-      }
-    // column k: the owning warp zeroes it and sets its "pivot row" entry to inv, so the common
-    // update below yields -f*inv in column k and inv at the pivot position.
-    const int kw = k / CPW;
-    if (warp == kw) {
-      const int kj = k - kw * CPW;
-#pragma unroll
-      for (int j = 0; j < CPW; ++j)
-        if (j == kj) {
-          rp[j] = inv;
-#pragma unroll
-          for (int i = 0; i < RPL; ++i) a[i][j] = 0.0;
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const double f = cv[i];
-      if (pi == i) {  // the slot holding the pivot row (one lane) takes rp itself
-        const bool prow = (lane == pl);
-#pragma unroll
-        for (int j = 0; j < CPW; ++j) {
-          const double v = fma(-f, rp[j], a[i][j]);
-          a[i][j] = prow ? rp[j] : v;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < CPW; ++j) a[i][j] = fma(-f, rp[j], a[i][j]);
-      }
-    }
-    // publish column k+1 (after this step's update) for the next step
-    if (k + 1 < n && warp == (k + 1) / CPW) {
-      const int j1 = (k + 1) - warp * CPW;
-#pragma unroll
-      for (int j = 0; j < CPW; ++j)
-        if (j == j1) {
-#pragma unroll
-          for (int i = 0; i < RPL; ++i) sts64(&colbuf[(k + 1) & 1][lane + 32 * i], a[i][j]);
-        }
-    }
-    __syncthreads();
-  }
-  // inv(X)[rowstep[r]][pivrow[c]] = B[r][c]
-#pragma unroll
-  for (int i = 0; i < RPL; ++i) {
-    const int r = lane + 32 * i;
-    if (r >= n) continue;
-    const long long orow = (long long)rowstep[r] * lda;
-#pragma unroll
-    for (int j = 0; j < CPW; ++j) {
-      const int c = cbase + j;
-      if (c < n) Xb[orow + pivrow[c]] = a[i][j];
-    }
-  }
-  if (singular && status && threadIdx.x == 0) atomicMax(status, status_base + b);
-}
-
-// Blocked Gauss-Jordan inverse (n <= 8*NT), same pivoting rule as k_gj_inverse (partial pivoting,
-// ties to the smallest row, implicit row order), built for a short critical path:
+// Blocked Gauss-Jordan inverse (n <= 8*NT) with partial pivoting (ties to the smallest row; implicit
+// row order: row p_k is eliminated at step k and inv(X)[k][p_j] = B[p_k][j] in the in-place result
+// B, the write-out applies that permutation), built for a short critical path:
 //  * the matrix lives in registers in DMMA C-fragment layout: warp w owns columns 16w..16w+15,
 //    lane (g, tq) holds a[r][c][h] = A(8r + g, 16w + 8c + 2tq + h);
 //  * pivots go in blocks of 8 (one 8-column tile). The warp owning the tile factors it alone
@@ -720,55 +596,30 @@ __global__ void k_deflate(double* X, int n, int q, const double* __restrict__ vs
   }
 }
 
-// In-place batched inverse of n x n blocks (n <= 128), stride lda.
-// reserve_sm: the look-ahead inverse runs beside a full-GPU GEMM. Its Gauss-Jordan CTAs are chains
-// of dependent FP64 operations, which slow down sharply when GEMM CTAs on the same SM keep the FP64
-// pipe busy; padding the launch with unused dynamic shared memory keeps GEMM CTAs off those SMs.
-template <int NT>
-static int launch_gj(double* X, long long lda, long long strideX, int n, int batch, int* status, int status_base,
-                     bool reserve_sm, cudaStream_t st) {
-  static const int pad_kb = getenv("HPS_GJ_RESERVE_KB") ? atoi(getenv("HPS_GJ_RESERVE_KB")) : 160;
-  static bool attr = false;
-  const int pad = reserve_sm ? pad_kb * 1024 : 0;
-  if (pad && !attr) {
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(k_gj_blk<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
-    attr = true;
-  }
-  k_gj_blk<NT><<<batch, NT * 16, pad, st>>>(X, lda, strideX, n, status, status_base);
-  HPS_LAUNCH_CHECK();
-  return HPS_OK;
-}
-
+// In-place batched inverse of n x n blocks (n <= 128), stride lda: blocked Gauss-Jordan.
 static int inverse_small(double* X, long long lda, long long strideX, int n, int batch, int* status,
-                         int status_base, cudaStream_t st, bool reserve_sm = false) {
+                         int status_base, cudaStream_t st) {
   if (n > 128) {
     set_error("inverse_small: n=%d > 128", n);
     return HPS_ERR_ARG;
   }
-  static const int v = getenv("HPS_GJ_V") ? atoi(getenv("HPS_GJ_V")) : 3;
-  if (v == 3) {  // blocked GJ (8-pivot panels, DMMA block updates)
-    if (n <= 16) return launch_gj<2>(X, lda, strideX, n, batch, status, status_base, reserve_sm, st);
-    if (n <= 32) return launch_gj<4>(X, lda, strideX, n, batch, status, status_base, reserve_sm, st);
-    if (n <= 64) return launch_gj<8>(X, lda, strideX, n, batch, status, status_base, reserve_sm, st);
-    return launch_gj<16>(X, lda, strideX, n, batch, status, status_base, reserve_sm, st);
-  }
   if (n <= 16)
-    k_gj_inverse<1, 8, 2><<<batch, 64, 0, st>>>(X, lda, strideX, n, status, status_base);
+    k_gj_blk<2><<<batch, 32, 0, st>>>(X, lda, strideX, n, status, status_base);
   else if (n <= 32)
-    k_gj_inverse<1, 8, 4><<<batch, 128, 0, st>>>(X, lda, strideX, n, status, status_base);
+    k_gj_blk<4><<<batch, 64, 0, st>>>(X, lda, strideX, n, status, status_base);
   else if (n <= 64)
-    k_gj_inverse<2, 8, 8><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
+    k_gj_blk<8><<<batch, 128, 0, st>>>(X, lda, strideX, n, status, status_base);
   else
-    k_gj_inverse<4, 16, 8><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
+    k_gj_blk<16><<<batch, 256, 0, st>>>(X, lda, strideX, n, status, status_base);
   HPS_LAUNCH_CHECK();
   return HPS_OK;
 }
 
-static int gemm(int M, int N, int K, int batch, double alpha, const double* A, long long lda, long long sA,
+static int gemm(Ctx& cx, int M, int N, int K, int batch, double alpha, const double* A, long long lda, long long sA,
                 const double* B, long long ldb, long long sB, double beta, double* C, long long ldc, long long sC,
                 cudaStream_t st, int* nonfinite = nullptr) {
   GemmParams p{M, N, K, batch, A, lda, sA, B, ldb, sB, nullptr, 0, C, ldc, sC, alpha, beta, nonfinite};
-  return dgemm_launch(p, st);
+  return dgemm_launch(p, cx, st);
 }
 
 #define HPS_TRY(x)            \
@@ -780,51 +631,12 @@ static int gemm(int M, int N, int K, int batch, double alpha, const double* A, l
 // Recursive 2x2 block inverse, in place, batched (all matrices n x n with leading dim lda).
 //   A11 <- inv(A11); T12 = A11 A12; T21 = A21 A11; A22 <- A22 - A21 T12; A22 <- inv(A22)
 //   A12 <- -T12 A22; A21 <- -A22 T21; A11 <- A11 - A12 T21
-// Base blocks (<= 128) use pivoted Gauss-Jordan in shared memory.
-// Side stream + event ring of the recursive inverse: the independent GEMM pairs of each level run
-// concurrently (fork/join through events; captured CUDA graphs get parallel branches).
-struct ForkCtx {
-  cudaStream_t side = nullptr;
-  cudaStream_t ahead = nullptr, ahead_side = nullptr;  // look-ahead inverse (highest priority)
-  cudaEvent_t ev[64];
-  int next = 0;
-  bool ok = false;
-};
-static ForkCtx& fork_ctx() {
-  static ForkCtx c;
-  static bool init = false;
-  if (!init) {
-    init = true;
-    c.ok = cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking) == cudaSuccess;
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    c.ok = c.ok && cudaStreamCreateWithPriority(&c.ahead, cudaStreamNonBlocking, hi) == cudaSuccess;
-    c.ok = c.ok && cudaStreamCreateWithPriority(&c.ahead_side, cudaStreamNonBlocking, hi) == cudaSuccess;
-    for (int i = 0; i < 64 && c.ok; ++i) c.ok = cudaEventCreateWithFlags(&c.ev[i], cudaEventDisableTiming) == cudaSuccess;
-    cudaGetLastError();
-  }
-  return c;
-}
-cudaStream_t fork_side_stream() { return fork_ctx().ok ? fork_ctx().side : nullptr; }
-// split-K scratch role of a stream: 0 the caller's, 1 the fork side stream, 2/3 the look-ahead pair
-int stream_role(cudaStream_t st) {
-  ForkCtx& c = fork_ctx();
-  if (!c.ok || st == nullptr) return 0;
-  return st == c.side ? 1 : st == c.ahead ? 2 : st == c.ahead_side ? 3 : 0;
-}
-
-static cudaEvent_t record_on(cudaStream_t st) {
-  ForkCtx& c = fork_ctx();
-  cudaEvent_t e = c.ev[c.next];
-  c.next = (c.next + 1) & 63;
-  cudaEventRecord(e, st);
-  return e;
-}
-
-static int inverse_rec(double* A, long long lda, long long strideA, int n, int batch, double* tmp, int* status,
-                       int status_base, cudaStream_t st, cudaStream_t side = nullptr, bool reserve_sm = false) {
-  static const int base = getenv("HPS_INV_BASE") ? atoi(getenv("HPS_INV_BASE")) : 128;
-  if (n <= base || n <= 16) return inverse_small(A, lda, strideA, n, batch, status, status_base, st, reserve_sm);
+// Base blocks (<= 128) use pivoted Gauss-Jordan in registers. The independent GEMM pairs of each
+// level run concurrently on the context's fork stream (fork/join through its event ring; captured
+// CUDA graphs get parallel branches).
+static int inverse_rec(Ctx& cx, double* A, long long lda, long long strideA, int n, int batch, double* tmp,
+                       int* status, int status_base, cudaStream_t st, cudaStream_t side = nullptr) {
+  if (n <= 128) return inverse_small(A, lda, strideA, n, batch, status, status_base, st);
   const int h = n / 2, h2 = n - h;  // unequal halves allowed (q = 21 gives n3 = 21 * 2^j)
   double* A11 = A;
   double* A12 = A + h;
@@ -834,24 +646,22 @@ static int inverse_rec(double* A, long long lda, long long strideA, int n, int b
   double* T21 = tmp + (long long)batch * h * h2;  // h2 x h
   double* deeper = T21 + (long long)batch * h * h2;
   const long long sT = (long long)h * h2;
-  static const int par = getenv("HPS_INV_FORK") ? atoi(getenv("HPS_INV_FORK")) : 1;
-  ForkCtx& fc = fork_ctx();
-  const bool fork = par && fc.ok;
-  if (!side) side = fc.side;
+  const bool fork = cx.opt[HPS_OPT_INV_FORK] && cx.streams_ok;
+  if (!side) side = cx.side;
   cudaStream_t s2 = fork ? side : st;
-  HPS_TRY(inverse_rec(A11, lda, strideA, h, batch, deeper, status, status_base, st, side, reserve_sm));
-  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(s2, record_on(st), 0));
+  HPS_TRY(inverse_rec(cx, A11, lda, strideA, h, batch, deeper, status, status_base, st, side));
+  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(s2, cx.record_on(st), 0));
   // T21 = A21 inv(A11) on the side stream, T12 = inv(A11) A12 and the Schur update on the main one
-  HPS_TRY(gemm(h2, h, h, batch, 1.0, A21, lda, strideA, A11, lda, strideA, 0.0, T21, h, sT, s2));
-  HPS_TRY(gemm(h, h2, h, batch, 1.0, A11, lda, strideA, A12, lda, strideA, 0.0, T12, h2, sT, st));
-  HPS_TRY(gemm(h2, h2, h, batch, -1.0, A21, lda, strideA, T12, h2, sT, 1.0, A22, lda, strideA, st));
-  HPS_TRY(inverse_rec(A22, lda, strideA, h2, batch, deeper, status, status_base, st, side, reserve_sm));
-  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(s2, record_on(st), 0));
+  HPS_TRY(gemm(cx, h2, h, h, batch, 1.0, A21, lda, strideA, A11, lda, strideA, 0.0, T21, h, sT, s2));
+  HPS_TRY(gemm(cx, h, h2, h, batch, 1.0, A11, lda, strideA, A12, lda, strideA, 0.0, T12, h2, sT, st));
+  HPS_TRY(gemm(cx, h2, h2, h, batch, -1.0, A21, lda, strideA, T12, h2, sT, 1.0, A22, lda, strideA, st));
+  HPS_TRY(inverse_rec(cx, A22, lda, strideA, h2, batch, deeper, status, status_base, st, side));
+  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(s2, cx.record_on(st), 0));
   // A21 = -inv(S) T21 on the side stream (after T21 there), A12 = -T12 inv(S) on the main one
-  HPS_TRY(gemm(h2, h, h2, batch, -1.0, A22, lda, strideA, T21, h, sT, 0.0, A21, lda, strideA, s2));
-  HPS_TRY(gemm(h, h2, h2, batch, -1.0, T12, h2, sT, A22, lda, strideA, 0.0, A12, lda, strideA, st));
-  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(st, record_on(s2), 0));  // join: T21 and A21 done
-  HPS_TRY(gemm(h, h, h2, batch, -1.0, A12, lda, strideA, T21, h, sT, 1.0, A11, lda, strideA, st));
+  HPS_TRY(gemm(cx, h2, h, h2, batch, -1.0, A22, lda, strideA, T21, h, sT, 0.0, A21, lda, strideA, s2));
+  HPS_TRY(gemm(cx, h, h2, h2, batch, -1.0, T12, h2, sT, A22, lda, strideA, 0.0, A12, lda, strideA, st));
+  if (fork) HPS_CUDA_CHECK(cudaStreamWaitEvent(st, cx.record_on(s2), 0));  // join: T21 and A21 done
+  HPS_TRY(gemm(cx, h, h, h2, batch, -1.0, A12, lda, strideA, T21, h, sT, 1.0, A11, lda, strideA, st));
   return HPS_OK;
 }
 
@@ -870,24 +680,24 @@ extern "C" size_t hps_merge_workspace_bytes(int nbatch, int n3, int ne) {
   return d * sizeof(double) + 256;
 }
 
-// HPS_AHEAD_PROFILE=1 (eager builds only, dev tool): timing events at the look-ahead fork (0), the
-// end of the parent inverse on the look-ahead stream (1), the end of the T GEMM (2) and the join
-// (3), per depth; hps_debug_ahead_times reads the elapsed times relative to event 0.
-static cudaEvent_t g_probe_ev[32][4];
-static int g_probe_depth = -1;
-static void ahead_probe(int k, cudaStream_t s) {
-  static const int on = getenv("HPS_AHEAD_PROFILE") ? atoi(getenv("HPS_AHEAD_PROFILE")) : 0;
-  if (!on || g_probe_depth < 0 || g_probe_depth >= 32) return;
-  cudaEvent_t& e = g_probe_ev[g_probe_depth][k];
+// HPS_OPT_PROFILE_AHEAD (eager builds only, dev tool): timing events at the look-ahead fork (0),
+// the end of the parent inverse on the look-ahead stream (1), the end of the T GEMM (2) and the
+// join (3), per depth; hps_debug_ahead_times reads the elapsed times relative to event 0.
+static void ahead_probe(Ctx& cx, int k, cudaStream_t s) {
+  if (!cx.opt[HPS_OPT_PROFILE_AHEAD] || cx.probe_depth < 0 || cx.probe_depth >= 32) return;
+  cudaEvent_t& e = cx.probe[cx.probe_depth][k];
   if (!e) cudaEventCreate(&e);
   cudaEventRecord(e, s);
 }
-extern "C" int hps_debug_ahead_times(int depth, float* out) {  // ms since the fork: inv end, T end, join
-  if (depth < 0 || depth >= 32 || !g_probe_ev[depth][0]) return 1;
-  for (int k = 1; k < 4; ++k) cudaEventElapsedTime(out + k - 1, g_probe_ev[depth][0], g_probe_ev[depth][k]);
+extern "C" int hps_debug_ahead_times(hps_ctx_t ctx, int depth, float* out) {  // ms since the fork
+  Ctx* cx = reinterpret_cast<Ctx*>(ctx);
+  if (!cx || depth < 0 || depth >= 32 || !cx->probe[depth][0]) return 1;
+  for (int k = 1; k < 4; ++k) cudaEventElapsedTime(out + k - 1, cx->probe[depth][0], cx->probe[depth][k]);
   return 0;
 }
-extern "C" void hps_debug_ahead_depth(int depth) { g_probe_depth = depth; }
+extern "C" void hps_debug_ahead_depth(hps_ctx_t ctx, int depth) {
+  if (ctx) reinterpret_cast<Ctx*>(ctx)->probe_depth = depth;
+}
 
 // Parent-depth look-ahead of hps_merge_level_ahead (see k_ahead_rows).
 struct AheadArgs {
@@ -900,7 +710,7 @@ struct AheadArgs {
   int pstatus_base;
 };
 
-static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const double* T_child, long long child_stride,
+static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, const double* T_child, long long child_stride,
                             const int* child_idx, const int* maps, const double* vmode, double* S_out, double* T_out,
                             void* ws, size_t ws_bytes, int* status, int status_base, bool pre_inverted,
                             const AheadArgs* ah, cudaStream_t st) {
@@ -937,13 +747,17 @@ static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const doub
       k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vmode, vmode + q, diagmax);
       HPS_LAUNCH_CHECK();
     }
-    HPS_TRY(inverse_rec(X, n3, (long long)n3 * n3, n3, nbatch, tmp, status, status_base, st));
+    HPS_TRY(inverse_rec(cx, X, n3, (long long)n3 * n3, n3, nbatch, tmp, status, status_base, st));
   }
-  HPS_TRY(gemm(n3, ne, n3, nbatch, 1.0, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, 0.0, S_out, ne,
+  HPS_TRY(gemm(cx, n3, ne, n3, nbatch, 1.0, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, 0.0, S_out, ne,
                (long long)n3 * ne, st, status));
   // nonfinite flag reports merge index; shift by status_base happens on the host side
-  ForkCtx& fc = fork_ctx();
-  const bool ahead = ah != nullptr && fc.ok && (nbatch % 2) == 0;
+  if (ah != nullptr && !(cx.streams_ok && (nbatch % 2) == 0)) {
+    // the caller would treat the parent's X as inverted: refuse instead of skipping silently
+    set_error("hps_merge_level_ahead: look-ahead needs an even nbatch (got %d) and the context's streams", nbatch);
+    return HPS_ERR_ARG;
+  }
+  const bool ahead = ah != nullptr;
   if (ahead) {
     // parent X from the pj3 rows / columns of this depth's T (before the T GEMM): gathered
     // operands in the parent workspace's R and C regions, X into its X region
@@ -965,7 +779,7 @@ static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const doub
     HPS_LAUNCH_CHECK();
     k_ahead_bg<<<dim3(P, (2 * n3 + 7) / 8), 256, 0, st>>>(S_out, n3, ne, pj3a, pj3b, pn3, Bg);
     HPS_LAUNCH_CHECK();
-    HPS_TRY(gemm(pn3, pn3, 2 * n3, P, 1.0, Ag, 2 * n3, (long long)pn3 * 2 * n3, Bg, pn3, (long long)2 * n3 * pn3,
+    HPS_TRY(gemm(cx, pn3, pn3, 2 * n3, P, 1.0, Ag, 2 * n3, (long long)pn3 * 2 * n3, Bg, pn3, (long long)2 * n3 * pn3,
                  1.0, pX, pn3, (long long)pn3 * pn3, st));
     const bool pdefl = pn3 > q;
     if (pdefl) {
@@ -974,18 +788,15 @@ static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const doub
       HPS_LAUNCH_CHECK();
     }
     // fork: deflate + invert the parent X on the high-priority look-ahead stream
-    ahead_probe(0, st);
-    HPS_CUDA_CHECK(cudaStreamWaitEvent(fc.ahead, record_on(st), 0));
+    ahead_probe(cx, 0, st);
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(cx.ahead, cx.record_on(st), 0));
     if (pdefl) {
-      k_deflate<<<dim3(P, pn3 / q), 256, 0, fc.ahead>>>(pX, pn3, q, ah->pvmode, ah->pvmode + q, pdiag);
+      k_deflate<<<dim3(P, pn3 / q), 256, 0, cx.ahead>>>(pX, pn3, q, ah->pvmode, ah->pvmode + q, pdiag);
       HPS_LAUNCH_CHECK();
     }
-    // HPS_GJ_RESERVE=1 pads the look-ahead Gauss-Jordan launches so no GEMM CTA shares their SMs:
-    // measured no faster (cfg2 13.45 vs 13.41-13.46 ms), so off by default
-    static const int reserve = getenv("HPS_GJ_RESERVE") ? atoi(getenv("HPS_GJ_RESERVE")) : 0;
-    HPS_TRY(inverse_rec(pX, pn3, (long long)pn3 * pn3, pn3, P, ptmp, ah->pstatus, ah->pstatus_base, fc.ahead,
-                        fc.ahead_side, reserve != 0));
-    ahead_probe(1, fc.ahead);
+    HPS_TRY(inverse_rec(cx, pX, pn3, (long long)pn3 * pn3, pn3, P, ptmp, ah->pstatus, ah->pstatus_base, cx.ahead,
+                        cx.ahead_side));
+    ahead_probe(cx, 1, cx.ahead);
   }
   {  // T = blkdiag(Ta[j1a, j1a], Tb[j2b, j2b]) + C S, the blkdiag read by the GEMM epilogue
     GemmParams gp{ne, ne, n3, nbatch, Cm, n3, (long long)ne * n3, S_out, ne, (long long)n3 * ne, nullptr, 0,
@@ -993,30 +804,32 @@ static int merge_level_impl(int nbatch, int n3, int ne, int m, int q, const doub
     gp.blk = ch;
     gp.blk_j1a = j1a;
     gp.blk_j2b = j2b;
-    HPS_TRY(dgemm_launch(gp, st));
+    HPS_TRY(dgemm_launch(gp, cx, st));
   }
-  if (ahead) ahead_probe(2, st);
-  if (ahead) HPS_CUDA_CHECK(cudaStreamWaitEvent(st, record_on(fc.ahead), 0));  // join
-  if (ahead) ahead_probe(3, st);
+  if (ahead) ahead_probe(cx, 2, st);
+  if (ahead) HPS_CUDA_CHECK(cudaStreamWaitEvent(st, cx.record_on(cx.ahead), 0));  // join
+  if (ahead) ahead_probe(cx, 3, st);
   return HPS_OK;
 }
 
-extern "C" int hps_merge_level(int nbatch, int n3, int ne, int m, int q, const double* T_child,
+extern "C" int hps_merge_level(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, const double* T_child,
                                long long child_stride, const int* child_idx, const int* maps, const double* vmode,
                                double* S_out, double* T_out, void* ws, size_t ws_bytes, int* status,
                                int status_base, void* stream) {
-  return merge_level_impl(nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, S_out, T_out, ws,
+  HPS_CTX(cx, ctx);
+  return merge_level_impl(*cx, nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, S_out, T_out, ws,
                           ws_bytes, status, status_base, false, nullptr, static_cast<cudaStream_t>(stream));
 }
 
-extern "C" int hps_merge_level_ahead(int nbatch, int n3, int ne, int m, int q, const double* T_child,
+extern "C" int hps_merge_level_ahead(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, const double* T_child,
                                      long long child_stride, const int* child_idx, const int* maps,
                                      const double* vmode, double* S_out, double* T_out, void* ws, size_t ws_bytes,
                                      int* status, int status_base, int pre_inverted, const int* pmaps, int pn3,
                                      int pne, const double* pvmode, void* pws, size_t pws_bytes, int* pstatus,
                                      int pstatus_base, void* stream) {
+  HPS_CTX(cx, ctx);
   AheadArgs ah{pmaps, pn3, pne, pvmode, pws, pws_bytes, pstatus, pstatus_base};
-  return merge_level_impl(nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, S_out, T_out, ws,
+  return merge_level_impl(*cx, nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, S_out, T_out, ws,
                           ws_bytes, status, status_base, pre_inverted != 0, pmaps ? &ah : nullptr,
                           static_cast<cudaStream_t>(stream));
 }
@@ -1027,12 +840,13 @@ extern "C" size_t hps_inverse_workspace_bytes(int n, int batch) {
   return inverse_rec_tmp_doubles(n, batch) * sizeof(double) + 256;
 }
 
-extern "C" int hps_inverse_batched(int n, int batch, double* X, long long lda, long long strideX, void* ws,
+extern "C" int hps_inverse_batched(hps_ctx_t ctx, int n, int batch, double* X, long long lda, long long strideX, void* ws,
                                    size_t ws_bytes, int* status, void* stream) {
   if (ws_bytes < hps_inverse_workspace_bytes(n, batch) || n <= 0) {
     set_error("hps_inverse_batched: bad arguments n=%d ws=%zu", n, ws_bytes);
     return HPS_ERR_ARG;
   }
-  return inverse_rec(X, lda, strideX, n, batch, static_cast<double*>(ws), status, 0,
+  HPS_CTX(cx, ctx);
+  return inverse_rec(*cx, X, lda, strideX, n, batch, static_cast<double*>(ws), status, 0,
                      static_cast<cudaStream_t>(stream));
 }

@@ -5,6 +5,7 @@
 // is a plain strided store. Large batches go through the DMMA GEMM (B-row gather). For
 // nrhs <= 8 a warp-per-row kernel streams S once (HBM-bound, like a batched GEMV).
 #include "common.cuh"
+#include "ctx.cuh"
 #include "gemm.cuh"
 
 namespace hps {
@@ -57,8 +58,9 @@ __global__ void __launch_bounds__(256) k_solve_small(const double* __restrict__ 
 
 using namespace hps;
 
-extern "C" int hps_solve_level(int nbatch, int n3, int ne, const double* S, const int* Ie, long long ii_start0,
+extern "C" int hps_solve_level(hps_ctx_t ctx, int nbatch, int n3, int ne, const double* S, const int* Ie, long long ii_start0,
                                double* u, int ldu, int nrhs, void* stream) {
+  HPS_CTX(cx, ctx);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (nbatch <= 0 || nrhs <= 0) return HPS_OK;
   if (nrhs > ldu) {
@@ -80,5 +82,5 @@ extern "C" int hps_solve_level(int nbatch, int n3, int ne, const double* S, cons
   // GEMM: C = u rows [start0 + b*n3, +n3), A = S[b] (n3 x ne), B = u[Ie[b]] (ne x nrhs)
   GemmParams p{n3, nrhs, ne, nbatch, S, ne, (long long)n3 * ne, u, ldu, 0, Ie, ne,
                u + ii_start0 * ldu, ldu, (long long)n3 * ldu, 1.0, 0.0, nullptr};
-  return dgemm_launch(p, st);
+  return dgemm_launch(p, *cx, st);
 }

@@ -87,6 +87,7 @@ class CudaBackend:
         self.lay = layout_of(tree)
         self.geom = LeafGeometry.get(self.lay.q, tree.leaf_width, tree.leaf_height)
         self.dl = _DeviceLayout.get(self.lay, self.geom, self.device)
+        self.ctx = _native.context(device=self.device)
 
     # -- tensors / transport --
     def empty(self, shape):
@@ -119,9 +120,9 @@ class CudaBackend:
         Psi = self.empty((ngroups, ni, nb))
         T = self.empty((ngroups, ng, ng))
         cond = self.empty((ngroups,))
-        wsb = lib.hps_leaf_workspace_bytes(q, ngroups)
+        wsb = lib.hps_leaf_workspace_bytes(self.ctx, q, ngroups)
         ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
-        _native.check(lib.hps_leaf_stage(q, ngroups, fptr, scal, _native.ptr(self.dl.leaf_consts),
+        _native.check(lib.hps_leaf_stage(self.ctx, q, ngroups, fptr, scal, _native.ptr(self.dl.leaf_consts),
                                          _native.ptr(self.dl.leaf_idx), self.dl.probe_max, _native.ptr(Psi),
                                          _native.ptr(T), _native.ptr(cond), _native.ptr(ws), wsb,
                                          _native.stream_ptr()), "hps_leaf_stage")
@@ -152,7 +153,7 @@ class CudaBackend:
             self._ahead_ws = ((d - 1, nbatch // 2), pws)
         else:
             pargs = (None, 0, 0, None, None, 0, None, 0)
-        _native.check(lib.hps_merge_level_ahead(nbatch, dl.n3, dl.ne, dl.m, self.lay.q, _native.ptr(child_T),
+        _native.check(lib.hps_merge_level_ahead(self.ctx, nbatch, dl.n3, dl.ne, dl.m, self.lay.q, _native.ptr(child_T),
                                                 dl.m * dl.m, _native.ptr(idx), _native.ptr(self.dl.maps[d]),
                                                 _native.ptr(self.dl.vmode[d]), _native.ptr(S), _native.ptr(T),
                                                 _native.ptr(ws), wsb, _native.ptr(status), 0, int(pre), *pargs,
@@ -165,7 +166,7 @@ class CudaBackend:
         ldu = u.shape[1]
         Ie = self.dl.Ie[d][slot0:slot0 + nslots]
         start = int(self.lay.depth_off[d]) + slot0 * dl.n3
-        _native.check(self.lib.hps_solve_level(nslots, dl.n3, dl.ne, _native.ptr(S), _native.ptr(Ie), start,
+        _native.check(self.lib.hps_solve_level(self.ctx, nslots, dl.n3, dl.ne, _native.ptr(S), _native.ptr(Ie), start,
                                                _native.ptr(u), ldu, nrhs, _native.stream_ptr()), "hps_solve_level")
 
     def zeros(self, shape):

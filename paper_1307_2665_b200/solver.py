@@ -60,6 +60,30 @@ def _torch():
     return torch
 
 
+def _device_apply(A, x):
+    """A @ x for a device matrix A (m x k) and host x (k,) or (k, b), on the device (the library's
+    DGEMM): the operator containers never compute on the host."""
+    torch = _torch()
+    xv = np.asarray(x, dtype=float)
+    single = xv.ndim == 1
+    X = xv[:, None] if single else xv
+    m, k = A.shape
+    if X.shape[0] != k:
+        raise ValueError(f"operand has {X.shape[0]} rows, the operator {k} columns")
+    b = X.shape[1]
+    ld = -(-b // 2) * 2
+    Xd = torch.zeros((k, ld), dtype=torch.float64, device=A.device)
+    Xd[:, :b] = torch.from_numpy(np.ascontiguousarray(X)).to(A.device)
+    out = torch.empty((m, ld), dtype=torch.float64, device=A.device)
+    Ac = A.contiguous()
+    with torch.cuda.device(A.device):
+        _native.check(_native.load().hps_dgemm_batched(
+            _native.context(), m, ld, k, 1, 1.0, _native.ptr(Ac), k, 0, _native.ptr(Xd), ld, 0, None, 0, 0.0,
+            _native.ptr(out), ld, 0, _native.stream_ptr()), "hps_dgemm_batched")
+    r = out[:, :b].cpu().numpy()
+    return r[:, 0].copy() if single else r
+
+
 # ----------------------------------------------------------------------------------------------
 # Reference-shaped operator containers (solver.py:53-119), backed by device tensors
 # ----------------------------------------------------------------------------------------------
@@ -91,7 +115,7 @@ class DtnOperator:
         return t.shape[0]
 
     def apply(self, x):
-        return self.dense @ x
+        return _device_apply(self.device_tensor, x) if self.device_tensor is not None else self._host @ x
 
     def to_dense(self):
         return self.dense
@@ -122,7 +146,7 @@ class SolutionOperator:
         return True
 
     def apply(self, u_e):
-        return self.dense @ u_e
+        return _device_apply(self.device_tensor, u_e) if self.device_tensor is not None else self._host @ u_e
 
     def n_stored_entries(self):
         t = self.device_tensor if self.device_tensor is not None else self._host
@@ -504,10 +528,11 @@ def lookahead_depths(lay):
 
 
 def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_threshold=math.inf,
-                 hbs_leaf_size=64, stage_begin=None):
+                 hbs_leaf_size=64, stage_begin=None, ctx=None):
     """Enqueue the leaf stage and every merge level on the current stream (no host sync).
     `stage_begin(name)`, if given, is called before each stage ("leaf", "merge_d<d>"): BuildGraph
-    uses it to capture one CUDA graph per stage."""
+    uses it to capture one CUDA graph per stage. `ctx` is the library context (_native.Context;
+    default: slot 0 of the current device); builds in flight at the same time need different ones."""
     if stage_begin is not None:
         stage_begin("leaf")
     torch = _torch()
@@ -519,6 +544,7 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
     p2, ni, nb, ng = p * p, (p - 2) ** 2, 4 * (p - 1), 4 * p
     ngroups = inp.ngroups
     stream = _native.stream_ptr()
+    cx = ctx if ctx is not None else _native.context()
 
     # ---- leaf stage (solver.py:184-247) ----
     fptr = (ctypes_vp * 6)()
@@ -530,10 +556,10 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
     Psi = torch.empty((ngroups, ni, nb), dtype=torch.float64, device=device)
     Tleaf = torch.empty((ngroups, ng, ng), dtype=torch.float64, device=device)
     cond = torch.empty(ngroups, dtype=torch.float64, device=device)
-    wsb = lib.hps_leaf_workspace_bytes(p, ngroups)
+    wsb = lib.hps_leaf_workspace_bytes(cx, p, ngroups)
     ws = torch.empty(wsb, dtype=torch.uint8, device=device)
     mark = _marker(timeline, "leaf")
-    _native.check(lib.hps_leaf_stage(p, ngroups, fptr, scal, _native.ptr(dl.leaf_consts), _native.ptr(dl.leaf_idx),
+    _native.check(lib.hps_leaf_stage(cx, p, ngroups, fptr, scal, _native.ptr(dl.leaf_consts), _native.ptr(dl.leaf_idx),
                                      dl.probe_max, _native.ptr(Psi), _native.ptr(Tleaf), _native.ptr(cond),
                                      _native.ptr(ws), wsb, stream), "hps_leaf_stage")
     mark()
@@ -568,7 +594,7 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
             pwsb = lib.hps_merge_workspace_bytes(pl.n_boxes, pl.n3, pl.ne)
             ws_next = torch.empty(pwsb, dtype=torch.uint8, device=device)
             _native.check(lib.hps_merge_level_ahead(
-                nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride, _native.ptr(child_idx),
+                cx, nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride, _native.ptr(child_idx),
                 _native.ptr(dl.maps[d]), _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T), _native.ptr(ws),
                 wsb, status_d, 0, int(pre_inv), _native.ptr(dl.maps[d - 1]), pl.n3, pl.ne,
                 _native.ptr(dl.vmode[d - 1]), _native.ptr(ws_next), pwsb, ctypes_vp(status.data_ptr() + 4 * (d - 1)),
@@ -576,7 +602,7 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
             next_pre = True
         else:
             _native.check(lib.hps_merge_level_ahead(
-                nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride, _native.ptr(child_idx),
+                cx, nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride, _native.ptr(child_idx),
                 _native.ptr(dl.maps[d]), _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T), _native.ptr(ws),
                 wsb, status_d, 0, int(pre_inv), None, 0, 0, None, None, 0, None, 0, stream),
                 f"hps_merge_level(depth {d})")
@@ -673,11 +699,12 @@ def rhs_ld(b):
     return 1 if b == 1 else -(-b // 8) * 8
 
 
-def solve_device(state, F, out=None):
+def solve_device(state, F, out=None, ctx=None):
     """Device-resident batched solve. F: torch (|Gamma|, b) or (|Gamma|,) fp64 on the device, in
     root.I_e order. Returns U (N, ldu) on the device; columns [:b] are the solutions."""
     torch = _torch()
     lib = _native.load()
+    cx = ctx if ctx is not None else _native.context()
     lay = state.layout
     if F.dim() == 1:
         F = F[:, None]
@@ -694,7 +721,7 @@ def solve_device(state, F, out=None):
     for d in range(2 * lay.L):
         dl = lay.depths[d]
         nrhs = b if b <= 8 else ldu
-        _native.check(lib.hps_solve_level(dl.n_boxes, dl.n3, dl.ne, _native.ptr(state.S_levels[d]),
+        _native.check(lib.hps_solve_level(cx, dl.n_boxes, dl.n3, dl.ne, _native.ptr(state.S_levels[d]),
                                           _native.ptr(state.Ie_levels[d]), int(lay.depth_off[d]),
                                           _native.ptr(U), ldu, nrhs, stream), f"hps_solve_level(depth {d})")
     return U
@@ -798,21 +825,17 @@ class Pipeline:
                     if not Fh.is_pinned():
                         Fh = Fh.pin_memory()
                     Fd = Fh.to(self.device, non_blocking=True)
-                    multi = len(self._mains) > 1
-                    if multi:  # this job's split-K scratch set (its neighbour may still be running)
-                        _native.check(_native.load().hps_set_scratch_slot(sl), "hps_set_scratch_slot")
-                    try:
-                        g = self._graph_for(inp, Fd.shape[1], sl) if self.reuse_graphs else None
-                        if g is not None:
-                            g.load(inp, Fd)
-                            st = g.replay_build()
-                            U = g.replay_solve()
-                        else:
-                            st = build_device(inp)
-                            U = solve_device(st, Fd)
-                    finally:
-                        if multi:
-                            _native.load().hps_set_scratch_slot(0)
+                    # this job's library context (its own side streams and split-K scratch: the
+                    # neighbouring job on the other stream may still be running)
+                    cx = _native.context(sl if len(self._mains) > 1 else 0, self.device)
+                    g = self._graph_for(inp, Fd.shape[1], sl) if self.reuse_graphs else None
+                    if g is not None:
+                        g.load(inp, Fd)
+                        st = g.replay_build()
+                        U = g.replay_solve()
+                    else:
+                        st = build_device(inp, ctx=cx)
+                        U = solve_device(st, Fd, ctx=cx)
                     solved = torch.cuda.Event()
                     solved.record(main)
                 # results and status words come back on their own stream, so the next job's build
@@ -850,7 +873,7 @@ class Pipeline:
                 slot.clear()
             torch = _torch()
             try:
-                g = slot[key] = BuildGraph(inp, nrhs=nrhs, scratch_slot=sidx if len(self._mains) > 1 else 0)
+                g = slot[key] = BuildGraph(inp, nrhs=nrhs, ctx_slot=sidx if len(self._mains) > 1 else 0)
             except torch.OutOfMemoryError:  # two captured states do not fit: stay eager from here on
                 slot.clear()
                 self._graphs = [{} for _ in range(4)]
@@ -889,13 +912,13 @@ class BuildGraph:
 
     _warmed = set()
 
-    def __init__(self, inp, nrhs=0, scratch_slot=0):
+    def __init__(self, inp, nrhs=0, ctx_slot=0):
         torch = _torch()
         lib = _native.load()
-        # the library's split-K scratch set this capture bakes in (two graphs replayed at once on two
-        # streams need different slots, see Pipeline(streams=2))
-        self.scratch_slot = int(scratch_slot)
-        _native.check(lib.hps_set_scratch_slot(self.scratch_slot), "hps_set_scratch_slot")
+        # the library context (side streams, split-K scratch) this capture bakes in: two graphs
+        # replayed at once on two streams need different ones, see Pipeline(streams=2)
+        self.ctx_slot = int(ctx_slot)
+        self.ctx = _native.context(self.ctx_slot, inp.device)
         self.torch = torch
         self.layout, self.ngroups, self.scalars = inp.layout, inp.ngroups, tuple(inp.scalars)
         self._present = tuple(t is not None for t in inp.fields_dev)
@@ -910,13 +933,13 @@ class BuildGraph:
         pool = torch.cuda.graph_pool_handle()
         self.stages = []
         n0 = lib.hps_launch_count()
-        key = (id(inp.layout), inp.ngroups, self._present, self.scalars, self.nrhs, self.scratch_slot)
+        key = (id(inp.layout), inp.ngroups, self._present, self.scalars, self.nrhs, self.ctx_slot)
         with torch.cuda.stream(side):
             if key not in BuildGraph._warmed:
                 # warm-up: lazy attributes and scratch sizes outside the capture (once per shape)
-                st = build_device(self._inp)
+                st = build_device(self._inp, ctx=self.ctx)
                 if self.nrhs:
-                    solve_device(st, self._F)
+                    solve_device(st, self._F, ctx=self.ctx)
                 del st
                 torch.cuda.synchronize()
                 torch.cuda.empty_cache()  # the warm-up state's memory (L=9: ~50 GB) back before the capture
@@ -939,7 +962,7 @@ class BuildGraph:
                 active[0] = self.stages[-1][1]
 
             try:
-                self.state = build_device(self._inp, stage_begin=begin_tracked)
+                self.state = build_device(self._inp, stage_begin=begin_tracked, ctx=self.ctx)
                 self.stages[-1][1].capture_end()
                 active[0] = None
                 self.solve_graph, self.U = None, None
@@ -947,7 +970,7 @@ class BuildGraph:
                     self.solve_graph = torch.cuda.CUDAGraph()
                     self.solve_graph.capture_begin(pool=pool, capture_error_mode="thread_local")
                     active[0] = self.solve_graph
-                    self.U = solve_device(self.state, self._F)
+                    self.U = solve_device(self.state, self._F, ctx=self.ctx)
                     self.solve_graph.capture_end()
                     active[0] = None
             except BaseException:
@@ -958,8 +981,6 @@ class BuildGraph:
                         pass
                 self.stages, self.state = [], None
                 raise
-            finally:
-                lib.hps_set_scratch_slot(0)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.launches = int(lib.hps_launch_count() - n0)
@@ -1028,12 +1049,10 @@ def apply_global_dtn(state, f):
     F[:, :b] = torch.from_numpy(np.ascontiguousarray(V)).to(state.device)
     out = torch.empty((n, ld), dtype=torch.float64, device=state.device)
     Tr = state.root_T.device_tensor
-    if n % 16 == 0:
-        _native.check(lib.hps_dgemm_batched(n, ld, n, 1, 1.0, _native.ptr(Tr), n, 0, _native.ptr(F), ld, 0, None, 0,
-                                            0.0, _native.ptr(out), ld, 0, _native.stream_ptr()), "hps_dgemm_batched")
-        r = out[:, :b].cpu().numpy()
-    else:  # tiny odd q: not a hot path
-        r = state.root_T.dense @ V
+    _native.check(lib.hps_dgemm_batched(_native.context(), n, ld, n, 1, 1.0, _native.ptr(Tr), n, 0, _native.ptr(F), ld,
+                                        0, None, 0, 0.0, _native.ptr(out), ld, 0, _native.stream_ptr()),
+                  "hps_dgemm_batched")
+    r = out[:, :b].cpu().numpy()
     return r[:, 0].copy() if single else r
 
 

@@ -19,7 +19,7 @@ def check_gemm():
     for (M, N, K, B) in [(64, 64, 16, 1), (96, 96, 16, 3), (256, 512, 128, 2), (1000, 130, 64, 1), (128, 128, 32, 200)]:
         A = rng.standard_normal((B, M, K)); Bm = rng.standard_normal((B, K, N)); C = rng.standard_normal((B, M, N))
         tA, tB, tC = (torch.from_numpy(x).cuda() for x in (A, Bm, C))
-        st = lib.hps_dgemm_batched(M, N, K, B, 0.5, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N, None, 0, 2.0,
+        st = lib.hps_dgemm_batched(_native.context(), M, N, K, B, 0.5, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N, None, 0, 2.0,
                                    _native.ptr(tC), N, M * N, _native.stream_ptr())
         _native.check(st, "gemm")
         ref = 0.5 * A @ Bm + 2.0 * C
@@ -29,7 +29,7 @@ def check_gemm():
     U = rng.standard_normal((500, N)); idx = rng.integers(0, 500, K).astype(np.int32); A = rng.standard_normal((M, K))
     C = np.zeros((M, N))
     tA, tU, tC, ti = torch.from_numpy(A).cuda(), torch.from_numpy(U).cuda(), torch.from_numpy(C).cuda(), torch.from_numpy(idx).cuda()
-    _native.check(lib.hps_dgemm_batched(M, N, K, 1, 1.0, _native.ptr(tA), K, 0, _native.ptr(tU), N, 0, _native.ptr(ti), 0, 0.0,
+    _native.check(lib.hps_dgemm_batched(_native.context(), M, N, K, 1, 1.0, _native.ptr(tA), K, 0, _native.ptr(tU), N, 0, _native.ptr(ti), 0, 0.0,
                                         _native.ptr(tC), N, 0, _native.stream_ptr()), "gemm gather")
     print(f"gemm gather rel {rel(tC.cpu().numpy(), A @ U[idx]):.2e}")
 

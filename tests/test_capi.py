@@ -33,8 +33,27 @@ def test_library_exports_every_declared_symbol():
 def test_workspace_queries_are_host_only():
     lib = _native.load()
     ni, nb = 14 * 14, 60
-    assert lib.hps_leaf_workspace_bytes(16, 1) >= ni * (ni + nb + 1) * 8
+    assert lib.hps_leaf_workspace_bytes(None, 16, 1) >= ni * (ni + nb + 1) * 8
     assert lib.hps_merge_workspace_bytes(4, 32, 128) >= 4 * (32 * 32 + 2 * 32 * 128) * 8
+
+
+def test_context_calls_reject_a_null_context():
+    lib = _native.load()
+    assert lib.hps_ctx_get_option(None, _native.HPS_OPT_SPLITK) == -1
+    assert lib.hps_ctx_set_option(None, _native.HPS_OPT_SPLITK, 0) == _native.HPS_ERR_ARG
+    assert lib.hps_ctx_device(None) == -1
+    assert lib.hps_ctx_destroy(None) == _native.HPS_OK
+    st = lib.hps_dgemm_batched(None, 4, 4, 16, 1, 1.0, None, 16, 0, None, 4, 0, None, 0, 0.0, None, 4, 0, None)
+    assert st == _native.HPS_ERR_ARG and "null hps_ctx_t" in _native.last_error()
+
+
+def test_library_has_no_environment_knobs():
+    """Settings live in the context (hps_ctx_set_option), not in getenv calls inside the library's
+    sources (the static CUDA runtime it links reads its own variables)."""
+    import glob
+    csrc = os.path.join(os.path.dirname(_native.__file__), "csrc")
+    for path in glob.glob(os.path.join(csrc, "*.cu")) + glob.glob(os.path.join(csrc, "*.cuh")):
+        assert "getenv(" not in open(path).read(), path
 
 
 def test_no_cpu_fallback():

@@ -23,7 +23,7 @@ def test_dgemm(M, N, K, B, alpha, beta):
     rng = np.random.default_rng(M + N + K)
     A, Bm, C = rng.standard_normal((B, M, K)), rng.standard_normal((B, K, N)), rng.standard_normal((B, M, N))
     tA, tB, tC = cuda(A), cuda(Bm), cuda(C)
-    _native.check(lib.hps_dgemm_batched(M, N, K, B, alpha, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N,
+    _native.check(lib.hps_dgemm_batched(_native.context(), M, N, K, B, alpha, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N,
                                         None, 0, beta, _native.ptr(tC), N, M * N, _native.stream_ptr()), "gemm")
     assert rel(tC.cpu().numpy(), alpha * A @ Bm + beta * C) < 1e-14
 
@@ -37,7 +37,7 @@ def test_dgemm_row_gather():
     A = rng.standard_normal((B, M, K))
     tA, tU, ti = cuda(A), cuda(U), cuda(idx)
     tC = torch.zeros((B, M, N), dtype=torch.float64, device="cuda")
-    _native.check(lib.hps_dgemm_batched(M, N, K, B, 1.0, _native.ptr(tA), K, M * K, _native.ptr(tU), N, 0,
+    _native.check(lib.hps_dgemm_batched(_native.context(), M, N, K, B, 1.0, _native.ptr(tA), K, M * K, _native.ptr(tU), N, 0,
                                         _native.ptr(ti), K, 0.0, _native.ptr(tC), N, M * N, _native.stream_ptr()), "g")
     want = np.stack([A[b] @ U[idx[b]] for b in range(B)])
     assert rel(tC.cpu().numpy(), want) < 1e-14
@@ -50,7 +50,7 @@ def test_dgemm_generic_shapes(M, N, K, B):
     rng = np.random.default_rng(M * N + K)
     A, Bm, C = rng.standard_normal((B, M, K)), rng.standard_normal((B, K, N)), rng.standard_normal((B, M, N))
     tA, tB, tC = cuda(A), cuda(Bm), cuda(C)
-    _native.check(lib.hps_dgemm_batched(M, N, K, B, 1.5, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N, None, 0,
+    _native.check(lib.hps_dgemm_batched(_native.context(), M, N, K, B, 1.5, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N, None, 0,
                                         -0.5, _native.ptr(tC), N, M * N, _native.stream_ptr()), "gemm")
     assert rel(tC.cpu().numpy(), 1.5 * A @ Bm - 0.5 * C) < 1e-14
 
@@ -58,7 +58,7 @@ def test_dgemm_generic_shapes(M, N, K, B):
 def test_dgemm_rejects_empty_k():
     lib = _native.load()
     t = torch.zeros(64, dtype=torch.float64, device="cuda")
-    st = lib.hps_dgemm_batched(4, 4, 0, 1, 1.0, _native.ptr(t), 4, 0, _native.ptr(t), 4, 0, None, 0, 0.0,
+    st = lib.hps_dgemm_batched(_native.context(), 4, 4, 0, 1, 1.0, _native.ptr(t), 4, 0, _native.ptr(t), 4, 0, None, 0, 0.0,
                                _native.ptr(t), 4, 0, _native.stream_ptr())
     assert st == _native.HPS_ERR_ARG
 
@@ -74,7 +74,7 @@ def test_solve_level(nb, n3, ne, ldu, nrhs):
     u = np.zeros((N, ldu))
     u[:300] = rng.standard_normal((300, ldu))
     tS, tI, tu = cuda(S), cuda(Ie), cuda(u)
-    _native.check(lib.hps_solve_level(nb, n3, ne, _native.ptr(tS), _native.ptr(tI), 300, _native.ptr(tu), ldu,
+    _native.check(lib.hps_solve_level(_native.context(), nb, n3, ne, _native.ptr(tS), _native.ptr(tI), 300, _native.ptr(tu), ldu,
                                       nrhs, _native.stream_ptr()), "solve")
     ref = u.copy()
     for b in range(nb):

@@ -300,7 +300,7 @@ def test_inverse_batched(n, batch):
     X = torch.from_numpy(A.copy()).cuda()
     ws = torch.empty(lib.hps_inverse_workspace_bytes(n, batch), dtype=torch.uint8, device="cuda")
     stw = torch.full((1,), -1, dtype=torch.int32, device="cuda")
-    _native.check(lib.hps_inverse_batched(n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(),
+    _native.check(lib.hps_inverse_batched(_native.context(), n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(),
                                           _native.ptr(stw), _native.stream_ptr()), "inverse")
     Xi = X.cpu().numpy()
     assert np.abs(A @ Xi - np.eye(n)).max() < 1e-11

@@ -11,14 +11,14 @@ def t_inv(n, batch, reps=5):
     st = torch.full((1,), -1, dtype=torch.int32, device="cuda")
     def run():
         X.copy_(A)
-        _native.check(lib.hps_inverse_batched(n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr()), "inv")
+        _native.check(lib.hps_inverse_batched(_native.context(), n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr()), "inv")
     run(); torch.cuda.synchronize()
     err = float((torch.bmm(A, X) - torch.eye(n, dtype=torch.float64, device="cuda")).abs().max())
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     best = 1e9
     for _ in range(reps):
         X.copy_(A); e0.record()
-        _native.check(lib.hps_inverse_batched(n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr()), "inv")
+        _native.check(lib.hps_inverse_batched(_native.context(), n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr()), "inv")
         e1.record(); e1.synchronize(); best = min(best, e0.elapsed_time(e1))
     print(f"inverse n={n:5d} batch={batch:6d}: {best*1e3:9.1f} us  {2*n**3*batch/best/1e9:8.2f} TF/s  |AX-I|={err:.1e}", flush=True)
 def t_gemm(M, N, K, batch, reps=5):
@@ -28,7 +28,7 @@ def t_gemm(M, N, K, batch, reps=5):
     best = 1e9
     for _ in range(reps + 1):
         e0.record()
-        _native.check(lib.hps_dgemm_batched(M, N, K, batch, 1.0, _native.ptr(A), K, M*K, _native.ptr(B), N, K*N, None, 0, 0.0, _native.ptr(C), N, M*N, _native.stream_ptr()), "g")
+        _native.check(lib.hps_dgemm_batched(_native.context(), M, N, K, batch, 1.0, _native.ptr(A), K, M*K, _native.ptr(B), N, K*N, None, 0, 0.0, _native.ptr(C), N, M*N, _native.stream_ptr()), "g")
         e1.record(); e1.synchronize(); best = min(best, e0.elapsed_time(e1))
     tc = 1e9
     for _ in range(reps + 1):

@@ -11,11 +11,11 @@ for n in (32, 64, 128):
     st = torch.full((1,), -1, dtype=torch.int32, device="cuda")
     buf = (ctypes.c_longlong * 8)()
     X = A.clone()
-    lib.hps_inverse_batched(n, 1, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr())
+    lib.hps_inverse_batched(_native.context(), n, 1, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr())
     torch.cuda.synchronize()
     lib.hps_debug_gj_profile(buf, 1)
     X = A.clone()
-    lib.hps_inverse_batched(n, 1, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr())
+    lib.hps_inverse_batched(_native.context(), n, 1, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr())
     torch.cuda.synchronize()
     lib.hps_debug_gj_profile(buf, 0)
     nb = n // 8 - 1

@@ -24,7 +24,7 @@ for r in range(4):
     wsb = lib.hps_merge_workspace_bytes(nb, n3, ne)
     ws = torch.full((wsb // 8,), float(r), dtype=torch.float64, device="cuda")  # different garbage per run
     status = torch.full((1,), -1, dtype=torch.int32, device="cuda")
-    _native.check(lib.hps_merge_level(nb, n3, ne, m, lay.q, _native.ptr(child), ne_c := child.shape[-1] ** 2 if False else child.shape[1] * child.shape[2],
+    _native.check(lib.hps_merge_level(_native.context(), nb, n3, ne, m, lay.q, _native.ptr(child), ne_c := child.shape[-1] ** 2 if False else child.shape[1] * child.shape[2],
                                       None, _native.ptr(dl.maps[dtarget]), _native.ptr(dl.vmode[dtarget]),
                                       _native.ptr(S), _native.ptr(T), _native.ptr(ws), wsb,
                                       ctypes.c_void_p(status.data_ptr()), 0, _native.stream_ptr()), "merge")

@@ -9,5 +9,5 @@ ws = torch.empty(lib.hps_inverse_workspace_bytes(n, batch), dtype=torch.uint8, d
 st = torch.full((1,), -1, dtype=torch.int32, device="cuda")
 for _ in range(2):
     X = A.clone()
-    _native.check(lib.hps_inverse_batched(n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr()), "inv")
+    _native.check(lib.hps_inverse_batched(_native.context(), n, batch, _native.ptr(X), n, n * n, _native.ptr(ws), ws.numel(), _native.ptr(st), _native.stream_ptr()), "inv")
 torch.cuda.synchronize(); print("ok")

@@ -19,7 +19,7 @@ for rep in range(5):
         dl = lay.depths[d]
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        _native.check(lib.hps_solve_level(dl.n_boxes, dl.n3, dl.ne, _native.ptr(st.S_levels[d]), _native.ptr(st.Ie_levels[d]),
+        _native.check(lib.hps_solve_level(_native.context(), dl.n_boxes, dl.n3, dl.ne, _native.ptr(st.S_levels[d]), _native.ptr(st.Ie_levels[d]),
                                           int(lay.depth_off[d]), _native.ptr(U), ldu, b if b <= 8 else ldu, _native.stream_ptr()), "s")
         e1.record(); e1.synchronize()
         res.setdefault(d, []).append(e0.elapsed_time(e1) * 1e3)
