@@ -56,6 +56,13 @@ def test_baseline_size_against_reference(tag):
     for name, diff, noise in checks:
         gate = max(TOL[cfg], 10.0 * noise)
         report.append(f"{tag} {name}: diff {diff:.2e}, reference self-noise {noise:.2e}, gate {gate:.2e}")
+    # tie-breaker where an exact solution exists: cfg 1 exp(x1) sin(x2), cfg 3 plane wave
+    ex = problems.exact_solution(cfg, nodes.points[:, 0], nodes.points[:, 1], seed=21, batch=1)
+    if ex is not None:
+        want = np.einsum("rc,lc->lr", st.geometry.L1, ex[Ie])
+        e_gpu, e_ref = rel(L1u, want), rel(g["L1u"], want)
+        print(f"{tag} L1 u vs the exact solution: GPU {e_gpu:.2e}, reference {e_ref:.2e}")
+        assert e_gpu <= max(10 * e_ref, TOL[cfg])
     print("\n".join(report))
     for (name, diff, noise), line in zip(checks, report):
         assert diff <= max(TOL[cfg], 10.0 * noise), line

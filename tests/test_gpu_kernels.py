@@ -123,3 +123,61 @@ def test_leaf_verify_flags_a_wrong_representative():
     wrong = torch.tensor([0, 0, 2, 3], dtype=torch.int64, device="cuda")
     _native.check(lib.hps_leaf_verify(4, 256, 1, ptrs, _native.ptr(wrong), _native.ptr(flag), _native.stream_ptr()), "v")
     assert int(flag.item()) == 1
+
+
+def test_two_contexts_on_one_device():
+    """Two hps_ctx_t on one device: independent options and split-K scratch; concurrent split-K
+    GEMMs on two streams through the two contexts give the same bits as alone."""
+    lib = _native.load()
+    a, b = _native.Context(0), _native.Context(0)
+    try:
+        assert lib.hps_ctx_device(a) == 0 and lib.hps_ctx_device(b) == 0
+        b.set("splitk", 0)
+        assert a.get("splitk") == 1 and b.get("splitk") == 0
+        rng = np.random.default_rng(3)
+        M, N, K = 128, 128, 4096  # 4 tiles: split-K in a context that allows it
+        A, B = cuda(rng.standard_normal((M, K))), cuda(rng.standard_normal((K, N)))
+        outs = []
+        for cx in (a, b):
+            C = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+            _native.check(lib.hps_dgemm_batched(cx, M, N, K, 1, 1.0, _native.ptr(A), K, 0, _native.ptr(B), N, 0, None,
+                                                0, 0.0, _native.ptr(C), N, 0, _native.stream_ptr()), "gemm")
+            outs.append(C)
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        conc = [torch.zeros((M, N), dtype=torch.float64, device="cuda") for _ in range(2)]
+        torch.cuda.synchronize()
+        for cx, s, C in ((a, s1, conc[0]), (b, s2, conc[1])):
+            with torch.cuda.stream(s):
+                _native.check(lib.hps_dgemm_batched(cx, M, N, K, 1, 1.0, _native.ptr(A), K, 0, _native.ptr(B), N, 0,
+                                                    None, 0, 0.0, _native.ptr(C), N, 0, _native.stream_ptr(s)), "g")
+        torch.cuda.synchronize()
+        assert torch.equal(conc[0], outs[0]) and torch.equal(conc[1], outs[1])
+        want = A.cpu().numpy() @ B.cpu().numpy()
+        assert rel(outs[0].cpu().numpy(), want) < 1e-13 and rel(outs[1].cpu().numpy(), want) < 1e-13
+    finally:
+        a.close()
+        b.close()
+
+
+def test_lookahead_refuses_odd_batch():
+    """hps_merge_level_ahead with parent arguments but an odd nbatch returns HPS_ERR_ARG instead of
+    skipping the look-ahead the caller relies on."""
+    lib = _native.load()
+    n3, ne, q = 32, 128, 16
+    m = ne // 2 + n3
+    T = torch.zeros((6, m, m), dtype=torch.float64, device="cuda")
+    maps = torch.zeros(ne + 2 * n3, dtype=torch.int32, device="cuda")
+    vm = torch.zeros(2 * q, dtype=torch.float64, device="cuda")
+    S = torch.empty((3, n3, ne), dtype=torch.float64, device="cuda")
+    To = torch.empty((3, ne, ne), dtype=torch.float64, device="cuda")
+    wsb = lib.hps_merge_workspace_bytes(3, n3, ne)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    pwsb = lib.hps_merge_workspace_bytes(2, 64, 256)
+    pws = torch.empty(pwsb, dtype=torch.uint8, device="cuda")
+    st = torch.full((2,), -1, dtype=torch.int32, device="cuda")
+    pmaps = torch.zeros(256 + 128, dtype=torch.int32, device="cuda")
+    r = lib.hps_merge_level_ahead(_native.context(), 3, n3, ne, m, q, _native.ptr(T), m * m, None, _native.ptr(maps),
+                                  _native.ptr(vm), _native.ptr(S), _native.ptr(To), _native.ptr(ws), wsb,
+                                  _native.ptr(st), 0, 0, _native.ptr(pmaps), 64, 256, _native.ptr(vm), _native.ptr(pws),
+                                  pwsb, _native.ptr(st), 0, _native.stream_ptr())
+    assert r == _native.HPS_ERR_ARG and "even nbatch" in _native.last_error()
