@@ -11,6 +11,7 @@
  *                       (assemble_operator leafops.py:217-233, interior_solve_batch
  *                        leafops.py:273-295, DtN product solver.py:241-242)
  *   hps_merge_level  <- merge.merge_dtn, merge.py:92-119, for all 2^d parents of one depth
+ *   hps_lu_solve_batched <- scipy.linalg.lu_factor / lu_solve (LAPACK getrf/getrs), merge.py:106-110
  *                       (the dense-branch loop body of solver.build, solver.py:266-285)
  *   hps_solve_level  <- SolutionOperator.apply inside solver.solve, solver.py:93-97 / 312-315,
  *                       for all parents of one depth and a batch of right-hand sides
@@ -112,16 +113,45 @@ int hps_merge_level_ahead(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int 
                           int pre_inverted, const int* pmaps, int pn3, int pne, const double* pvmode, void* pws,
                           size_t pws_bytes, int* pstatus, int pstatus_base, void* stream);
 
+/* Split merge of the distributed top depths (parallel.py): the parent's owner runs
+ * hps_merge_interface (gathers, deflation, factorisation: the in-place inverse for n3 <= 128, the
+ * pivoted LU for n3 > 128; outputs the factored X, its row permutation (identity for n3 <= 128), R
+ * and C, each nbatch-batched like hps_merge_level's workspace); every rank of the parent's group
+ * solves a column panel S_p = X^-1 R[:, panel] (hps_interface_solve) and forms T_p = C S_p
+ * (hps_dgemm_batched); the owner assembles T = blkdiag(Ta11, Tb22) + [T_0 | T_1 | ...]
+ * (hps_merge_assemble; panels laid out [npanels][nbatch][ne][ne / npanels]). Same per-element
+ * arithmetic as hps_merge_level. */
+int hps_merge_interface(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, const double* T_child,
+                        long long child_stride, const int* child_idx, const int* maps, const double* vmode,
+                        double* Xf_out, int* perm_out, double* R_out, double* C_out, void* ws, size_t ws_bytes,
+                        int* status, int status_base, void* stream);
+int hps_interface_solve(hps_ctx_t ctx, int n3, int ncols, int batch, const double* Xf, const int* perm,
+                        const double* R, double* S_out, int* status, int status_base, void* stream);
+int hps_merge_assemble(hps_ctx_t ctx, int nbatch, int ne, int m, const double* T_child, long long child_stride,
+                       const int* child_idx, const int* maps, const double* panels, int npanels, double* T_out,
+                       void* stream);
+
 /* u[ii_start0 + b*n3 + r, :nrhs] = sum_c S[b][r][c] * u[Ie[b][c], :nrhs] for all nbatch parents of
  * one depth; u is node-major with leading dimension ldu (solver.py:312-315). */
 int hps_solve_level(hps_ctx_t ctx, int nbatch, int n3, int ne, const double* S, const int* Ie, long long ii_start0,
                     double* u, int ldu, int nrhs, void* stream);
 
-/* In-place inverse of `batch` n x n matrices (partial-pivoting Gauss-Jordan for n <= 128, recursive
- * 2x2 block inverse on the DMMA GEMM above that; n % 32 == 0 when n > 128). *status as above. */
+/* In-place inverse of `batch` n x n matrices: partial-pivoting Gauss-Jordan for n <= 128 (what the
+ * merges use there); above 128 a recursive 2x2 block inverse on the DMMA GEMM, which pivots only
+ * inside its 128-blocks (a utility; the merges factor n3 > 128 with hps_lu_solve_batched's LU).
+ * *status as above. */
 size_t hps_inverse_workspace_bytes(int n, int batch);
 int hps_inverse_batched(hps_ctx_t ctx, int n, int batch, double* X, long long lda, long long strideX, void* ws,
                         size_t ws_bytes, int* status, void* stream);
+
+/* Pivoted LU (partial pivoting over the whole column, LAPACK getrf row order; merge.py:106-110) of
+ * `batch` n x n matrices X (stride n^2, overwritten by L\U), then S = X^-1 R (R, S: n x ne per
+ * matrix) by two triangular solves. ipiv_out (optional, device, batch x n): LAPACK-style 0-based
+ * swap rows. *status (init -1) is raised to b for a zero pivot column or a non-finite S. This is
+ * the factorisation hps_merge_level uses for interfaces of n3 > 128. */
+size_t hps_lu_workspace_bytes(int n, int batch);
+int hps_lu_solve_batched(hps_ctx_t ctx, int n, int ne, int batch, double* X, const double* R, double* S_out,
+                         int* ipiv_out, void* ws, size_t ws_bytes, int* status, void* stream);
 
 /* C[b] = alpha A[b] B[b] + beta C[b]; optional B-row gather Bidx (NULL = none). K % 16 == 0. */
 int hps_dgemm_batched(hps_ctx_t ctx, int M, int N, int K, int batch, double alpha, const double* A, long long lda,

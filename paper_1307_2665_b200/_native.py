@@ -27,7 +27,8 @@ EXPORTS = ("hps_ctx_create", "hps_ctx_destroy", "hps_ctx_set_option", "hps_ctx_g
            "hps_leaf_stage", "hps_merge_workspace_bytes", "hps_merge_level", "hps_solve_level",
            "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched", "hps_leaf_hash",
            "hps_leaf_verify", "hps_leaf_fields", "hps_eval_points", "hps_gauge_sides", "hps_gauge_gather",
-           "hps_merge_level_ahead", "hps_tree_sizes", "hps_tree_layout")
+           "hps_merge_level_ahead", "hps_tree_sizes", "hps_tree_layout", "hps_lu_workspace_bytes",
+           "hps_lu_solve_batched", "hps_merge_interface", "hps_interface_solve", "hps_merge_assemble")
 
 HPS_OPT_SPLITK = 0
 HPS_OPT_GEMM_GROUP_M = 1
@@ -103,6 +104,17 @@ def load():
     lib.hps_inverse_workspace_bytes.restype = c_sz
     lib.hps_inverse_batched.argtypes = [c_dp, c_int, c_int, c_dp, c_ll, c_ll, c_dp, c_sz, c_dp, c_dp]
     lib.hps_inverse_batched.restype = c_int
+    lib.hps_lu_workspace_bytes.argtypes = [c_int, c_int]
+    lib.hps_lu_workspace_bytes.restype = c_sz
+    lib.hps_lu_solve_batched.argtypes = [c_dp, c_int, c_int, c_int, c_dp, c_dp, c_dp, c_dp, c_dp, c_sz, c_dp, c_dp]
+    lib.hps_lu_solve_batched.restype = c_int
+    lib.hps_merge_interface.argtypes = [c_dp, c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp,
+                                        c_dp, c_dp, c_dp, c_dp, c_sz, c_dp, c_int, c_dp]
+    lib.hps_merge_interface.restype = c_int
+    lib.hps_interface_solve.argtypes = [c_dp, c_int, c_int, c_int, c_dp, c_dp, c_dp, c_dp, c_dp, c_int, c_dp]
+    lib.hps_interface_solve.restype = c_int
+    lib.hps_merge_assemble.argtypes = [c_dp, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_int, c_dp, c_dp]
+    lib.hps_merge_assemble.restype = c_int
     lib.hps_leaf_hash.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_dp), c_dp, c_dp]
     lib.hps_leaf_hash.restype = c_int
     lib.hps_leaf_verify.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_dp), c_dp, c_dp, c_dp]

@@ -9,12 +9,12 @@ FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompil
 objs=()
 pids=()
 mkdir -p "${HPS_OBJ:-${here}/../build_obj}"
-for f in capi gemm merge solve leaf leaf3 group post tree; do
+for f in capi gemm merge lu solve leaf leaf3 group post tree; do
   o="${HPS_OBJ:-${here}/../build_obj}/${f}.o"
   # tree.cu is host code that must reproduce numpy's fp64 results bit for bit: no FMA contraction
   extra=()
   [[ "$f" == tree ]] && extra=(-Xcompiler -ffp-contract=off)
-  if [[ ! -f "$o" || "${here}/${f}.cu" -nt "$o" || "${here}/common.cuh" -nt "$o" || "${here}/gemm.cuh" -nt "$o" || "${here}/leaf.cuh" -nt "$o" || "${here}/ctx.cuh" -nt "$o" || "${here}/../../include/hps_b200.h" -nt "$o" ]]; then
+  if [[ ! -f "$o" || "${here}/${f}.cu" -nt "$o" || "${here}/common.cuh" -nt "$o" || "${here}/gemm.cuh" -nt "$o" || "${here}/leaf.cuh" -nt "$o" || "${here}/ctx.cuh" -nt "$o" || "${here}/lu.cuh" -nt "$o" || "${here}/../../include/hps_b200.h" -nt "$o" ]]; then
     rm -f "$o"
     "$NVCC" "${FLAGS[@]}" "${extra[@]}" -c "${here}/${f}.cu" -o "$o" &
     pids+=($!)

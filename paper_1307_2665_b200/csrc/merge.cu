@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "ctx.cuh"
 #include "gemm.cuh"
+#include "lu.cuh"
 
 namespace hps {
 
@@ -666,9 +667,28 @@ static int inverse_rec(Ctx& cx, double* A, long long lda, long long strideA, int
 }
 
 static size_t inverse_rec_tmp_doubles(int n, int batch) {
-  if (n <= 16) return 0;  // (workspace sized for the smallest recursion base, HPS_INV_BASE)
+  if (n <= 128) return 0;  // the Gauss-Jordan base needs no workspace
   const int h = n / 2, h2 = n - h;
   return 2ull * batch * h * h2 + std::max(inverse_rec_tmp_doubles(h, batch), inverse_rec_tmp_doubles(h2, batch));
+}
+
+// Merge workspace of one depth: X (inverted in place for n3 <= 128, LU-factored for n3 > 128), R,
+// C, the LU pivots (n3 > 128) and the per-merge deflation shifts.
+struct MergeWs {
+  double *X, *R, *C;
+  LuWs lu;
+  unsigned long long* diagmax;
+};
+static size_t lu_bytes_aligned(int n3, int nbatch) { return n3 > 128 ? (lu_ws_bytes(n3, nbatch) + 255) & ~size_t(255) : 0; }
+static MergeWs merge_ws(void* ws, int nbatch, int n3, int ne) {
+  MergeWs w;
+  w.X = static_cast<double*>(ws);
+  w.R = w.X + (size_t)nbatch * n3 * n3;
+  w.C = w.R + (size_t)nbatch * n3 * ne;
+  char* aux = reinterpret_cast<char*>(w.C + (size_t)nbatch * ne * n3);
+  if (n3 > 128) w.lu = lu_ws(aux, n3, nbatch);
+  w.diagmax = reinterpret_cast<unsigned long long*>(aux + lu_bytes_aligned(n3, nbatch));
+  return w;
 }
 
 }  // namespace hps
@@ -676,8 +696,8 @@ static size_t inverse_rec_tmp_doubles(int n, int batch) {
 using namespace hps;
 
 extern "C" size_t hps_merge_workspace_bytes(int nbatch, int n3, int ne) {
-  size_t d = size_t(nbatch) * (size_t(n3) * n3 + 2ull * n3 * ne + 1) + inverse_rec_tmp_doubles(n3, nbatch);
-  return d * sizeof(double) + 256;
+  const size_t d = size_t(nbatch) * (size_t(n3) * n3 + 2ull * n3 * ne + 1);
+  return d * sizeof(double) + lu_bytes_aligned(n3, nbatch) + 256;
 }
 
 // HPS_OPT_PROFILE_AHEAD (eager builds only, dev tool): timing events at the look-ahead fork (0),
@@ -724,15 +744,17 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
   const int* j2b = maps + n1;
   const int* j3a = maps + 2 * n1;
   const int* j3b = j3a + n3;
-  double* X = static_cast<double*>(ws);
-  double* R = X + (size_t)nbatch * n3 * n3;
-  double* Cm = R + (size_t)nbatch * n3 * ne;
-  double* tmp = Cm + (size_t)nbatch * ne * n3;
-  unsigned long long* diagmax = reinterpret_cast<unsigned long long*>(tmp + inverse_rec_tmp_doubles(n3, nbatch));
+  const MergeWs W = merge_ws(ws, nbatch, n3, ne);
+  double* X = W.X;
+  double* R = W.R;
+  double* Cm = W.C;
+  unsigned long long* diagmax = W.diagmax;
+  const bool big = n3 > 128;  // pivoted LU + triangular solves; else in-register Gauss-Jordan inverse
   const bool deflate = n3 > q;  // deflate the n3/q - 1 corner null modes
   ChildRef ch{T_child, child_stride, child_idx, m};
   if (!pre_inverted && deflate) HPS_CUDA_CHECK(cudaMemsetAsync(diagmax, 0, sizeof(unsigned long long) * nbatch, st));
-  // pre_inverted: X was formed, deflated and inverted by the child depth's look-ahead; R and C only
+  // pre_inverted: X was formed, deflated and inverted (n3 <= 128) or LU-factored (n3 > 128) by the
+  // child depth's look-ahead; R and C only
   k_gather_xr<<<dim3(nbatch, (n3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, pre_inverted ? nullptr : X,
                                                         R, (deflate && !pre_inverted) ? diagmax : nullptr);
   HPS_LAUNCH_CHECK();
@@ -747,11 +769,18 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
       k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vmode, vmode + q, diagmax);
       HPS_LAUNCH_CHECK();
     }
-    HPS_TRY(inverse_rec(cx, X, n3, (long long)n3 * n3, n3, nbatch, tmp, status, status_base, st));
+    if (big)
+      HPS_TRY(lu_factor(cx, X, n3, nbatch, W.lu, status, status_base, st));
+    else
+      HPS_TRY(inverse_small(X, n3, (long long)n3 * n3, n3, nbatch, status, status_base, st));
   }
-  HPS_TRY(gemm(cx, n3, ne, n3, nbatch, 1.0, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, 0.0, S_out, ne,
-               (long long)n3 * ne, st, status));
-  // nonfinite flag reports merge index; shift by status_base happens on the host side
+  if (!S_out) return HPS_OK;  // interface only (hps_merge_interface): X factored, R and C gathered
+  // S = X^-1 R; a non-finite S raises the status word to the merge index (MergeResonanceError)
+  if (big)
+    HPS_TRY(lu_solve(cx, X, n3, nbatch, W.lu, R, ne, S_out, status, status_base, st));
+  else
+    HPS_TRY(gemm(cx, n3, ne, n3, nbatch, 1.0, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, 0.0, S_out, ne,
+                 (long long)n3 * ne, st, status));
   if (ah != nullptr && !(cx.streams_ok && (nbatch % 2) == 0)) {
     // the caller would treat the parent's X as inverted: refuse instead of skipping silently
     set_error("hps_merge_level_ahead: look-ahead needs an even nbatch (got %d) and the context's streams", nbatch);
@@ -768,11 +797,11 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
     }
     const int* pj3a = ah->pmaps + 2 * pn1;
     const int* pj3b = pj3a + pn3;
-    double* pX = static_cast<double*>(ah->pws);
-    double* pR = pX + (size_t)P * pn3 * pn3;
-    double* pC = pR + (size_t)P * pn3 * pne;
-    double* ptmp = pC + (size_t)P * pne * pn3;
-    unsigned long long* pdiag = reinterpret_cast<unsigned long long*>(ptmp + inverse_rec_tmp_doubles(pn3, P));
+    const MergeWs PW = merge_ws(ah->pws, P, pn3, pne);
+    double* pX = PW.X;
+    double* pR = PW.R;
+    double* pC = PW.C;
+    unsigned long long* pdiag = PW.diagmax;
     double* Ag = pR;  // P x pn3 x 2 n3  (2 n3 <= pne)
     double* Bg = pC;  // P x 2 n3 x pn3
     k_ahead_rows<<<dim3(P, (pn3 + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, n3, ne, Cm, pj3a, pj3b, pn3, Ag, pX);
@@ -794,8 +823,10 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
       k_deflate<<<dim3(P, pn3 / q), 256, 0, cx.ahead>>>(pX, pn3, q, ah->pvmode, ah->pvmode + q, pdiag);
       HPS_LAUNCH_CHECK();
     }
-    HPS_TRY(inverse_rec(cx, pX, pn3, (long long)pn3 * pn3, pn3, P, ptmp, ah->pstatus, ah->pstatus_base, cx.ahead,
-                        cx.ahead_side));
+    if (pn3 > 128)
+      HPS_TRY(lu_factor(cx, pX, pn3, P, PW.lu, ah->pstatus, ah->pstatus_base, cx.ahead));
+    else
+      HPS_TRY(inverse_small(pX, pn3, (long long)pn3 * pn3, pn3, P, ah->pstatus, ah->pstatus_base, cx.ahead));
     ahead_probe(cx, 1, cx.ahead);
   }
   {  // T = blkdiag(Ta[j1a, j1a], Tb[j2b, j2b]) + C S, the blkdiag read by the GEMM epilogue
@@ -849,4 +880,94 @@ extern "C" int hps_inverse_batched(hps_ctx_t ctx, int n, int batch, double* X, l
   HPS_CTX(cx, ctx);
   return inverse_rec(*cx, X, lda, strideX, n, batch, static_cast<double*>(ws), status, 0,
                      static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------------------------------------
+// Split merge for the distributed top depths (parallel.py): the owner of a parent forms and factors
+// its interface system (hps_merge_interface), every rank of the parent's group solves a column panel
+// of S and multiplies it into a column panel of T (hps_interface_solve + hps_dgemm_batched), and the
+// owner assembles T = blkdiag + panels (hps_merge_assemble). Per-element arithmetic is that of
+// hps_merge_level (same kernels, same summation order), so with split-K off the two agree bitwise.
+// ---------------------------------------------------------------------------------------------
+namespace hps {
+__global__ void k_iota_rows(int* perm, int n, int batch) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * batch; i += gridDim.x * blockDim.x) perm[i] = i % n;
+}
+
+// T[b][r][c] = blkdiag(Ta[j1a, j1a], Tb[j2b, j2b])[r][c] + panels[c / w][b][r][c % w], one warp per row.
+__global__ void k_merge_assemble(ChildRef ch, const int* __restrict__ j1a, const int* __restrict__ j2b, int ne,
+                                 const double* __restrict__ panels, int w, int nbatch, double* __restrict__ T) {
+  const int b = blockIdx.y;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= ne) return;
+  const int n1 = ne / 2;
+  const bool top = r < n1;
+  const double* src = top ? ch.a(b) : ch.bb(b);
+  const int rm = top ? j1a[r] : j2b[r - n1];
+  double* Tr = T + ((long long)b * ne + r) * ne;
+  for (int c = lane; c < ne; c += 32) {
+    const int p = c / w, cc = c - p * w;
+    double v = panels[(((long long)p * nbatch + b) * ne + r) * w + cc];
+    double blk = 0.0;
+    if ((c < n1) == top) blk = src[(long long)rm * ch.m + (top ? j1a[c] : j2b[c - n1])];
+    Tr[c] = v + blk;
+  }
+}
+}  // namespace hps
+
+extern "C" int hps_merge_interface(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, const double* T_child,
+                                   long long child_stride, const int* child_idx, const int* maps, const double* vmode,
+                                   double* Xf_out, int* perm_out, double* R_out, double* C_out, void* ws,
+                                   size_t ws_bytes, int* status, int status_base, void* stream) {
+  HPS_CTX(cx, ctx);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  HPS_TRY(merge_level_impl(*cx, nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, nullptr,
+                           nullptr, ws, ws_bytes, status, status_base, false, nullptr, st));
+  const MergeWs W = merge_ws(ws, nbatch, n3, ne);
+  const size_t nX = (size_t)nbatch * n3 * n3, nR = (size_t)nbatch * n3 * ne;
+  if (Xf_out) HPS_CUDA_CHECK(cudaMemcpyAsync(Xf_out, W.X, nX * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (R_out) HPS_CUDA_CHECK(cudaMemcpyAsync(R_out, W.R, nR * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (C_out) HPS_CUDA_CHECK(cudaMemcpyAsync(C_out, W.C, nR * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (perm_out) {
+    if (n3 > 128) {
+      HPS_CUDA_CHECK(cudaMemcpyAsync(perm_out, W.lu.perm, (size_t)nbatch * n3 * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    } else {
+      k_iota_rows<<<std::max(1, std::min(1024, (n3 * nbatch + 255) / 256)), 256, 0, st>>>(perm_out, n3, nbatch);
+      HPS_LAUNCH_CHECK();
+    }
+  }
+  return HPS_OK;
+}
+
+extern "C" int hps_interface_solve(hps_ctx_t ctx, int n3, int ncols, int batch, const double* Xf, const int* perm,
+                                   const double* R, double* S_out, int* status, int status_base, void* stream) {
+  HPS_CTX(cx, ctx);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n3 <= 0 || ncols <= 0 || batch <= 0) {
+    set_error("hps_interface_solve: bad arguments n3=%d ncols=%d", n3, ncols);
+    return HPS_ERR_ARG;
+  }
+  if (n3 <= 128)
+    return gemm(*cx, n3, ncols, n3, batch, 1.0, Xf, n3, (long long)n3 * n3, R, ncols, (long long)n3 * ncols, 0.0,
+                S_out, ncols, (long long)n3 * ncols, st, status);
+  LuWs w;
+  w.perm = const_cast<int*>(perm);
+  return lu_solve(*cx, Xf, n3, batch, w, R, ncols, S_out, status, status_base, st);
+}
+
+extern "C" int hps_merge_assemble(hps_ctx_t ctx, int nbatch, int ne, int m, const double* T_child,
+                                  long long child_stride, const int* child_idx, const int* maps, const double* panels,
+                                  int npanels, double* T_out, void* stream) {
+  HPS_CTX(cx, ctx);
+  (void)cx;
+  if (npanels <= 0 || ne % npanels || ne % 2) {
+    set_error("hps_merge_assemble: ne=%d not divisible into %d panels", ne, npanels);
+    return HPS_ERR_ARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ChildRef ch{T_child, child_stride, child_idx, m};
+  k_merge_assemble<<<dim3((ne + 7) / 8, nbatch), 256, 0, st>>>(ch, maps, maps + ne / 2, ne, panels, ne / npanels,
+                                                              nbatch, T_out);
+  HPS_LAUNCH_CHECK();
+  return HPS_OK;
 }

@@ -30,8 +30,8 @@ from .errors import ConfigError
 from .grid import layout_of
 from .leafops import LeafGeometry
 
-__all__ = ["CudaBackend", "DistState", "prepare_distributed", "build_distributed", "solve_distributed",
-           "gather_solution", "subtree_plan", "TorchComm"]
+__all__ = ["CudaBackend", "DistState", "prepare_distributed", "build_distributed", "check_distributed",
+           "solve_distributed", "gather_solution", "subtree_plan", "TorchComm", "LocalComm"]
 
 
 # ----------------------------------------------------------------------------------------------
@@ -75,7 +75,7 @@ def subtree_plan(L, world):
 class CudaBackend:
     """Stage calls into libhps_b200.so for a subset of slots, on the current CUDA device."""
 
-    def __init__(self, tree, device=None):
+    def __init__(self, tree, device=None, ctx_slot=0):
         import torch
 
         from .solver import _DeviceLayout
@@ -87,7 +87,8 @@ class CudaBackend:
         self.lay = layout_of(tree)
         self.geom = LeafGeometry.get(self.lay.q, tree.leaf_width, tree.leaf_height)
         self.dl = _DeviceLayout.get(self.lay, self.geom, self.device)
-        self.ctx = _native.context(device=self.device)
+        # ranks sharing one device (LocalComm) need their own library context each
+        self.ctx = _native.context(ctx_slot, device=self.device)
 
     # -- tensors / transport --
     def empty(self, shape):
@@ -161,6 +162,66 @@ class CudaBackend:
                       f"hps_merge_level(depth {d})")
         return S, T
 
+    # -- split merge of the distributed top depths (hps_merge_interface / _interface_solve / _assemble) --
+    def merge_interface(self, d, children, status):
+        """Gathers, deflation and factorisation of one parent's interface system. Returns the
+        factored X (inverse for n3 <= 128, L\\U for n3 > 128), its row permutation, R and C."""
+        lib, torch = self.lib, self.torch
+        dl = self.lay.depths[d]
+        n3, ne, m = dl.n3, dl.ne, dl.m
+        Xf = self.empty((1, n3, n3))
+        perm = torch.empty((1, n3), dtype=torch.int32, device=self.device)
+        R = self.empty((1, n3, ne))
+        C = self.empty((1, ne, n3))
+        wsb = lib.hps_merge_workspace_bytes(1, n3, ne)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        _native.check(lib.hps_merge_interface(self.ctx, 1, n3, ne, m, self.lay.q, _native.ptr(children), m * m, None,
+                                              _native.ptr(self.dl.maps[d]), _native.ptr(self.dl.vmode[d]),
+                                              _native.ptr(Xf), _native.ptr(perm), _native.ptr(R), _native.ptr(C),
+                                              _native.ptr(ws), wsb, _native.ptr(status), 0, _native.stream_ptr()),
+                      f"hps_merge_interface(depth {d})")
+        return Xf, perm, R, C
+
+    def interface_solve(self, d, Xf, perm, Rp, status):
+        n3, w = Rp.shape[1], Rp.shape[2]
+        Sp = self.empty((1, n3, w))
+        _native.check(self.lib.hps_interface_solve(self.ctx, n3, w, 1, _native.ptr(Xf), _native.ptr(perm),
+                                                   _native.ptr(Rp), _native.ptr(Sp), _native.ptr(status), 0,
+                                                   _native.stream_ptr()), f"hps_interface_solve(depth {d})")
+        return Sp
+
+    def panel_gemm(self, C, Sp):
+        ne, n3, w = C.shape[1], C.shape[2], Sp.shape[2]
+        Tp = self.empty((1, ne, w))
+        _native.check(self.lib.hps_dgemm_batched(self.ctx, ne, w, n3, 1, 1.0, _native.ptr(C), n3, 0, _native.ptr(Sp),
+                                                 w, 0, None, 0, 0.0, _native.ptr(Tp), w, 0, _native.stream_ptr()),
+                      "hps_dgemm_batched(T panel)")
+        return Tp
+
+    def col_panel(self, M, c0, w):
+        return M[:, :, c0:c0 + w].contiguous()
+
+    def concat_cols(self, parts):
+        return self.torch.cat(parts, dim=2).contiguous()
+
+    def assemble(self, d, children, panels):
+        dl = self.lay.depths[d]
+        ne, m = dl.ne, dl.m
+        P = self.torch.stack(panels).contiguous()  # (npanels, 1, ne, w)
+        T = self.empty((1, ne, ne))
+        _native.check(self.lib.hps_merge_assemble(self.ctx, 1, ne, m, _native.ptr(children), m * m, None,
+                                                  _native.ptr(self.dl.maps[d]), _native.ptr(P), len(panels),
+                                                  _native.ptr(T), _native.stream_ptr()), f"hps_merge_assemble({d})")
+        return T
+
+    def empty_int(self, shape):
+        return self.torch.empty(shape, dtype=self.torch.int32, device=self.device)
+
+    def read_failures(self, st):
+        """(leaf cond array, [(depth, slot0, status value)]) of this rank, on the host."""
+        cond = st.cond.cpu().numpy() if st.cond is not None else np.zeros(0)
+        return cond, [(d, k, int(t.cpu().item())) for d, k, t in st.statuses]
+
     def solve_level(self, d, slot0, nslots, S, u, nrhs):
         dl = self.lay.depths[d]
         ldu = u.shape[1]
@@ -197,6 +258,7 @@ class DistState:
     T_leaf_groups: object = None
     leaf_group: np.ndarray = None                  # local leaf -> local group
     cond: object = None
+    reps: np.ndarray = None                        # local leaf index of each group's first leaf
     statuses: list = field(default_factory=list)
 
     def owned_rows(self):
@@ -257,9 +319,12 @@ def prepare_distributed(tree, coeffs, rank, world, backend):
     return LocalInputs(local_fields, scalars, reps, gid)
 
 
-def build_distributed(tree, coeffs, comm, backend, inputs=None):
+def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels", check=True):
     """Subtree-parallel build. `comm` provides rank, world, send(tensor, dst), recv(tensor, src).
-    `inputs` (from prepare_distributed) skips the host sampling/grouping."""
+    `inputs` (from prepare_distributed) skips the host sampling/grouping. `top_mode` is "panels"
+    (the top merges' solves and T GEMMs split in column panels over the parent's group) or "owner"
+    (the parent's owner merges alone). With check=True every rank raises the reference's exception
+    for the first failure in the reference's order (check_distributed)."""
     lay = layout_of(tree)
     L = lay.L
     plan = subtree_plan(L, comm.world)
@@ -271,6 +336,7 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None):
     gid = inputs.gid
     Psi, Tleaf, cond = backend.leaf_stage(inputs.fields, inputs.scalars, int(inputs.reps.size))
     st.psi_groups, st.T_leaf_groups, st.leaf_group, st.cond = Psi, Tleaf, gid, cond
+    st.reps = inputs.reps
 
     # ---- local merges, depths 2L-1 .. s (the parents of a local depth above s are local too, so
     # their status words exist one call early for the look-ahead inverse) ----
@@ -292,28 +358,108 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None):
         child_T = Tleaf[gid[0]:gid[0] + 1]
     st.subtree_T = child_T  # (1, ne_s, ne_s)
 
-    # ---- top merges, depths s-1 .. 0: child b's owner sends its T to child a's owner ----
+    # ---- top merges, depths s-1 .. 0. Child b's owner sends its DtN map to the
+    # parent's owner (child a's owner), which forms and factors the interface system. "panels"
+    # (default): every rank of the parent's group (2^(s-d) ranks) then solves a column panel of S and
+    # forms the matching column panel of T = C S, so the dominant T GEMM (and the triangular solves)
+    # run on all ranks instead of one; the owner assembles T = blkdiag + panels and keeps S for the
+    # solve. "owner": the owner merges alone (hps_merge_level). Same per-element arithmetic. ----
     cur = child_T
     for d in range(s - 1, -1, -1):
-        span = 1 << (s - d - 1)  # ranks per box at depth d+1
-        if rank % span:
-            continue  # this rank owns no box at depth d+1
-        kc = rank // span
-        if kc % 2 == 1:
-            comm.send(cur, plan.owner(d, kc // 2))
-            cur = None
+        P = 1 << (s - d)  # ranks in the parent's group
+        k = rank >> (s - d)
+        owner = k << (s - d)
+        span = P // 2
+        dl = lay.depths[d]
+        m = dl.m
+        other = None
+        if rank % span == 0:
+            kc = rank // span
+            if kc % 2 == 1:
+                comm.send(cur, owner)
+                cur = None
+            else:
+                other = backend.empty((1, m, m))
+                comm.recv(other, owner + span)
+        panels = top_mode == "panels" and dl.n3 >= 64 and dl.ne % P == 0 and (dl.ne // P) % 2 == 0
+        if not panels:
+            if rank == owner:
+                status = backend.status_word()
+                st.statuses.append((d, k, status))
+                S, T = backend.merge_level(d, 1, backend.stack2(cur, other), None, status)
+                st.S_top[d] = S
+                cur = T
             continue
-        m = lay.depths[d].m
-        other = backend.empty((1, m, m))
-        comm.recv(other, plan.owner(d + 1, kc + 1))
+        n3, ne, w = dl.n3, dl.ne, dl.ne // P
         status = backend.status_word()
-        st.statuses.append((d, kc // 2, status))
-        S, T = backend.merge_level(d, 1, backend.stack2(cur, other), None, status)
-        st.S_top[d] = S
-        cur = T
+        st.statuses.append((d, k, status))
+        if rank == owner:
+            children = backend.stack2(cur, other)
+            Xf, perm, R, C = backend.merge_interface(d, children, status)
+            for r in range(1, P):
+                comm.send(Xf, owner + r)
+                comm.send(perm, owner + r)
+                comm.send(C, owner + r)
+                comm.send(backend.col_panel(R, r * w, w), owner + r)
+            Rp = backend.col_panel(R, 0, w)
+        else:
+            Xf, perm = backend.empty((1, n3, n3)), backend.empty_int((1, n3))
+            C, Rp = backend.empty((1, ne, n3)), backend.empty((1, n3, w))
+            for t in (Xf, perm, C, Rp):
+                comm.recv(t, owner)
+        Sp = backend.interface_solve(d, Xf, perm, Rp, status)
+        Tp = backend.panel_gemm(C, Sp)
+        if rank == owner:
+            Tps, Sps = [Tp], [Sp]
+            for r in range(1, P):
+                t, sp = backend.empty((1, ne, w)), backend.empty((1, n3, w))
+                comm.recv(t, owner + r)
+                comm.recv(sp, owner + r)
+                Tps.append(t)
+                Sps.append(sp)
+            cur = backend.assemble(d, children, Tps)
+            st.S_top[d] = backend.concat_cols(Sps)
+        else:
+            comm.send(Tp, owner)
+            comm.send(Sp, owner)
+            cur = None
     if rank == 0:
         st.root_T = cur
+    if check:
+        check_distributed(st, comm)
     return st
+
+
+def check_distributed(st, comm):
+    """Raise on every rank the exception the single-process build would raise: LeafResonanceError for
+    the first resonant leaf group (smallest global leaf index of a bad group's first leaf), else
+    MergeResonanceError for the first failing merge in the reference's order (deepest first,
+    highest box index first; solver.py:235-239, 280-281). One host sync and a min-reduction."""
+    from .errors import LeafResonanceError, MergeResonanceError
+    from .solver import RESONANCE_COND
+
+    lay, plan = st.layout, st.plan
+    n_leaf = 1 << (2 * lay.L)
+    cond, statuses = st.backend.read_failures(st)
+    key, info = n_leaf + (1 << (2 * lay.L + 1)), None  # "no failure"
+    bad = np.flatnonzero(cond > RESONANCE_COND)
+    if bad.size:
+        lo, _ = plan.local_slots(st.rank, 2 * lay.L)
+        g = int(bad[0])
+        leaf = lo + int(st.reps[g])
+        key, info = leaf, float(cond[g])
+    else:
+        boxes = [(1 << d) - 1 + k + v for d, k, v in statuses if v >= 0]
+        if boxes:
+            box = max(boxes)
+            key = n_leaf + ((1 << (2 * lay.L + 1)) - 1 - box)
+    keys = comm.allgather_obj((key, info))
+    key, info = min(keys, key=lambda x: x[0])
+    if key < n_leaf:
+        raise LeafResonanceError(box=n_leaf - 1 + key, cond=info)
+    if key < n_leaf + (1 << (2 * lay.L + 1)):
+        box = (1 << (2 * lay.L + 1)) - 1 - (key - n_leaf)
+        raise MergeResonanceError(box=box, detail="non-finite solution operator")
 
 
 def solve_distributed(st, F, comm):
@@ -399,10 +545,78 @@ class TorchComm:
     def send_obj(self, o, dst):
         self.dist.send_object_list([o], dst, group=self.group)
 
+    def allgather_obj(self, o):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, o, group=self.group)
+        return out
+
     def recv_obj(self, src):
         obj = [None]
         self.dist.recv_object_list(obj, src, group=self.group)
         return obj[0]
+
+
+class LocalComm:
+    """In-process transport for `world` ranks run as threads of one process, sharing one device
+    (the 2/4/8-way partition on one GPU, device-to-device copies in place of
+    NCCL). `LocalComm.run(world, fn)` calls fn(comm) on every rank's thread and returns the results
+    in rank order. Sends are device copies (the sender's tensor is cloned when sent)."""
+
+    def __init__(self, rank, world, hub):
+        self.rank, self.world, self._hub = rank, world, hub
+
+    @staticmethod
+    def run(world, fn):
+        import queue
+        import threading
+
+        hub = {"q": {(a, b): queue.Queue() for a in range(world) for b in range(world)},
+               "barrier": threading.Barrier(world), "slots": [None] * world}
+        results, errors = [None] * world, [None] * world
+
+        def body(r):
+            try:
+                results[r] = fn(LocalComm(r, world, hub))
+            except BaseException as e:  # noqa: BLE001 -- re-raised on the caller's thread
+                errors[r] = e
+                hub["barrier"].abort()
+
+        ths = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        for e in errors:
+            if e is not None and not isinstance(e, threading.BrokenBarrierError):
+                raise e
+        for e in errors:
+            if e is not None:
+                raise e
+        return results
+
+    def send(self, t, dst):
+        self._hub["q"][(self.rank, dst)].put(t.clone())
+
+    def recv(self, t, src):
+        t.copy_(self._hub["q"][(src, self.rank)].get(timeout=600))
+
+    def send_obj(self, o, dst):
+        self._hub["q"][(self.rank, dst)].put(o)
+
+    def recv_obj(self, src):
+        return self._hub["q"][(src, self.rank)].get(timeout=600)
+
+    def allgather_obj(self, o):
+        hub = self._hub
+        hub["barrier"].wait()
+        hub["slots"][self.rank] = o
+        hub["barrier"].wait()
+        out = list(hub["slots"])
+        hub["barrier"].wait()
+        return out
+
+    def bcast_int(self, v):
+        return int(self.allgather_obj(v)[0])
 
 
 def _cuda_backend_extras():

@@ -132,3 +132,34 @@ def test_lookahead_rule_and_stage_flop_accounting(monkeypatch):
     monkeypatch.setenv("HPS_AHEAD_MIN_N3", "0")
     tree, _ = P.build_tree(P.Rectangle(0, 1, 0, 1), 6, 16)
     assert solver.lookahead_depths(layout_of(tree)) == set()
+
+
+@pytest.mark.parametrize("cfg,L", [(3, 4), (4, 4)])
+def test_interface_conditioning_report(cfg, L):
+    """Helmholtz interfaces (configs 3, 4) at every depth with n3 > q: cond of the deflated X_d, cond of
+    its leading half block A11 (what a factorisation pivoting only inside blocks depends on) and the
+    growth factor max|U| / max|X_d| of LAPACK's partially pivoted LU (what the device LU depends on;
+    tests/test_gpu_lu.py checks it picks LAPACK's pivots). Printed with pytest -s."""
+    import scipy.linalg as sla
+    ot = O.build_tree((0, 1, 0, 1), L, 16)
+    st = O.build(ot, {n: getattr(problems.coefficients(cfg), n) for n in O.COEFF_NAMES}, keep_T=True)
+    geom = P.LeafGeometry.get(16, ot.leaf_width, ot.leaf_height)
+    for d in range(2 * L - 1):
+        box = (1 << d) - 1
+        axis = "v" if d % 2 == 0 else "h"
+        a, c = ot.child_a[box], ot.child_b[box]
+        j1a, j2b, j3a, j3b = O.split_indices(ot.I_e[a], ot.I_e[c], ot.I_i[box])
+        X = st.T[a][np.ix_(j3a, j3a)] - st.T[c][np.ix_(j3b, j3b)]
+        n3 = X.shape[0]
+        vs, ve = geom.corner_mode_vectors(axis)
+        V = np.zeros((n3, n3 // 16 - 1))
+        for s_ in range(n3 // 16 - 1):
+            V[s_ * 16:(s_ + 1) * 16, s_] = ve
+            V[(s_ + 1) * 16:(s_ + 2) * 16, s_] = vs
+        Xd = X + np.abs(np.diag(X)).max() * V @ V.T
+        h = n3 // 2
+        lu, _ = sla.lu_factor(Xd)
+        growth = np.abs(np.triu(lu)).max() / np.abs(Xd).max()
+        cx, c11 = np.linalg.cond(Xd), np.linalg.cond(Xd[:h, :h])
+        print(f"cfg{cfg} L{L} depth {d}: n3 {n3}, cond(X_d) {cx:.2e}, cond(A11) {c11:.2e}, LU growth {growth:.2f}")
+        assert np.isfinite(cx) and cx < 1e10 and growth < 1e3  # cfg4 reaches 5e6 (its global problem is near-resonant)
