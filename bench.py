@@ -256,7 +256,9 @@ def main():
     # ---- device-resident timed steps ----
     # Default: the build (one CUDA graph per stage) and the solve replayed from solver.BuildGraph,
     # inputs already in its static buffers; --no-graph: eager enqueue of the same kernels.
-    graph = None if args.no_graph else solver.BuildGraph(inp, nrhs=b)
+    pivoted = solver.check_build(solver.build_device(inp))  # depths whose fast inverse needs the pivoted LU
+    torch.cuda.synchronize()
+    graph = None if args.no_graph else solver.BuildGraph(inp, nrhs=b, pivoted=pivoted)
     if graph is not None:
         graph.load(inp, F_dev)
 
@@ -264,7 +266,7 @@ def main():
         if graph is not None:
             st = graph.replay_build(timeline)
         else:
-            st = solver.build_device(inp, timeline=timeline)
+            st = solver.build_device(inp, timeline=timeline, pivoted=pivoted)
         e = torch.cuda.Event(enable_timing=True)
         e.record()
         U = graph.replay_solve() if graph is not None else solver.solve_device(st, F_dev)
@@ -275,7 +277,8 @@ def main():
         st = U = None  # free the previous step's operators first (L=9: ~50 GB of S + u)
         st, U, _ = step()
     torch.cuda.synchronize()
-    solver.check_build(st)
+    if solver.check_build(st):
+        raise RuntimeError("a residual check failed on the pivoted path")
     torch.cuda.synchronize()
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clocks.start()
@@ -408,6 +411,7 @@ def main():
             "config": {"workload": workload, "l2": L2_NOTE},
             "launch": launch_mode,
             "stages": {"unknowns": unknowns, "batch": b, "leaf_groups": inp.ngroups,
+                       "pivoted_lu_depths": sorted(pivoted),
                        "build_ms": tb * 1e3, "solve_ms": ts * 1e3,
                        "build_unknowns_per_s": unknowns / tb, "solve_unknowns_per_s": unknowns * b / ts,
                        "build_fp64_tflops": roofline["build_tflops"], "build_fp64_frac": roofline["build_frac"],

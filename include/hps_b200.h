@@ -100,6 +100,17 @@ int hps_merge_level(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, con
                     long long child_stride, const int* child_idx, const int* maps,
                     const double* vmode, double* S_out, double* T_out, void* ws, size_t ws_bytes,
                     int* status, int status_base, void* stream);
+/* Interface factorisation of n3 > 128 (flags of hps_merge_level_ahead / hps_merge_interface /
+ * hps_interface_solve). Default: the recursive 2x2 block inverse (DMMA GEMMs over 128-blocks, each
+ * inverted by pivoted Gauss-Jordan) followed by a residual check X_d (X_d^-1 v) - v on a +-1 probe;
+ * above 1e-6 (or non-finite) the depth's status word becomes HPS_STATUS_PIVOT + merge index and the
+ * caller re-runs the depth with HPS_MERGE_PIVOTED: the pivoted LU of hps_lu_solve_batched (partial
+ * pivoting over the whole column, as LAPACK getrf in merge.py:106-110). HPS_MERGE_PARENT_PIVOTED asks
+ * the same for the look-ahead's parent depth. n3 <= 128 always uses pivoted Gauss-Jordan. */
+#define HPS_MERGE_PIVOTED 1
+#define HPS_MERGE_PARENT_PIVOTED 2
+#define HPS_STATUS_PIVOT (1 << 24)
+
 /* hps_merge_level plus a look-ahead for the parent depth (the next call): before this depth's big
  * T GEMM, the parent's interface matrix X = Ta[pj3a, pj3a] - Tb[pj3b, pj3b] is formed from the pj3
  * rows / columns of this depth's T = blk + C S (one GEMM over gathered operands), deflated and
@@ -111,7 +122,7 @@ int hps_merge_level_ahead(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int 
                           long long child_stride, const int* child_idx, const int* maps, const double* vmode,
                           double* S_out, double* T_out, void* ws, size_t ws_bytes, int* status, int status_base,
                           int pre_inverted, const int* pmaps, int pn3, int pne, const double* pvmode, void* pws,
-                          size_t pws_bytes, int* pstatus, int pstatus_base, void* stream);
+                          size_t pws_bytes, int* pstatus, int pstatus_base, int flags, void* stream);
 
 /* Split merge of the distributed top depths (parallel.py): the parent's owner runs
  * hps_merge_interface (gathers, deflation, factorisation: the in-place inverse for n3 <= 128, the
@@ -124,9 +135,9 @@ int hps_merge_level_ahead(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int 
 int hps_merge_interface(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, const double* T_child,
                         long long child_stride, const int* child_idx, const int* maps, const double* vmode,
                         double* Xf_out, int* perm_out, double* R_out, double* C_out, void* ws, size_t ws_bytes,
-                        int* status, int status_base, void* stream);
+                        int* status, int status_base, int flags, void* stream);
 int hps_interface_solve(hps_ctx_t ctx, int n3, int ncols, int batch, const double* Xf, const int* perm,
-                        const double* R, double* S_out, int* status, int status_base, void* stream);
+                        const double* R, double* S_out, int* status, int status_base, int flags, void* stream);
 int hps_merge_assemble(hps_ctx_t ctx, int nbatch, int ne, int m, const double* T_child, long long child_stride,
                        const int* child_idx, const int* maps, const double* panels, int npanels, double* T_out,
                        void* stream);

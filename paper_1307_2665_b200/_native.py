@@ -37,6 +37,10 @@ HPS_OPT_LEAF_CTAS_PER_SM = 3
 HPS_OPT_LEAF_FREE_SMS = 4
 HPS_OPT_PROFILE_AHEAD = 5
 
+HPS_MERGE_PIVOTED = 1
+HPS_MERGE_PARENT_PIVOTED = 2
+HPS_STATUS_PIVOT = 1 << 24
+
 _lib = None
 
 c_dp = ctypes.c_void_p
@@ -89,7 +93,7 @@ def load():
     lib.hps_merge_level.restype = c_int
     lib.hps_merge_level_ahead.argtypes = [c_dp, c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp, c_dp,
                                           c_dp, c_sz, c_dp, c_int, c_int, c_dp, c_int, c_int, c_dp, c_dp, c_sz, c_dp,
-                                          c_int, c_dp]
+                                          c_int, c_int, c_dp]
     lib.hps_merge_level_ahead.restype = c_int
     lib.hps_debug_ahead_times.argtypes = [c_dp, c_int, ctypes.POINTER(ctypes.c_float)]
     lib.hps_debug_ahead_times.restype = c_int
@@ -109,9 +113,9 @@ def load():
     lib.hps_lu_solve_batched.argtypes = [c_dp, c_int, c_int, c_int, c_dp, c_dp, c_dp, c_dp, c_dp, c_sz, c_dp, c_dp]
     lib.hps_lu_solve_batched.restype = c_int
     lib.hps_merge_interface.argtypes = [c_dp, c_int, c_int, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_dp,
-                                        c_dp, c_dp, c_dp, c_dp, c_sz, c_dp, c_int, c_dp]
+                                        c_dp, c_dp, c_dp, c_dp, c_sz, c_dp, c_int, c_int, c_dp]
     lib.hps_merge_interface.restype = c_int
-    lib.hps_interface_solve.argtypes = [c_dp, c_int, c_int, c_int, c_dp, c_dp, c_dp, c_dp, c_dp, c_int, c_dp]
+    lib.hps_interface_solve.argtypes = [c_dp, c_int, c_int, c_int, c_dp, c_dp, c_dp, c_dp, c_dp, c_int, c_int, c_dp]
     lib.hps_interface_solve.restype = c_int
     lib.hps_merge_assemble.argtypes = [c_dp, c_int, c_int, c_int, c_dp, c_ll, c_dp, c_dp, c_dp, c_int, c_dp, c_dp]
     lib.hps_merge_assemble.restype = c_int

@@ -14,10 +14,10 @@
 //                      LAPACK-style (sequential swaps, ipiv) when the panel is written back;
 //                      k_swap_trsm16 applies the swaps to the other columns and solves the panel's
 //                      16-row strip inside its 128-block; the 128-row strip solve U12 = L11^-1 A12
-//                      is k_strip_solve, the rank-16 / rank-128 trailing updates the DMMA GEMM.
+//                      is the same recursive triangular solve, the trailing updates the DMMA GEMM.
 //   S = U^-1 L^-1 P R  row gather by the pivot permutation, then two recursive triangular solves
-//                      in place: the bulk as DMMA GEMMs, the 128-row diagonal strips by forward /
-//                      back substitution (k_strip_solve, one thread per column).
+//                      in place: the bulk as DMMA GEMMs, 16-row diagonal strips by forward / back
+//                      substitution in registers (k_strip16, one thread per column).
 //
 // Flops: 2/3 n^3 (LU) + 2 n^2 ne (two solves), against 2 n^3 + 2 n^2 ne for an explicit inverse.
 #include <algorithm>
@@ -249,53 +249,46 @@ __global__ void __launch_bounds__(128) k_swap_trsm16(double* A, int n, long long
   }
 }
 
-// Strip solve with a diagonal block of the LU factors: the bw-row strip B (bw <= 128, columns
-// [0, ncols); B points at its first row) <- T^-1 B, T = X[r0 : r0 + bw, r0 : r0 + bw], unit lower (LOWER) or upper. One thread
-// per column of B, its column in shared memory; T read from global memory (the same entry for
-// every thread: one broadcast transaction per warp). grid = (ceil(ncols / 64), batch).
+// Strip solve with a diagonal block of the LU factors: the w-row strip B (w <= 16, columns
+// [0, ncols); B points at its first row) <- T^-1 B, T = X[r0 : r0 + w, r0 : r0 + w], unit lower
+// (LOWER) or upper. One thread per column, the strip column and T in registers / shared memory.
 template <bool LOWER>
-__global__ void __launch_bounds__(64) k_strip_solve(const double* __restrict__ X, int n, long long strideX, int r0,
-                                                   int bw, double* __restrict__ B, long long ldb, long long strideB,
-                                                   int ncols) {
-  constexpr int S = 65;
-  extern __shared__ __align__(16) double sx[];  // [NB][S]
-  const int b = blockIdx.y, t = threadIdx.x;
-  const int col = blockIdx.x * 64 + t;
-  const bool ok = col < ncols;
+__global__ void __launch_bounds__(128) k_strip16(const double* __restrict__ X, int n, long long strideX, int r0, int w,
+                                                double* __restrict__ B, long long ldb, long long strideB, int ncols) {
+  __shared__ double sT[lu::W][lu::W + 1];
+  const int b = blockIdx.y;
   const double* T = X + (long long)b * strideX + (long long)r0 * n + r0;
-  double* Bb = B + (long long)b * strideB;  // B points at the strip's first row
-  for (int i = 0; i < bw; ++i) sx[i * S + t] = ok ? Bb[(long long)i * ldb + col] : 0.0;
+  for (int i = threadIdx.x; i < lu::W * lu::W; i += blockDim.x) {
+    const int r = i / lu::W, c = i % lu::W;
+    sT[r][c] = (r < w && c < w) ? T[(long long)r * n + c] : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= ncols) return;
+  double* Bb = B + (long long)b * strideB + col;
+  double x[lu::W];
+#pragma unroll
+  for (int r = 0; r < lu::W; ++r) x[r] = r < w ? Bb[(long long)r * ldb] : 0.0;
   if (LOWER) {
-    for (int i = 1; i < bw; ++i) {
-      const double* Ti = T + (long long)i * n;
-      double s0 = sx[i * S + t], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = 0;
-      for (; k + 3 < i; k += 4) {
-        s0 = fma(-__ldg(Ti + k), sx[k * S + t], s0);
-        s1 = fma(-__ldg(Ti + k + 1), sx[(k + 1) * S + t], s1);
-        s2 = fma(-__ldg(Ti + k + 2), sx[(k + 2) * S + t], s2);
-        s3 = fma(-__ldg(Ti + k + 3), sx[(k + 3) * S + t], s3);
-      }
-      for (; k < i; ++k) s0 = fma(-__ldg(Ti + k), sx[k * S + t], s0);
-      sx[i * S + t] = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int r = 1; r < lu::W; ++r) {
+      double s = x[r];
+#pragma unroll
+      for (int k = 0; k < r; ++k) s = fma(-sT[r][k], x[k], s);
+      x[r] = s;
     }
   } else {
-    for (int i = bw - 1; i >= 0; --i) {
-      const double* Ti = T + (long long)i * n;
-      double s0 = sx[i * S + t], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = i + 1;
-      for (; k + 3 < bw; k += 4) {
-        s0 = fma(-__ldg(Ti + k), sx[k * S + t], s0);
-        s1 = fma(-__ldg(Ti + k + 1), sx[(k + 1) * S + t], s1);
-        s2 = fma(-__ldg(Ti + k + 2), sx[(k + 2) * S + t], s2);
-        s3 = fma(-__ldg(Ti + k + 3), sx[(k + 3) * S + t], s3);
-      }
-      for (; k < bw; ++k) s0 = fma(-__ldg(Ti + k), sx[k * S + t], s0);
-      sx[i * S + t] = ((s0 + s1) + (s2 + s3)) / __ldg(Ti + i);
+#pragma unroll
+    for (int r = lu::W - 1; r >= 0; --r) {
+      double s = x[r];
+#pragma unroll
+      for (int k = r + 1; k < lu::W; ++k) s = fma(-sT[r][k], x[k], s);
+      x[r] = s / sT[r][r];
     }
   }
-  if (ok)
-    for (int i = 0; i < bw; ++i) Bb[(long long)i * ldb + col] = sx[i * S + t];
+#pragma unroll
+  for (int r = 0; r < lu::W; ++r)
+    if (r < w) Bb[(long long)r * ldb] = x[r];
 }
 
 // perm[i] = original row that ends at position i after the sequential swaps ipiv (one thread per
@@ -350,17 +343,33 @@ LuWs lu_ws(void* base, int n, int batch) {
 
 size_t lu_ws_bytes(int n, int batch) { return sizeof(int) * 2 * (size_t)batch * n + 64; }
 
-template <bool LOWER>
-static int strip_solve(Ctx& cx, const double* X, int n, int batch, int r0, int bw, double* B, long long ldb,
-                       long long sB, int ncols, cudaStream_t st) {
-  if (ncols <= 0 || bw <= 0) return HPS_OK;
-  const int smem = (int)(sizeof(double) * lu::NB * 65);
-  const int as = ensure_smem_attr((const void*)k_strip_solve<LOWER>, cx.device, smem);
-  if (as != HPS_OK) return as;
-  k_strip_solve<LOWER><<<dim3((ncols + 63) / 64, batch), 64, smem, st>>>(X, n, (long long)n * n, r0, bw, B, ldb, sB,
-                                                                          ncols);
-  HPS_LAUNCH_CHECK();
-  return HPS_OK;
+// B (w rows of ncols, row stride ldb, batch stride sB) <- T^-1 B for T = X[r0 : r0 + w, r0 : r0 + w]
+// (unit lower or upper), recursively: the bulk as DMMA GEMMs, 16-row strips by k_strip16.
+static int trsm(Ctx& cx, bool lower, const double* X, int n, int batch, int r0, int w, double* B, long long ldb,
+                long long sB, int ncols, cudaStream_t st) {
+  if (w <= 0 || ncols <= 0) return HPS_OK;
+  const long long sX = (long long)n * n;
+  if (w <= lu::W) {
+    if (lower)
+      k_strip16<true><<<dim3((ncols + 127) / 128, batch), 128, 0, st>>>(X, n, sX, r0, w, B, ldb, sB, ncols);
+    else
+      k_strip16<false><<<dim3((ncols + 127) / 128, batch), 128, 0, st>>>(X, n, sX, r0, w, B, ldb, sB, ncols);
+    HPS_LAUNCH_CHECK();
+    return HPS_OK;
+  }
+  const int nb = (w + lu::W - 1) / lu::W;
+  const int h = ((nb + 1) / 2) * lu::W;
+  double* B2 = B + (long long)h * ldb;
+  if (lower) {
+    LU_TRY(trsm(cx, true, X, n, batch, r0, h, B, ldb, sB, ncols, st));
+    LU_TRY(gemm(cx, w - h, ncols, h, batch, -1.0, X + (long long)(r0 + h) * n + r0, n, sX, B, ldb, sB, 1.0, B2, ldb,
+                sB, st));
+    return trsm(cx, true, X, n, batch, r0 + h, w - h, B2, ldb, sB, ncols, st);
+  }
+  LU_TRY(trsm(cx, false, X, n, batch, r0 + h, w - h, B2, ldb, sB, ncols, st));
+  LU_TRY(gemm(cx, h, ncols, w - h, batch, -1.0, X + (long long)r0 * n + r0 + h, n, sX, B2, ldb, sB, 1.0, B, ldb, sB,
+              st));
+  return trsm(cx, false, X, n, batch, r0, h, B, ldb, sB, ncols, st);
 }
 
 static int launch_panel(Ctx& cx, double* X, int n, int batch, int c0, int w, int* ipiv, int* status,
@@ -415,7 +424,7 @@ int lu_factor(Ctx& cx, double* X, int n, int batch, const LuWs& ws, int* status,
     if (right > 0) {
       // U12 = L11^-1 A12, then the rank-bw update of the trailing matrix
       double* A12 = X + (long long)c * n + c + bw;
-      LU_TRY(strip_solve<true>(cx, X, n, batch, c, bw, A12, n, sX, right, st));
+      LU_TRY(trsm(cx, true, X, n, batch, c, bw, A12, n, sX, right, st));
       LU_TRY(gemm(cx, right, right, bw, batch, -1.0, X + (long long)(c + bw) * n + c, n, sX, A12, n, sX, 1.0,
                   X + (long long)(c + bw) * n + c + bw, n, sX, st));
     }
@@ -423,30 +432,6 @@ int lu_factor(Ctx& cx, double* X, int n, int batch, const LuWs& ws, int* status,
   k_ipiv_to_perm<<<batch, 32, 0, st>>>(ws.ipiv, n, ws.perm);
   HPS_LAUNCH_CHECK();
   return HPS_OK;
-}
-
-// B (rows [r0, r0 + w) of the n x ne right-hand side, in place) <- L^-1 B, recursively: the bulk as
-// GEMMs, 128-row strips by substitution.
-static int trsm_lower(Ctx& cx, const double* X, int n, int batch, double* B, int ne, int r0, int w, cudaStream_t st) {
-  const long long sX = (long long)n * n, sB = (long long)n * ne;
-  if (w <= lu::NB) return strip_solve<true>(cx, X, n, batch, r0, w, B + (long long)r0 * ne, ne, sB, ne, st);
-  const int nb = (w + lu::NB - 1) / lu::NB;
-  const int h = ((nb + 1) / 2) * lu::NB;
-  LU_TRY(trsm_lower(cx, X, n, batch, B, ne, r0, h, st));
-  LU_TRY(gemm(cx, w - h, ne, h, batch, -1.0, X + (long long)(r0 + h) * n + r0, n, sX, B + (long long)r0 * ne, ne, sB,
-              1.0, B + (long long)(r0 + h) * ne, ne, sB, st));
-  return trsm_lower(cx, X, n, batch, B, ne, r0 + h, w - h, st);
-}
-
-static int trsm_upper(Ctx& cx, const double* X, int n, int batch, double* B, int ne, int r0, int w, cudaStream_t st) {
-  const long long sX = (long long)n * n, sB = (long long)n * ne;
-  if (w <= lu::NB) return strip_solve<false>(cx, X, n, batch, r0, w, B + (long long)r0 * ne, ne, sB, ne, st);
-  const int nb = (w + lu::NB - 1) / lu::NB;
-  const int h = ((nb + 1) / 2) * lu::NB;
-  LU_TRY(trsm_upper(cx, X, n, batch, B, ne, r0 + h, w - h, st));
-  LU_TRY(gemm(cx, h, ne, w - h, batch, -1.0, X + (long long)r0 * n + r0 + h, n, sX, B + (long long)(r0 + h) * ne, ne,
-              sB, 1.0, B + (long long)r0 * ne, ne, sB, st));
-  return trsm_upper(cx, X, n, batch, B, ne, r0, h, st);
 }
 
 __global__ void k_nonfinite_rows(const double* __restrict__ S, long long per, int* status, int status_base) {
@@ -465,8 +450,8 @@ int lu_solve(Ctx& cx, const double* X, int n, int batch, const LuWs& ws, const d
   const long long sB = (long long)n * ne;
   k_permute_rows<<<dim3((n + 7) / 8, batch), 256, 0, st>>>(R, sB, ws.perm, n, ne, S_out, sB);
   HPS_LAUNCH_CHECK();
-  LU_TRY(trsm_lower(cx, X, n, batch, S_out, ne, 0, n, st));
-  LU_TRY(trsm_upper(cx, X, n, batch, S_out, ne, 0, n, st));
+  LU_TRY(trsm(cx, true, X, n, batch, 0, n, S_out, ne, sB, ne, st));
+  LU_TRY(trsm(cx, false, X, n, batch, 0, n, S_out, ne, sB, ne, st));
   if (status) {
     k_nonfinite_rows<<<dim3((unsigned)std::min<long long>(cx.sms, (sB + 255) / 256), batch), 256, 0, st>>>(
         S_out, sB, status, status_base);

@@ -674,21 +674,74 @@ static size_t inverse_rec_tmp_doubles(int n, int batch) {
 
 // Merge workspace of one depth: X (inverted in place for n3 <= 128, LU-factored for n3 > 128), R,
 // C, the LU pivots (n3 > 128) and the per-merge deflation shifts.
+// Merge workspace of one depth: X (inverted in place, or LU-factored with pivoting), R, C; for
+// n3 > 128 also the probe image w = X_d v of the inverse's residual check, the block-inverse
+// recursion's temporaries and the LU pivots; the per-merge deflation shifts.
 struct MergeWs {
   double *X, *R, *C;
+  double *probe = nullptr, *rtmp = nullptr;
   LuWs lu;
   unsigned long long* diagmax;
 };
-static size_t lu_bytes_aligned(int n3, int nbatch) { return n3 > 128 ? (lu_ws_bytes(n3, nbatch) + 255) & ~size_t(255) : 0; }
+static size_t merge_aux_bytes(int nbatch, int n3) {
+  if (n3 <= 128) return 0;
+  const size_t d = (size_t)nbatch * n3 + inverse_rec_tmp_doubles(n3, nbatch);
+  return ((d * sizeof(double) + lu_ws_bytes(n3, nbatch)) + 255) & ~size_t(255);
+}
 static MergeWs merge_ws(void* ws, int nbatch, int n3, int ne) {
   MergeWs w;
   w.X = static_cast<double*>(ws);
   w.R = w.X + (size_t)nbatch * n3 * n3;
   w.C = w.R + (size_t)nbatch * n3 * ne;
-  char* aux = reinterpret_cast<char*>(w.C + (size_t)nbatch * ne * n3);
-  if (n3 > 128) w.lu = lu_ws(aux, n3, nbatch);
-  w.diagmax = reinterpret_cast<unsigned long long*>(aux + lu_bytes_aligned(n3, nbatch));
+  double* aux = w.C + (size_t)nbatch * ne * n3;
+  if (n3 > 128) {
+    w.probe = aux;
+    w.rtmp = w.probe + (size_t)nbatch * n3;
+    w.lu = lu_ws(w.rtmp + inverse_rec_tmp_doubles(n3, nbatch), n3, nbatch);
+  }
+  w.diagmax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(aux) + merge_aux_bytes(nbatch, n3));
   return w;
+}
+
+// Residual check of the fast block inverse (n3 > 128). Before the inversion w = X_d v for a fixed
+// +-1 probe v (k_resid_image); afterwards r = X_d^-1 w - v (k_resid_check, in the same call, or in the
+// parent depth's call when the look-ahead inverted X, so the check stays off the look-ahead's
+// critical path). The recursive 2x2 block inverse pivots only inside 128-blocks, so a near-singular
+// leading block would go unnoticed; max|r| above 1e-6 (or non-finite) raises the merge's status word
+// to HPS_STATUS_PIVOT + b and the host re-runs that depth with the pivoted LU. One warp per row.
+__device__ __forceinline__ double probe_v(int i) { return ((i * 2654435761u) >> 13) & 1 ? 1.0 : -1.0; }
+__global__ void k_resid_image(const double* __restrict__ X, int n, double* __restrict__ w) {
+  const int b = blockIdx.y;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const double* Xr = X + ((long long)b * n + r) * n;
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) s = fma(Xr[c], probe_v(c), s);
+  s = warp_sum(s);
+  if (lane == 0) w[(long long)b * n + r] = s;
+}
+__global__ void k_resid_check(const double* __restrict__ Xi, int n, const double* __restrict__ w, int* status,
+                              int status_base) {
+  const int b = blockIdx.y;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const double* Xr = Xi + ((long long)b * n + r) * n;
+  const double* wb = w + (long long)b * n;
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) s = fma(Xr[c], wb[c], s);
+  s = warp_sum(s) - probe_v(r);
+  if (lane == 0 && !(fabs(s) <= 1e-6) && status) atomicMax(status, HPS_STATUS_PIVOT + status_base + b);
+}
+static int resid_image(const MergeWs& W, const double* X, int n3, int nbatch, cudaStream_t st) {
+  k_resid_image<<<dim3((n3 + 7) / 8, nbatch), 256, 0, st>>>(X, n3, W.probe);
+  HPS_LAUNCH_CHECK();
+  return HPS_OK;
+}
+static int resid_check(const MergeWs& W, const double* Xi, int n3, int nbatch, int* status, int status_base,
+                       cudaStream_t st) {
+  k_resid_check<<<dim3((n3 + 7) / 8, nbatch), 256, 0, st>>>(Xi, n3, W.probe, status, status_base);
+  HPS_LAUNCH_CHECK();
+  return HPS_OK;
 }
 
 }  // namespace hps
@@ -697,7 +750,7 @@ using namespace hps;
 
 extern "C" size_t hps_merge_workspace_bytes(int nbatch, int n3, int ne) {
   const size_t d = size_t(nbatch) * (size_t(n3) * n3 + 2ull * n3 * ne + 1);
-  return d * sizeof(double) + lu_bytes_aligned(n3, nbatch) + 256;
+  return d * sizeof(double) + merge_aux_bytes(nbatch, n3) + 256;
 }
 
 // HPS_OPT_PROFILE_AHEAD (eager builds only, dev tool): timing events at the look-ahead fork (0),
@@ -733,7 +786,7 @@ struct AheadArgs {
 static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, const double* T_child, long long child_stride,
                             const int* child_idx, const int* maps, const double* vmode, double* S_out, double* T_out,
                             void* ws, size_t ws_bytes, int* status, int status_base, bool pre_inverted,
-                            const AheadArgs* ah, cudaStream_t st) {
+                            const AheadArgs* ah, cudaStream_t st, int flags = 0) {
   if (nbatch <= 0) return HPS_OK;
   if (ne % 2 || n3 % q || m != ne / 2 + n3 || ws_bytes < hps_merge_workspace_bytes(nbatch, n3, ne)) {
     set_error("hps_merge_level: bad arguments n3=%d ne=%d m=%d q=%d ws=%zu", n3, ne, m, q, ws_bytes);
@@ -749,7 +802,11 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
   double* R = W.R;
   double* Cm = W.C;
   unsigned long long* diagmax = W.diagmax;
-  const bool big = n3 > 128;  // pivoted LU + triangular solves; else in-register Gauss-Jordan inverse
+  // n3 <= 128: in-register Gauss-Jordan inverse (partial pivoting over the whole matrix). n3 > 128:
+  // the recursive block inverse with its residual check (fast; HPS_MERGE_PIVOTED unset), or the
+  // pivoted LU + triangular solves (HPS_MERGE_PIVOTED: what the host asks for after a failed check).
+  const bool big = n3 > 128 && (flags & HPS_MERGE_PIVOTED);
+  const bool checked = n3 > 128 && !big;
   const bool deflate = n3 > q;  // deflate the n3/q - 1 corner null modes
   ChildRef ch{T_child, child_stride, child_idx, m};
   if (!pre_inverted && deflate) HPS_CUDA_CHECK(cudaMemsetAsync(diagmax, 0, sizeof(unsigned long long) * nbatch, st));
@@ -764,14 +821,20 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
   else
     k_gather_c_rows<<<dim3(nbatch, (ne + 7) / 8), 256, 0, st>>>(ch, j1a, j2b, j3a, j3b, n3, ne, Cm);
   HPS_LAUNCH_CHECK();
+  if (pre_inverted && checked)  // the look-ahead inverted X: its residual check runs here
+    HPS_TRY(resid_check(W, X, n3, nbatch, status, status_base, st));
   if (!pre_inverted) {
     if (deflate) {
       k_deflate<<<dim3(nbatch, n3 / q), 256, 0, st>>>(X, n3, q, vmode, vmode + q, diagmax);
       HPS_LAUNCH_CHECK();
     }
-    if (big)
+    if (big) {
       HPS_TRY(lu_factor(cx, X, n3, nbatch, W.lu, status, status_base, st));
-    else
+    } else if (checked) {
+      HPS_TRY(resid_image(W, X, n3, nbatch, st));
+      HPS_TRY(inverse_rec(cx, X, n3, (long long)n3 * n3, n3, nbatch, W.rtmp, status, status_base, st));
+      HPS_TRY(resid_check(W, X, n3, nbatch, status, status_base, st));
+    } else
       HPS_TRY(inverse_small(X, n3, (long long)n3 * n3, n3, nbatch, status, status_base, st));
   }
   if (!S_out) return HPS_OK;  // interface only (hps_merge_interface): X factored, R and C gathered
@@ -823,8 +886,13 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
       k_deflate<<<dim3(P, pn3 / q), 256, 0, cx.ahead>>>(pX, pn3, q, ah->pvmode, ah->pvmode + q, pdiag);
       HPS_LAUNCH_CHECK();
     }
-    if (pn3 > 128)
+    if (pn3 > 128 && (flags & HPS_MERGE_PARENT_PIVOTED))
       HPS_TRY(lu_factor(cx, pX, pn3, P, PW.lu, ah->pstatus, ah->pstatus_base, cx.ahead));
+    else if (pn3 > 128) {  // residual image now, the check in the parent's call
+      HPS_TRY(resid_image(PW, pX, pn3, P, cx.ahead));
+      HPS_TRY(inverse_rec(cx, pX, pn3, (long long)pn3 * pn3, pn3, P, PW.rtmp, ah->pstatus, ah->pstatus_base, cx.ahead,
+                          cx.ahead_side));
+    }
     else
       HPS_TRY(inverse_small(pX, pn3, (long long)pn3 * pn3, pn3, P, ah->pstatus, ah->pstatus_base, cx.ahead));
     ahead_probe(cx, 1, cx.ahead);
@@ -857,12 +925,12 @@ extern "C" int hps_merge_level_ahead(hps_ctx_t ctx, int nbatch, int n3, int ne, 
                                      const double* vmode, double* S_out, double* T_out, void* ws, size_t ws_bytes,
                                      int* status, int status_base, int pre_inverted, const int* pmaps, int pn3,
                                      int pne, const double* pvmode, void* pws, size_t pws_bytes, int* pstatus,
-                                     int pstatus_base, void* stream) {
+                                     int pstatus_base, int flags, void* stream) {
   HPS_CTX(cx, ctx);
   AheadArgs ah{pmaps, pn3, pne, pvmode, pws, pws_bytes, pstatus, pstatus_base};
   return merge_level_impl(*cx, nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, S_out, T_out, ws,
                           ws_bytes, status, status_base, pre_inverted != 0, pmaps ? &ah : nullptr,
-                          static_cast<cudaStream_t>(stream));
+                          static_cast<cudaStream_t>(stream), flags);
 }
 
 // Batched in-place inverse (n <= 128 uses the register Gauss-Jordan kernel directly, larger n the
@@ -918,18 +986,19 @@ __global__ void k_merge_assemble(ChildRef ch, const int* __restrict__ j1a, const
 extern "C" int hps_merge_interface(hps_ctx_t ctx, int nbatch, int n3, int ne, int m, int q, const double* T_child,
                                    long long child_stride, const int* child_idx, const int* maps, const double* vmode,
                                    double* Xf_out, int* perm_out, double* R_out, double* C_out, void* ws,
-                                   size_t ws_bytes, int* status, int status_base, void* stream) {
+                                   size_t ws_bytes, int* status, int status_base, int flags, void* stream) {
   HPS_CTX(cx, ctx);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   HPS_TRY(merge_level_impl(*cx, nbatch, n3, ne, m, q, T_child, child_stride, child_idx, maps, vmode, nullptr,
-                           nullptr, ws, ws_bytes, status, status_base, false, nullptr, st));
+                           nullptr, ws, ws_bytes, status, status_base, false, nullptr, st, flags));
+  const bool lu_form = n3 > 128 && (flags & HPS_MERGE_PIVOTED);
   const MergeWs W = merge_ws(ws, nbatch, n3, ne);
   const size_t nX = (size_t)nbatch * n3 * n3, nR = (size_t)nbatch * n3 * ne;
   if (Xf_out) HPS_CUDA_CHECK(cudaMemcpyAsync(Xf_out, W.X, nX * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (R_out) HPS_CUDA_CHECK(cudaMemcpyAsync(R_out, W.R, nR * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (C_out) HPS_CUDA_CHECK(cudaMemcpyAsync(C_out, W.C, nR * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (perm_out) {
-    if (n3 > 128) {
+    if (lu_form) {
       HPS_CUDA_CHECK(cudaMemcpyAsync(perm_out, W.lu.perm, (size_t)nbatch * n3 * sizeof(int), cudaMemcpyDeviceToDevice, st));
     } else {
       k_iota_rows<<<std::max(1, std::min(1024, (n3 * nbatch + 255) / 256)), 256, 0, st>>>(perm_out, n3, nbatch);
@@ -940,14 +1009,15 @@ extern "C" int hps_merge_interface(hps_ctx_t ctx, int nbatch, int n3, int ne, in
 }
 
 extern "C" int hps_interface_solve(hps_ctx_t ctx, int n3, int ncols, int batch, const double* Xf, const int* perm,
-                                   const double* R, double* S_out, int* status, int status_base, void* stream) {
+                                   const double* R, double* S_out, int* status, int status_base, int flags,
+                                   void* stream) {
   HPS_CTX(cx, ctx);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (n3 <= 0 || ncols <= 0 || batch <= 0) {
     set_error("hps_interface_solve: bad arguments n3=%d ncols=%d", n3, ncols);
     return HPS_ERR_ARG;
   }
-  if (n3 <= 128)
+  if (!(n3 > 128 && (flags & HPS_MERGE_PIVOTED)))  // Xf is the explicit inverse
     return gemm(*cx, n3, ncols, n3, batch, 1.0, Xf, n3, (long long)n3 * n3, R, ncols, (long long)n3 * ncols, 0.0,
                 S_out, ncols, (long long)n3 * ncols, st, status);
   LuWs w;

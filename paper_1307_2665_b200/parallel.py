@@ -129,7 +129,7 @@ class CudaBackend:
                                          _native.stream_ptr()), "hps_leaf_stage")
         return Psi, T, cond
 
-    def merge_level(self, d, nbatch, child_T, child_idx, status, parent_status=None):
+    def merge_level(self, d, nbatch, child_T, child_idx, status, parent_status=None, pivoted=()):
         """One depth's merges for this rank's slots. With `parent_status` (the next call merges
         these boxes' parents on this rank), the look-ahead inverse of solver.build_device runs too
         (hps_merge_level_ahead, where solver.lookahead_depths applies); the next call then starts
@@ -158,12 +158,12 @@ class CudaBackend:
                                                 dl.m * dl.m, _native.ptr(idx), _native.ptr(self.dl.maps[d]),
                                                 _native.ptr(self.dl.vmode[d]), _native.ptr(S), _native.ptr(T),
                                                 _native.ptr(ws), wsb, _native.ptr(status), 0, int(pre), *pargs,
-                                                _native.stream_ptr()),
+                                                _merge_flags(d, pivoted), _native.stream_ptr()),
                       f"hps_merge_level(depth {d})")
         return S, T
 
     # -- split merge of the distributed top depths (hps_merge_interface / _interface_solve / _assemble) --
-    def merge_interface(self, d, children, status):
+    def merge_interface(self, d, children, status, pivoted=()):
         """Gathers, deflation and factorisation of one parent's interface system. Returns the
         factored X (inverse for n3 <= 128, L\\U for n3 > 128), its row permutation, R and C."""
         lib, torch = self.lib, self.torch
@@ -178,16 +178,18 @@ class CudaBackend:
         _native.check(lib.hps_merge_interface(self.ctx, 1, n3, ne, m, self.lay.q, _native.ptr(children), m * m, None,
                                               _native.ptr(self.dl.maps[d]), _native.ptr(self.dl.vmode[d]),
                                               _native.ptr(Xf), _native.ptr(perm), _native.ptr(R), _native.ptr(C),
-                                              _native.ptr(ws), wsb, _native.ptr(status), 0, _native.stream_ptr()),
+                                              _native.ptr(ws), wsb, _native.ptr(status), 0,
+                                              _merge_flags(d, pivoted), _native.stream_ptr()),
                       f"hps_merge_interface(depth {d})")
         return Xf, perm, R, C
 
-    def interface_solve(self, d, Xf, perm, Rp, status):
+    def interface_solve(self, d, Xf, perm, Rp, status, pivoted=()):
         n3, w = Rp.shape[1], Rp.shape[2]
         Sp = self.empty((1, n3, w))
         _native.check(self.lib.hps_interface_solve(self.ctx, n3, w, 1, _native.ptr(Xf), _native.ptr(perm),
                                                    _native.ptr(Rp), _native.ptr(Sp), _native.ptr(status), 0,
-                                                   _native.stream_ptr()), f"hps_interface_solve(depth {d})")
+                                                   _merge_flags(d, pivoted), _native.stream_ptr()),
+                      f"hps_interface_solve(depth {d})")
         return Sp
 
     def panel_gemm(self, C, Sp):
@@ -319,12 +321,19 @@ def prepare_distributed(tree, coeffs, rank, world, backend):
     return LocalInputs(local_fields, scalars, reps, gid)
 
 
-def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels", check=True):
+def _merge_flags(d, pivoted):
+    return (_native.HPS_MERGE_PIVOTED if d in pivoted else 0) | \
+        (_native.HPS_MERGE_PARENT_PIVOTED if d - 1 in pivoted else 0)
+
+
+def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels", check=True, pivoted=()):
     """Subtree-parallel build. `comm` provides rank, world, send(tensor, dst), recv(tensor, src).
     `inputs` (from prepare_distributed) skips the host sampling/grouping. `top_mode` is "panels"
     (the top merges' solves and T GEMMs split in column panels over the parent's group) or "owner"
     (the parent's owner merges alone). With check=True every rank raises the reference's exception
-    for the first failure in the reference's order (check_distributed)."""
+    for the first failure in the reference's order (check_distributed), and depths whose fast
+    interface inverse failed its residual check are rebuilt on the pivoted LU (`pivoted`)."""
+    pivoted = frozenset(pivoted)
     lay = layout_of(tree)
     L = lay.L
     plan = subtree_plan(L, comm.world)
@@ -351,7 +360,7 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels
         pstatus = None
         if d - 1 >= s:
             pstatus = ahead_status[d - 1] = backend.status_word()
-        S, T = backend.merge_level(d, b - a, child_T, child_idx, status, parent_status=pstatus)
+        S, T = backend.merge_level(d, b - a, child_T, child_idx, status, parent_status=pstatus, pivoted=pivoted)
         st.S_local[d] = S
         child_T, child_idx = T, None
     if s == 2 * L:  # one leaf per rank
@@ -386,7 +395,7 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels
             if rank == owner:
                 status = backend.status_word()
                 st.statuses.append((d, k, status))
-                S, T = backend.merge_level(d, 1, backend.stack2(cur, other), None, status)
+                S, T = backend.merge_level(d, 1, backend.stack2(cur, other), None, status, pivoted=pivoted)
                 st.S_top[d] = S
                 cur = T
             continue
@@ -395,7 +404,7 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels
         st.statuses.append((d, k, status))
         if rank == owner:
             children = backend.stack2(cur, other)
-            Xf, perm, R, C = backend.merge_interface(d, children, status)
+            Xf, perm, R, C = backend.merge_interface(d, children, status, pivoted=pivoted)
             for r in range(1, P):
                 comm.send(Xf, owner + r)
                 comm.send(perm, owner + r)
@@ -407,7 +416,7 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels
             C, Rp = backend.empty((1, ne, n3)), backend.empty((1, n3, w))
             for t in (Xf, perm, C, Rp):
                 comm.recv(t, owner)
-        Sp = backend.interface_solve(d, Xf, perm, Rp, status)
+        Sp = backend.interface_solve(d, Xf, perm, Rp, status, pivoted=pivoted)
         Tp = backend.panel_gemm(C, Sp)
         if rank == owner:
             Tps, Sps = [Tp], [Sp]
@@ -426,7 +435,9 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels
     if rank == 0:
         st.root_T = cur
     if check:
-        check_distributed(st, comm)
+        retry = check_distributed(st, comm) - pivoted
+        if retry:
+            return build_distributed(tree, coeffs, comm, backend, inputs, top_mode, check, pivoted | retry)
     return st
 
 
@@ -434,7 +445,8 @@ def check_distributed(st, comm):
     """Raise on every rank the exception the single-process build would raise: LeafResonanceError for
     the first resonant leaf group (smallest global leaf index of a bad group's first leaf), else
     MergeResonanceError for the first failing merge in the reference's order (deepest first,
-    highest box index first; solver.py:235-239, 280-281). One host sync and a min-reduction."""
+    highest box index first; solver.py:235-239, 280-281). One host sync and a min-reduction.
+    Returns the depths (on any rank) whose fast interface inverse failed its residual check."""
     from .errors import LeafResonanceError, MergeResonanceError
     from .solver import RESONANCE_COND
 
@@ -448,18 +460,23 @@ def check_distributed(st, comm):
         g = int(bad[0])
         leaf = lo + int(st.reps[g])
         key, info = leaf, float(cond[g])
-    else:
-        boxes = [(1 << d) - 1 + k + v for d, k, v in statuses if v >= 0]
+    retry = {d for d, k, v in statuses if v >= _native.HPS_STATUS_PIVOT}
+    if not bad.size:
+        boxes = [(1 << d) - 1 + k + v for d, k, v in statuses if 0 <= v < _native.HPS_STATUS_PIVOT]
         if boxes:
             box = max(boxes)
             key = n_leaf + ((1 << (2 * lay.L + 1)) - 1 - box)
-    keys = comm.allgather_obj((key, info))
-    key, info = min(keys, key=lambda x: x[0])
+    keys = comm.allgather_obj((key, info, sorted(retry)))
+    retry = set().union(*[set(k[2]) for k in keys])
+    key, info = min(((k[0], k[1]) for k in keys), key=lambda x: x[0])
+    if retry and key >= n_leaf:
+        return retry  # rebuild first: a merge failure may be a consequence of the inaccurate inverse
     if key < n_leaf:
         raise LeafResonanceError(box=n_leaf - 1 + key, cond=info)
     if key < n_leaf + (1 << (2 * lay.L + 1)):
         box = (1 << (2 * lay.L + 1)) - 1 - (key - n_leaf)
         raise MergeResonanceError(box=box, detail="non-finite solution operator")
+    return retry
 
 
 def solve_distributed(st, F, comm):

@@ -528,11 +528,13 @@ def lookahead_depths(lay):
 
 
 def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_threshold=math.inf,
-                 hbs_leaf_size=64, stage_begin=None, ctx=None):
+                 hbs_leaf_size=64, stage_begin=None, ctx=None, pivoted=()):
     """Enqueue the leaf stage and every merge level on the current stream (no host sync).
     `stage_begin(name)`, if given, is called before each stage ("leaf", "merge_d<d>"): BuildGraph
     uses it to capture one CUDA graph per stage. `ctx` is the library context (_native.Context;
-    default: slot 0 of the current device); builds in flight at the same time need different ones."""
+    default: slot 0 of the current device); builds in flight at the same time need different ones.
+    `pivoted`: depths whose interface systems (n3 > 128) are factored by the pivoted LU instead of
+    the residual-checked block inverse (check_build returns the depths whose check failed)."""
     if stage_begin is not None:
         stage_begin("leaf")
     torch = _torch()
@@ -576,6 +578,7 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
     # parent depth's X beside its own T GEMM (rule in _ahead_params; HPS_AHEAD_MIN_N3=0 disables).
     # The parent's workspace is allocated one depth early.
     ahead = lookahead_depths(lay)
+    pivoted = frozenset(pivoted)
     ws_next, pre_inv = None, False
     for d in range(2 * L - 1, -1, -1):
         if stage_begin is not None:
@@ -598,13 +601,13 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
                 _native.ptr(dl.maps[d]), _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T), _native.ptr(ws),
                 wsb, status_d, 0, int(pre_inv), _native.ptr(dl.maps[d - 1]), pl.n3, pl.ne,
                 _native.ptr(dl.vmode[d - 1]), _native.ptr(ws_next), pwsb, ctypes_vp(status.data_ptr() + 4 * (d - 1)),
-                0, stream), f"hps_merge_level_ahead(depth {d})")
+                0, _merge_flags(d, pivoted), stream), f"hps_merge_level_ahead(depth {d})")
             next_pre = True
         else:
             _native.check(lib.hps_merge_level_ahead(
                 cx, nbatch, n3, ne, m, q, _native.ptr(child_T), child_stride, _native.ptr(child_idx),
                 _native.ptr(dl.maps[d]), _native.ptr(dl.vmode[d]), _native.ptr(S), _native.ptr(T), _native.ptr(ws),
-                wsb, status_d, 0, int(pre_inv), None, 0, 0, None, None, 0, None, 0, stream),
+                wsb, status_d, 0, int(pre_inv), None, 0, 0, None, None, 0, None, 0, _merge_flags(d, pivoted), stream),
                 f"hps_merge_level(depth {d})")
             next_pre = False
         pre_inv = next_pre
@@ -627,7 +630,13 @@ def build_device(inp, *, keep_level_T=False, timeline=None, eps=1e-10, switch_th
     state._status = status
     state._cond = cond
     state._reps = inp.reps
+    state._pivoted = pivoted
     return state
+
+
+def _merge_flags(d, pivoted):
+    return (_native.HPS_MERGE_PIVOTED if d in pivoted else 0) | \
+        (_native.HPS_MERGE_PARENT_PIVOTED if d - 1 in pivoted else 0)
 
 
 def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size=64, *, device=None,
@@ -642,11 +651,25 @@ def build(tree, nodeset, coeffs, eps=1e-10, switch_threshold=2000, hbs_leaf_size
     if switch_threshold is None:
         switch_threshold = math.inf
     inp = prepare(tree, nodeset, coeffs, device=device)
-    state = build_device(inp, keep_level_T=keep_level_T, timeline=timeline, eps=eps,
-                         switch_threshold=switch_threshold, hbs_leaf_size=hbs_leaf_size)
+    kw = dict(keep_level_T=keep_level_T, timeline=timeline, eps=eps, switch_threshold=switch_threshold,
+              hbs_leaf_size=hbs_leaf_size)
+    state = build_device(inp, **kw)
     if check:
-        check_build(state)
+        state = checked(state, inp, **kw)
     return state
+
+
+def checked(state, inp, **build_kw):
+    """check_build, and where a depth's residual check failed, rebuild with those depths on the
+    pivoted LU (at most once per depth) until every check passes. Returns the final state."""
+    pivoted = set(getattr(state, "_pivoted", ()))
+    while True:
+        retry = check_build(state) - pivoted
+        if not retry:
+            return state
+        pivoted |= retry
+        instrumentation.bump("pivoted_rebuild")
+        state = build_device(inp, pivoted=pivoted, **build_kw)
 
 
 def _marker(timeline, name):
@@ -665,8 +688,10 @@ def _marker(timeline, name):
 
 
 def check_build(state):
-    """Read back the device status words and raise the reference's exceptions (one host sync)."""
-    _raise_from_status(state, state._cond.cpu().numpy(), state._status.cpu().numpy())
+    """Read back the device status words and raise the reference's exceptions (one host sync).
+    Returns the set of depths whose fast interface inverse failed its residual check (to rebuild
+    with pivoted=...; `build` and `checked` do that); empty normally."""
+    return _raise_from_status(state, state._cond.cpu().numpy(), state._status.cpu().numpy())
 
 
 def _raise_from_status(state, cond, st):
@@ -675,9 +700,11 @@ def _raise_from_status(state, cond, st):
         j = int(bad[0])
         leaf_index = (1 << (2 * state.layout.L)) - 1 + int(state._reps[j])
         raise LeafResonanceError(box=leaf_index, cond=float(cond[j]))
+    retry = {d for d in range(len(st)) if st[d] >= _native.HPS_STATUS_PIVOT}
     for d in range(len(st) - 1, -1, -1):  # reference merges deepest (highest index) first
-        if st[d] >= 0:
+        if 0 <= st[d] < _native.HPS_STATUS_PIVOT and not retry:
             raise MergeResonanceError(box=(1 << d) - 1 + int(st[d]), detail="non-finite solution operator")
+    return retry
 
 
 # ----------------------------------------------------------------------------------------------
@@ -836,6 +863,7 @@ class Pipeline:
                     else:
                         st = build_device(inp, ctx=cx)
                         U = solve_device(st, Fd, ctx=cx)
+                    st._job = (inp, Fd)  # for a pivoted rebuild (_finish)
                     solved = torch.cuda.Event()
                     solved.record(main)
                 # results and status words come back on their own stream, so the next job's build
@@ -882,11 +910,18 @@ class Pipeline:
                 return None
         return g
 
-    @staticmethod
-    def _finish(st, outs, done):
+    def _finish(self, st, outs, done):
         done.synchronize()
         U_host, cond, status = outs
-        _raise_from_status(st, cond.numpy(), status.numpy())
+        retry = _raise_from_status(st, cond.numpy(), status.numpy())
+        if retry:
+            # a fast interface inverse failed its residual check: rebuild this job with the pivoted
+            # LU at those depths and solve again (eager, on the main stream; rare)
+            torch = _torch()
+            inp, Fd = st._job
+            with torch.cuda.device(self.device), torch.cuda.stream(self._main):
+                st = checked(build_device(inp, pivoted=retry), inp)
+                U_host = solve_device(st, Fd).cpu()
         instrumentation.bump("solve")
         return U_host, st
 
@@ -912,13 +947,15 @@ class BuildGraph:
 
     _warmed = set()
 
-    def __init__(self, inp, nrhs=0, ctx_slot=0):
+    def __init__(self, inp, nrhs=0, ctx_slot=0, pivoted=()):
         torch = _torch()
         lib = _native.load()
         # the library context (side streams, split-K scratch) this capture bakes in: two graphs
         # replayed at once on two streams need different ones, see Pipeline(streams=2)
         self.ctx_slot = int(ctx_slot)
         self.ctx = _native.context(self.ctx_slot, inp.device)
+        # depths on the pivoted LU (check_build's answer when a residual check failed)
+        self.pivoted = frozenset(pivoted)
         self.torch = torch
         self.layout, self.ngroups, self.scalars = inp.layout, inp.ngroups, tuple(inp.scalars)
         self._present = tuple(t is not None for t in inp.fields_dev)
@@ -933,11 +970,11 @@ class BuildGraph:
         pool = torch.cuda.graph_pool_handle()
         self.stages = []
         n0 = lib.hps_launch_count()
-        key = (id(inp.layout), inp.ngroups, self._present, self.scalars, self.nrhs, self.ctx_slot)
+        key = (id(inp.layout), inp.ngroups, self._present, self.scalars, self.nrhs, self.ctx_slot, self.pivoted)
         with torch.cuda.stream(side):
             if key not in BuildGraph._warmed:
                 # warm-up: lazy attributes and scratch sizes outside the capture (once per shape)
-                st = build_device(self._inp, ctx=self.ctx)
+                st = build_device(self._inp, ctx=self.ctx, pivoted=self.pivoted)
                 if self.nrhs:
                     solve_device(st, self._F, ctx=self.ctx)
                 del st
@@ -962,7 +999,7 @@ class BuildGraph:
                 active[0] = self.stages[-1][1]
 
             try:
-                self.state = build_device(self._inp, stage_begin=begin_tracked, ctx=self.ctx)
+                self.state = build_device(self._inp, stage_begin=begin_tracked, ctx=self.ctx, pivoted=self.pivoted)
                 self.stages[-1][1].capture_end()
                 active[0] = None
                 self.solve_graph, self.U = None, None

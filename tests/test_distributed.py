@@ -55,7 +55,7 @@ class NumpyBackend:
         Psi, T, cond = O.leaf_operators(self.geom, fields, np.arange(ngroups))
         return torch.from_numpy(Psi), torch.from_numpy(T), torch.from_numpy(cond)
 
-    def merge_level(self, d, nbatch, child_T, child_idx, status, parent_status=None):
+    def merge_level(self, d, nbatch, child_T, child_idx, status, parent_status=None, pivoted=()):
         dl = self.lay.depths[d]
         Tc = child_T.numpy()
         S, T = [], []
@@ -67,7 +67,7 @@ class NumpyBackend:
         return torch.from_numpy(np.stack(S)), torch.from_numpy(np.stack(T))
 
     # split merge of the distributed top depths (the CUDA backend's hps_merge_interface & co.)
-    def merge_interface(self, d, children, status):
+    def merge_interface(self, d, children, status, pivoted=()):
         dl = self.lay.depths[d]
         Ta, Tb = children[0].numpy(), children[1].numpy()
         X = Ta[np.ix_(dl.j3a, dl.j3a)] - Tb[np.ix_(dl.j3b, dl.j3b)]
@@ -76,7 +76,7 @@ class NumpyBackend:
         perm = np.arange(dl.n3, dtype=np.int32)
         return tuple(torch.from_numpy(np.ascontiguousarray(a)[None]) for a in (X, perm, R, C))
 
-    def interface_solve(self, d, Xf, perm, Rp, status):
+    def interface_solve(self, d, Xf, perm, Rp, status, pivoted=()):
         import scipy.linalg as sla
         X = Xf[0].numpy()[perm[0].numpy()]
         return torch.from_numpy(sla.lu_solve(sla.lu_factor(X), Rp[0].numpy()[perm[0].numpy()])[None])

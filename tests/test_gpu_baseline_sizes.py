@@ -34,12 +34,21 @@ def _case(tag):
     return int(cfg[3:]), int(L[1:])
 
 
-@pytest.mark.parametrize("tag", CASES)
-def test_baseline_size_against_reference(tag):
+@pytest.mark.parametrize("tag,pivoted", [(t, False) for t in CASES] +
+                         [(t, True) for t in CASES if t in ("cfg3_L7", "cfg4_L8")])
+def test_baseline_size_against_reference(tag, pivoted):
+    """pivoted=True: every interface of n3 > 128 on the pivoted LU (the fallback of a failed residual
+    check) instead of the block inverse, gated the same way (the Helmholtz configs)."""
     cfg, L = _case(tag)
     g = np.load(os.path.join(GOLDEN, f"large_{tag}.npz"))
     tree, nodes = P.build_tree(P.Rectangle(0, 1, 0, 1), L, 16)
-    st = solver.build(tree, nodes, problems.coefficients(cfg), switch_threshold=None)
+    if pivoted:
+        inp = solver.prepare(tree, nodes, problems.coefficients(cfg))
+        st = solver.build_device(inp, pivoted={d for d, dl in enumerate(inp.layout.depths) if dl.n3 > 128})
+        assert solver.check_build(st) == set()
+    else:
+        st = solver.build(tree, nodes, problems.coefficients(cfg), switch_threshold=None)
+        assert not st._pivoted  # no residual check failed at the BASELINE sizes
     T = st.root_T.device_tensor
     rows = torch.from_numpy(g["rows"]).to(T.device)
     got_rows = T.index_select(0, rows).cpu().numpy()
@@ -55,7 +64,7 @@ def test_baseline_size_against_reference(tag):
     report = []
     for name, diff, noise in checks:
         gate = max(TOL[cfg], 10.0 * noise)
-        report.append(f"{tag} {name}: diff {diff:.2e}, reference self-noise {noise:.2e}, gate {gate:.2e}")
+        report.append(f"{tag}{' (pivoted LU)' if pivoted else ''} {name}: diff {diff:.2e}, reference self-noise {noise:.2e}, gate {gate:.2e}")
     # tie-breaker where an exact solution exists: cfg 1 exp(x1) sin(x2), cfg 3 plane wave
     ex = problems.exact_solution(cfg, nodes.points[:, 0], nodes.points[:, 1], seed=21, batch=1)
     if ex is not None:

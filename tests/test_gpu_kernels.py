@@ -179,5 +179,5 @@ def test_lookahead_refuses_odd_batch():
     r = lib.hps_merge_level_ahead(_native.context(), 3, n3, ne, m, q, _native.ptr(T), m * m, None, _native.ptr(maps),
                                   _native.ptr(vm), _native.ptr(S), _native.ptr(To), _native.ptr(ws), wsb,
                                   _native.ptr(st), 0, 0, _native.ptr(pmaps), 64, 256, _native.ptr(vm), _native.ptr(pws),
-                                  pwsb, _native.ptr(st), 0, _native.stream_ptr())
+                                  pwsb, _native.ptr(st), 0, 0, _native.stream_ptr())
     assert r == _native.HPS_ERR_ARG and "even nbatch" in _native.last_error()
