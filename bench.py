@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="override solve batch b")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="enqueue the build eagerly instead of replaying CUDA graphs")
+    ap.add_argument("--emu-slices", type=int, default=None,
+                    help="FP64 GEMM emulation on the int8 tensor cores: slices per operand (0 = DMMA only)")
     ap.add_argument("--validate-reference-model", action="store_true",
                     help="time whole oracle-port steps at configs 2 (L=6) and 3 (L=7) against the sampled model")
     ap.add_argument("--full-reference", action="store_true",
@@ -93,6 +95,16 @@ def traffic_from_profiles(workload, stage):
     src = (f"profiles/{os.path.basename(path)}: dram read+write per launch of {pj.get('kernel')} (ncu --set full; "
            f"{pj.get('gpu_time_ms', float('nan')):.3f} ms); algorithmic {pj.get('algorithmic_bytes_per_launch', 0):.3g} B")
     return float(pj["dram_bytes_per_launch"]), src
+
+
+def int8_peak():
+    """Dense int8 tensor rate: twice the measured bf16 GEMM rate (sm_100 runs int8 / fp8 at 2x bf16;
+    NVIDIA nominal 4.5 POPS dense vs 2.25 PFLOP/s bf16)."""
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            return 2.0 * float(json.load(f)["bf16_tflops"]), "2 x MEASURED_PEAKS.json bf16_tflops (int8 = 2x bf16 on sm_100)"
+    except Exception:
+        return 2.0 * 1590.0, "2 x fallback bf16 1.59 PFLOP/s (B200_PROFILING.md)"
 
 
 def hbm_peak():
@@ -244,6 +256,10 @@ def main():
         return bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, world)
     dev = torch.device("cuda")
     lib = _native.load()
+    if args.emu_slices is not None:
+        for slot in range(4):
+            _native.context(slot).set("emu_slices", args.emu_slices)
+    emu_slices = _native.context().get("emu_slices")
     tree, nodes = P.build_tree(P.Rectangle(0.0, 1.0, 0.0, 1.0), L, q)
     co = c.coefficients()
     F_host = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=0, batch=b)
@@ -342,7 +358,22 @@ def main():
         "solve": {"tflops": solve_flops / ts / 1e12, "frac_fp64": solve_flops / ts / 1e12 / peak,
                   "gbs_S_stream": S_bytes / ts / 1e9, "frac_hbm": S_bytes / ts / 1e9 / hpeak, "hbm_peak_source": hsrc},
     }
-
+    if dom.startswith("merge_d") and emu_slices > 0:
+        dd = int(dom.split("_d")[-1])
+        ops = Wk.emulated_int8_ops(L, q, dd, emu_slices)
+        if ops > 0:
+            # the dominant stage's bulk runs on the int8 tensor cores: its roofline is the int8 rate;
+            # its FP64-equivalent rate (the algorithmic FP64 flops over the stage time) goes beside it
+            i8peak, i8src = int8_peak()
+            i8 = ops / (stage_ms[dom] / 1e3) / 1e12
+            roofline.update({
+                "bound": "tensor", "achieved": i8, "peak": i8peak, "unit": "TOPS (int8)", "frac": i8 / i8peak,
+                "peak_source": i8src,
+                "kernels": (f"{dom}: S and T GEMMs as FP64 emulation on the int8 tensor cores ({emu_slices} slices, "
+                            f"{emu_slices * (emu_slices + 1) // 2} int8 products each, cuBLASLt IMMA) + hps::k_emu_split_* "
+                            f"/ k_emu_accum; interface inverse on DMMA"),
+                "fp64_equivalent": {"achieved_tflops": ach, "fp64_dmma_peak_tflops": peak, "ratio_to_fp64_peak": ach / peak,
+                                    "note": "algorithmic FP64 flops of the stage / stage time"}})
     # ---- end-to-end through the public API (solver.Pipeline), pinned host memory ----
     # Every step is one full problem: host sampling + grouping of the coefficients, their H2D
     # upload, the build, the H2D of the boundary data, the batched solve and the D2H of u. The
@@ -412,6 +443,7 @@ def main():
             "launch": launch_mode,
             "stages": {"unknowns": unknowns, "batch": b, "leaf_groups": inp.ngroups,
                        "pivoted_lu_depths": sorted(pivoted),
+                       "fp64_gemm_emulation_slices": emu_slices,
                        "build_ms": tb * 1e3, "solve_ms": ts * 1e3,
                        "build_unknowns_per_s": unknowns / tb, "solve_unknowns_per_s": unknowns * b / ts,
                        "build_fp64_tflops": roofline["build_tflops"], "build_fp64_frac": roofline["build_frac"],
@@ -432,6 +464,10 @@ def bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, w
 
     dev = torch.device("cuda")
     lib = _native.load()
+    if args.emu_slices is not None:
+        for slot in range(4):
+            _native.context(slot).set("emu_slices", args.emu_slices)
+    emu_slices = _native.context().get("emu_slices")
     tree, nodes = P.build_tree(P.Rectangle(0.0, 1.0, 0.0, 1.0), L, q)
     co = c.coefficients()
     F = None

@@ -36,6 +36,9 @@ HPS_OPT_INV_FORK = 2
 HPS_OPT_LEAF_CTAS_PER_SM = 3
 HPS_OPT_LEAF_FREE_SMS = 4
 HPS_OPT_PROFILE_AHEAD = 5
+HPS_OPT_EMU_SLICES = 6
+HPS_OPT_EMU_MIN_WORK = 7
+HPS_OPT_EMU_MIN_K = 8
 
 HPS_MERGE_PIVOTED = 1
 HPS_MERGE_PARENT_PIVOTED = 2

@@ -9,7 +9,7 @@ FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompil
 objs=()
 pids=()
 mkdir -p "${HPS_OBJ:-${here}/../build_obj}"
-for f in capi gemm merge lu solve leaf leaf3 group post tree; do
+for f in capi gemm emu merge lu solve leaf leaf3 group post tree; do
   o="${HPS_OBJ:-${here}/../build_obj}/${f}.o"
   # tree.cu is host code that must reproduce numpy's fp64 results bit for bit: no FMA contraction
   extra=()
@@ -24,5 +24,5 @@ done
 for pid in "${pids[@]}"; do
   wait "$pid" || { echo "build.sh: compile failed" >&2; exit 1; }
 done
-"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$out" "${objs[@]}" -lcudart_static -lrt -ldl -lpthread
+"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$out" "${objs[@]}" -lcudart_static -L/usr/local/cuda/lib64 -lcublasLt -Xlinker -rpath -Xlinker /usr/local/cuda/lib64 -lrt -ldl -lpthread
 echo "built $out"

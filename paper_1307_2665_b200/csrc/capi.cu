@@ -87,6 +87,23 @@ double* Ctx::splitk_scratch(size_t n, cudaStream_t st) {
   return splitk[r];
 }
 
+double* Ctx::emu_scratch(size_t n, cudaStream_t st) {
+  const int r = role(st);
+  if (n > emu_n[r]) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    double* fresh = nullptr;
+    if (cudaMalloc(&fresh, n * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    if (emu_buf[r]) retired.push_back(emu_buf[r]);
+    emu_buf[r] = fresh;
+    emu_n[r] = n;
+  }
+  return emu_buf[r];
+}
+
 int ensure_smem_attr(const void* kernel, int device, int bytes) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> done;
@@ -149,6 +166,9 @@ extern "C" int hps_ctx_destroy(hps_ctx_t handle) {
       if (e) cudaEventDestroy(e);
   for (auto p : c->splitk)
     if (p) cudaFree(p);
+  for (auto p : c->emu_buf)
+    if (p) cudaFree(p);
+  if (c->emu && c->emu_free) c->emu_free(c->emu);
   for (auto p : c->retired) cudaFree(p);
   cudaGetLastError();
   cudaSetDevice(prev);

@@ -17,7 +17,9 @@ namespace hps {
 struct Ctx {
   int device = 0;
   int sms = 148;
-  long long opt[HPS_OPT_COUNT] = {1, 16, 1, 2, 0, 0};
+  // defaults: split-K on, group-M 16, fork on, 2 leaf CTAs/SM, no free SMs, no profiling, FP64 GEMM
+  // emulation with 8 slices (FP64-equivalent accuracy) for K >= 1024 and >= 2^32 multiply-adds
+  long long opt[HPS_OPT_COUNT] = {1, 16, 1, 2, 0, 0, 8, 1LL << 32, 1024};
   // side streams: 1 = fork (recursive inverse), 2/3 = look-ahead inverse pair (highest priority)
   cudaStream_t side = nullptr, ahead = nullptr, ahead_side = nullptr;
   bool streams_ok = false;
@@ -44,6 +46,12 @@ struct Ctx {
     return e;
   }
   double* splitk_scratch(size_t n, cudaStream_t st);
+  // FP64-emulation state (emu.cu: cuBLASLt handle, plans) and its scratch per stream role
+  void* emu = nullptr;
+  void (*emu_free)(void*) = nullptr;
+  double* emu_buf[4] = {};
+  size_t emu_n[4] = {};
+  double* emu_scratch(size_t n, cudaStream_t st);
 };
 
 // Context of a C-ABI call: a valid handle whose device is the caller's current device.

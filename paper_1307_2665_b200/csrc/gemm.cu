@@ -93,11 +93,17 @@ static int launch_cfg64(const GemmParams& p, Ctx& cx, cudaStream_t stream) {
   return HPS_OK;
 }
 
+int emu_gemm(const GemmParams& p, Ctx& cx, cudaStream_t st);  // emu.cu
+
 int dgemm_launch(const GemmParams& p, Ctx& cx, cudaStream_t stream) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return HPS_OK;
   if (p.K <= 0) {
     set_error("dgemm: K=%d", p.K);
     return HPS_ERR_ARG;
+  }
+  if (p.emu_ok && cx.opt[HPS_OPT_EMU_SLICES] > 0) {
+    const int r = emu_gemm(p, cx, stream);
+    if (r != 1) return r;  // 1: not eligible here, run on DMMA
   }
   const bool vec = !(p.K % 16 != 0 || p.N % 2 != 0 || (p.ldb % 2) || (p.ldc % 2) || (p.lda % 2) ||
                      (p.strideA % 2) || (p.strideB % 2) || (p.strideC % 2) ||
@@ -145,6 +151,7 @@ extern "C" int hps_dgemm_batched(hps_ctx_t ctx, int M, int N, int K, int batch, 
                                  long long strideC, void* stream) {
   hps::GemmParams p{M, N, K, batch, A, lda, strideA, B, ldb, strideB, Bidx, strideBidx, C, ldc, strideC,
                     alpha, beta, nullptr};
+  p.emu_ok = true;
   HPS_CTX(cx, ctx);
   return hps::dgemm_launch(p, *cx, static_cast<cudaStream_t>(stream));
 }

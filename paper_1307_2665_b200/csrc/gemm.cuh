@@ -47,6 +47,7 @@ struct GemmParams {
   const int* blk_j1a = nullptr;
   const int* blk_j2b = nullptr;
   int group_m = 0;  // 64 x 64 kernel: grouped tile rasterisation (0 = row-major)
+  bool emu_ok = false;  // may run as the int8-sliced FP64 emulation (emu.cu) when the context enables it
 };
 
 __device__ __forceinline__ double blk_value(const GemmParams& p, int b, int r, int c) {

@@ -841,9 +841,12 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
   // S = X^-1 R; a non-finite S raises the status word to the merge index (MergeResonanceError)
   if (big)
     HPS_TRY(lu_solve(cx, X, n3, nbatch, W.lu, R, ne, S_out, status, status_base, st));
-  else
-    HPS_TRY(gemm(cx, n3, ne, n3, nbatch, 1.0, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, 0.0, S_out, ne,
-                 (long long)n3 * ne, st, status));
+  else {
+    GemmParams sp{n3, ne, n3, nbatch, X, n3, (long long)n3 * n3, R, ne, (long long)n3 * ne, nullptr, 0, S_out, ne,
+                  (long long)n3 * ne, 1.0, 0.0, status};
+    sp.emu_ok = true;
+    HPS_TRY(dgemm_launch(sp, cx, st));
+  }
   if (ah != nullptr && !(cx.streams_ok && (nbatch % 2) == 0)) {
     // the caller would treat the parent's X as inverted: refuse instead of skipping silently
     set_error("hps_merge_level_ahead: look-ahead needs an even nbatch (got %d) and the context's streams", nbatch);
@@ -903,6 +906,7 @@ static int merge_level_impl(Ctx& cx, int nbatch, int n3, int ne, int m, int q, c
     gp.blk = ch;
     gp.blk_j1a = j1a;
     gp.blk_j2b = j2b;
+    gp.emu_ok = true;
     HPS_TRY(dgemm_launch(gp, cx, st));
   }
   if (ahead) ahead_probe(cx, 2, st);

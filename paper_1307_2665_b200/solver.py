@@ -985,10 +985,14 @@ class BuildGraph:
 
             # thread_local: other host threads (the Pipeline's preparation thread) may sync or
             # allocate pinned memory meanwhile without invalidating this capture
+            self.stage_launches = []
+
             def begin(name):
                 if self.stages:
                     self.stages[-1][1].capture_end()
+                    self.stage_launches.append(int(lib.hps_launch_count() - self._l0))
                 g = torch.cuda.CUDAGraph()
+                self._l0 = lib.hps_launch_count()
                 g.capture_begin(pool=pool, capture_error_mode="thread_local")
                 self.stages.append((name, g))
 
@@ -1001,6 +1005,7 @@ class BuildGraph:
             try:
                 self.state = build_device(self._inp, stage_begin=begin_tracked, ctx=self.ctx, pivoted=self.pivoted)
                 self.stages[-1][1].capture_end()
+                self.stage_launches.append(int(lib.hps_launch_count() - self._l0))
                 active[0] = None
                 self.solve_graph, self.U = None, None
                 if self.nrhs:

@@ -68,3 +68,22 @@ def build_roofline_seconds(L, q, ngroups, f64_tflops, hbm_gbs):
     for d in range(2 * L):
         t += max(merge_flops_depth(L, q, d) / F, merge_bytes_depth(L, q, d) / B)
     return t
+
+
+def emulated_gemms(L, q, d, min_k=1024, min_work=2 ** 32):
+    """(M, N, K, batch) of the merge GEMMs of depth d that run as the int8-sliced FP64 emulation
+    (csrc/emu.cu: K >= min_k and M N K batch >= min_work): S = X^-1 R (n3 x ne x n3) and
+    T = blk + C S (ne x ne x n3), 2^d merges."""
+    n3, ne = depth_sizes(L, q, d)
+    out = []
+    for M, N, K in ((n3, ne, n3), (ne, ne, n3)):
+        if K >= min_k and float(M) * N * K * 2 ** d >= min_work and M % 4 == 0 and N % 4 == 0 and K % 16 == 0:
+            out.append((M, N, K, 2 ** d))
+    return out
+
+
+def emulated_int8_ops(L, q, d, slices, **kw):
+    """int8 tensor operations of depth d's emulated GEMMs: slices (slices + 1) / 2 products of 2 M N K."""
+    if slices <= 0:
+        return 0.0
+    return sum(slices * (slices + 1) / 2 * 2.0 * M * N * K * b for M, N, K, b in emulated_gemms(L, q, d, **kw))
