@@ -51,12 +51,18 @@ typedef struct hps_ctx_s* hps_ctx_t;
 #define HPS_OPT_LEAF_CTAS_PER_SM 3  /* leaf kernel CTAs per SM (2) */
 #define HPS_OPT_LEAF_FREE_SMS 4     /* leaf grid sized for this many fewer SMs (0) */
 #define HPS_OPT_PROFILE_AHEAD 5     /* timing events around the look-ahead inverse (0; dev tool) */
-#define HPS_OPT_EMU_SLICES 6        /* FP64 GEMM emulation on the int8 tensor cores: 7-bit slices per operand
-                                       (8, FP64-equivalent; 0 = off: DMMA); the merges' S / T GEMMs and
-                                       hps_dgemm_batched */
+#define HPS_OPT_EMU_SLICES 6        /* FP64 GEMM emulation on the int8 tensor cores, slice scheme: 7-bit slices
+                                       per operand, s (s + 1) / 2 int8 products (0 = off; used when
+                                       HPS_OPT_EMU_MODULI is 0); the merges' S / T GEMMs and hps_dgemm_batched */
 #define HPS_OPT_EMU_MIN_WORK 7      /* emulate GEMMs with M N K batch >= this (2^32) */
 #define HPS_OPT_EMU_MIN_K 8         /* ... and K >= this (1024): below it the fp64 accumulation traffic wins */
-#define HPS_OPT_COUNT 9
+#define HPS_OPT_EMU_MODULI 9        /* FP64 GEMM emulation, modular scheme: one int8 product per modulus
+                                       (14, FP64-equivalent; 6..16; 0 = off) with Chinese-remainder
+                                       reconstruction; takes precedence over HPS_OPT_EMU_SLICES */
+#define HPS_OPT_EMU_SCRATCH_MB 10   /* cap on the modular scheme's product scratch (8192 MB) */
+#define HPS_OPT_EMU_ENGINE 11       /* int8 products of the modular scheme: 0 = this library's tcgen05 kernel
+                                       (TMA + TMEM, residues reduced in its epilogue), 1 = cuBLASLt IMMA */
+#define HPS_OPT_COUNT 12
 int hps_ctx_create(int device, hps_ctx_t* out);
 int hps_ctx_destroy(hps_ctx_t ctx);
 int hps_ctx_set_option(hps_ctx_t ctx, int option, long long value);

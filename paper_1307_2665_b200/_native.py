@@ -39,6 +39,9 @@ HPS_OPT_PROFILE_AHEAD = 5
 HPS_OPT_EMU_SLICES = 6
 HPS_OPT_EMU_MIN_WORK = 7
 HPS_OPT_EMU_MIN_K = 8
+HPS_OPT_EMU_MODULI = 9
+HPS_OPT_EMU_SCRATCH_MB = 10
+HPS_OPT_EMU_ENGINE = 11
 
 HPS_MERGE_PIVOTED = 1
 HPS_MERGE_PARENT_PIVOTED = 2

@@ -9,7 +9,7 @@ FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompil
 objs=()
 pids=()
 mkdir -p "${HPS_OBJ:-${here}/../build_obj}"
-for f in capi gemm emu merge lu solve leaf leaf3 group post tree; do
+for f in capi gemm emu i8gemm merge lu solve leaf leaf3 group post tree; do
   o="${HPS_OBJ:-${here}/../build_obj}/${f}.o"
   # tree.cu is host code that must reproduce numpy's fp64 results bit for bit: no FMA contraction
   extra=()

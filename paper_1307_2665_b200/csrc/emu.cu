@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <map>
 #include <tuple>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ctx.cuh"
@@ -254,18 +255,24 @@ static EmuPlan* emu_plan(EmuState* es, int M, int N, int kp, int sK, int batch) 
   return ok ? &pl : nullptr;
 }
 
-// Returns HPS_OK when the GEMM ran emulated, 1 when the caller should run it on DMMA instead (not
-// eligible, no scratch inside a graph capture, or no cuBLASLt plan), an error code on failure.
-int emu_gemm(const GemmParams& p, Ctx& cx, cudaStream_t st) {
-  const int s = (int)cx.opt[HPS_OPT_EMU_SLICES];
-  if (s <= 0 || p.Bidx || p.beta != 0.0 || p.split > 1) return 1;
+// Shape / alignment test shared by both schemes: it pays where a GEMM is FP64-bound, K >=
+// HPS_OPT_EMU_MIN_K (each output element costs 2 K DMMA flops against the per-element conversion
+// and reconstruction traffic).
+static bool emu_eligible(const GemmParams& p, const Ctx& cx) {
+  if (p.Bidx || p.beta != 0.0 || p.split > 1) return false;
   const double work = (double)p.M * p.N * p.K;
-  // it pays where a GEMM is FP64-bound: K >= HPS_OPT_EMU_MIN_K (each output element costs 2 K DMMA flops
-  // against ~56 bytes of accumulation traffic plus 72 K int8 operations)
   if (work * p.batch < (double)cx.opt[HPS_OPT_EMU_MIN_WORK] || p.K < cx.opt[HPS_OPT_EMU_MIN_K] || p.M % 4 ||
       p.N % 4 || p.K % 16)
-    return 1;
-  if ((reinterpret_cast<uintptr_t>(p.C) & 15) || (p.ldc % 2) || (p.strideC % 2)) return 1;
+    return false;
+  return !((reinterpret_cast<uintptr_t>(p.C) & 15) || (p.ldc % 2) || (p.strideC % 2));
+}
+
+// Slice scheme. Returns HPS_OK when the GEMM ran emulated, 1 when the caller should run it on DMMA
+// instead (not eligible, no scratch inside a graph capture, or no cuBLASLt plan), an error code on
+// failure.
+static int emu_gemm_slices(const GemmParams& p, Ctx& cx, cudaStream_t st) {
+  const int s = (int)cx.opt[HPS_OPT_EMU_SLICES];
+  if (s <= 0 || !emu_eligible(p, cx)) return 1;
   if ((long long)(s) * p.K * 64 * 64 >= (1LL << 31)) return 1;  // C_t must stay exact in int32
   EmuState* es = emu_state(cx);
   if (!es) return 1;
@@ -318,6 +325,468 @@ int emu_gemm(const GemmParams& p, Ctx& cx, cudaStream_t st) {
     HPS_LAUNCH_CHECK();
   }
   return HPS_OK;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Modular scheme (Chinese remainder theorem; Ozaki, Uchino & Imamura's "scheme II", restated).
+//
+// Rows of A and columns of B are scaled by powers of two and rounded to integers,
+//   A' = rint(diag(2^sig) A),  B' = rint(B diag(2^tau)),  with ||A'_i||_2 <= 2^PA, ||B'_j||_2 <= 2^PB,
+// so by Cauchy-Schwarz every entry of the exact integer product C' = A'B' is at most 2^(PA + PB) <=
+// Mod / 8 in magnitude, Mod = m_0 ... m_(n-1) (pairwise coprime, <= 256). Per modulus the residues
+// A'_l = A' mod m_l, B'_l = B' mod m_l (symmetric, int8) give C_l = A'_l B'_l exactly in int32 (|C_l|
+// <= K 2^14), one int8 GEMM each, and
+//   C' = sum_l (C_l mod m_l) w_l  (mod Mod),  w_l = (Mod / m_l) ((Mod / m_l)^-1 mod m_l),
+// recovered in fp64 from an exact high part (w_l rounded to a multiple of 2^E, 42 significant bits:
+// sums of r w_hi are exact) plus a low part, and the quotient by Mod rounded away (|C'| <= Mod / 8
+// keeps it unambiguous). C = diag(2^-sig) C' diag(2^-tau). The only rounding is that of A' and B'
+// (<= 1/2 per entry, relative to the row / column 2-norm 2^-PA, 2^-PB) and the final fp64 sum: with
+// 14 moduli (Mod ~ 2^110.2, PA = 53, PB = 54) the product error is at or below a DGEMM's, for n
+// int8 GEMMs instead of the slice scheme's s (s + 1) / 2 = 36.
+// ---------------------------------------------------------------------------------------------
+constexpr int CRT_MAX = 16;
+struct CrtConst {
+  int n, PA, PB, E;
+  double m[CRT_MAX], inv_m[CRT_MAX];  // residues of the scaled operands (fp64, exact)
+  int mi[CRT_MAX], minv[CRT_MAX];     // reduction of int32 products: minv = floor(2^32 / m)
+  double W[CRT_MAX], wlo[CRT_MAX];    // w_l = W_l 2^E + wlo_l, W_l integer, |wlo_l| <= 2^(E - 1)
+  double Mh, Mlo;                     // Mod = Mh 2^E + Mlo
+  double twoE_over_M, inv_M, twoE;
+};
+
+static const int kModuli[CRT_MAX] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+
+// Reconstruction arithmetic (k_crt_accum), with r_l = C_l mod m_l in [-128, 127], n <= 16 and
+// E = bits - 42 (Mod < 2^bits), all in fp64:
+//   shi = sum r_l W_l                    exact: |W_l| <= 2^41 + 1, |shi| < 2^52
+//   slo = sum r_l wlo_l                  |slo| <= 2^(E + 10), rounding 2^(E - 43)
+//   q   = rint(shi 2^E / Mod + slo / Mod)   |C'| <= Mod / 8 leaves a 3/8 margin to the rounding edge
+//   C'  = (shi - q Mh) 2^E + (slo - q Mlo)  the first factor exact (an integer < 2^42)
+// so C' carries an absolute error ~2^(bits - 85), far below an fp64 ulp of the largest |C'| ~ 2^(bits - 4).
+static bool crt_constants(int n, CrtConst& c) {
+  if (n < 2 || n > CRT_MAX) return false;
+  typedef unsigned __int128 u128;
+  typedef __int128 i128;
+  u128 Mod = 1;
+  for (int l = 0; l < n; ++l) Mod *= (u128)kModuli[l];
+  int bits = 0;  // Mod < 2^bits
+  while (bits < 128 && (u128(1) << bits) <= Mod) ++bits;
+  const int flo = bits - 1;  // 2^flo <= Mod
+  // |C'| <= 2^(PA + PB) <= 2^(flo - 3) <= Mod / 8
+  c.n = n;
+  c.PA = (flo - 3) / 2;
+  c.PB = flo - 3 - c.PA;
+  c.E = bits - 42;
+  auto to_double = [](i128 v) {
+    const bool neg = v < 0;
+    u128 u = neg ? (u128)(-v) : (u128)v;
+    const double d = (double)(unsigned long long)(u >> 64) * 18446744073709551616.0 + (double)(unsigned long long)(u & ~0ULL);
+    return neg ? -d : d;
+  };
+  auto split = [&](i128 v, double& hi, double& lo) {  // v = hi 2^E + lo, hi integer, |lo| <= 2^(E - 1)
+    const i128 unit = (i128)1 << c.E;
+    const i128 qv = v >= 0 ? (v + unit / 2) >> c.E : -((-v + unit / 2) >> c.E);
+    hi = to_double(qv);  // |qv| < 2^42: exact
+    lo = to_double(v - qv * unit);
+  };
+  const double dMod = to_double((i128)Mod);
+  for (int l = 0; l < n; ++l) {
+    const long long m = kModuli[l];
+    const u128 Ml = Mod / (u128)m;
+    const long long r = (long long)(Ml % (u128)m);
+    long long y = 1;
+    while ((r * y) % m != 1) ++y;  // m <= 256: direct search
+    const u128 w = (Ml * (u128)y) % Mod;
+    const i128 ws = (w > Mod / 2) ? (i128)w - (i128)Mod : (i128)w;
+    c.m[l] = (double)m;
+    c.inv_m[l] = 1.0 / (double)m;
+    c.mi[l] = (int)m;
+    c.minv[l] = (int)((1ULL << 32) / (unsigned long long)m);
+    split(ws, c.W[l], c.wlo[l]);
+  }
+  split((i128)Mod, c.Mh, c.Mlo);
+  c.twoE = ldexp(1.0, c.E);
+  c.twoE_over_M = c.twoE / dMod;
+  c.inv_M = 1.0 / dMod;
+  return true;
+}
+
+// sig[b][i] (tau[b][j]): the power of two that brings row i of A (column j of B) to 2-norm < 2^P;
+// INT_MIN marks a non-finite row / column (its outputs become NaN, as a DGEMM's would be non-finite).
+// The squares are summed after an exact power-of-two prescale by the maximum (no overflow).
+__device__ __forceinline__ int crt_prescale(double mx, int& em) {  // 0: zero row, -1: non-finite, 1: ok
+  if (!isfinite(mx)) return -1;
+  if (mx == 0.0) return 0;
+  frexp(mx, &em);  // mx < 2^em
+  return 1;
+}
+__device__ __forceinline__ int crt_exponent(double ss, int em, int P) {
+  int ex;
+  frexp(sqrt(ss) * (1.0 + 0x1p-30), &ex);  // ||row|| 2^-em < 2^ex (an upper bound despite rounding)
+  return P - ex - em;
+}
+
+__global__ void k_crt_row_scale(const double* __restrict__ A, long long lda, long long sA, int M, int K, int P,
+                                int* __restrict__ sig) {
+  const int b = blockIdx.y;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const double* Ar = A + (long long)b * sA + (long long)r * lda;
+  double mx = 0.0;
+  for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(Ar[k]));
+  mx = warp_max(mx);
+  int em = 0;
+  const int kind = crt_prescale(mx, em);
+  if (kind <= 0) {
+    if (lane == 0) sig[(long long)b * M + r] = kind < 0 ? INT_MIN : 0;
+    return;
+  }
+  double ss = 0.0;
+  for (int k = lane; k < K; k += 32) {
+    const double v = ldexp(Ar[k], -em);
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) sig[(long long)b * M + r] = crt_exponent(ss, em, P);
+}
+
+__global__ void __launch_bounds__(256) k_crt_col_scale(const double* __restrict__ B, long long ldb, long long sB, int K,
+                                                      int N, int P, int* __restrict__ tau) {
+  __shared__ double red[8][33];
+  __shared__ int ems[32];
+  const int b = blockIdx.y;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
+  const double* Bb = B + (long long)b * sB + j;
+  double mx = 0.0;
+  if (j < N)
+    for (int k = ty; k < K; k += 8) mx = fmax(mx, fabs(Bb[(long long)k * ldb]));
+  red[ty][tx] = mx;
+  __syncthreads();
+  if (ty == 0) {
+#pragma unroll
+    for (int r = 1; r < 8; ++r) mx = fmax(mx, red[r][tx]);
+    int em = 0;
+    const int kind = crt_prescale(mx, em);
+    ems[tx] = kind > 0 ? em : (kind < 0 ? INT_MIN : 0x40000000);
+  }
+  __syncthreads();
+  const int em = ems[tx];
+  double ss = 0.0;
+  if (j < N && em != INT_MIN && em != 0x40000000)
+    for (int k = ty; k < K; k += 8) {
+      const double v = ldexp(Bb[(long long)k * ldb], -em);
+      ss = fma(v, v, ss);
+    }
+  __syncthreads();
+  red[ty][tx] = ss;
+  __syncthreads();
+  if (ty == 0 && j < N) {
+#pragma unroll
+    for (int r = 1; r < 8; ++r) ss += red[r][tx];
+    tau[(long long)b * N + j] = em == INT_MIN ? INT_MIN : em == 0x40000000 ? 0 : crt_exponent(ss, em, P);
+  }
+}
+
+// symmetric residue of the integer x (|x| <= 2^55, exact in fp64) modulo m, in [-128, 127]
+__device__ __forceinline__ int crt_residue(double x, double m, double inv_m) {
+  const double q = rint(x * inv_m);
+  double r = fma(-m, q, x);  // exact: a small integer
+  if (r > 127.0) r -= m;
+  if (r < -128.0) r += m;
+  return (int)r;
+}
+
+// residues of the scaled rows of A: out[l][b][i][k]; 4 k per thread
+__global__ void k_crt_split_rows(const double* __restrict__ A, long long lda, long long sA, int M, int K, int batch,
+                                 const int* __restrict__ sig, CrtConst c, signed char* __restrict__ out) {
+  const int b = blockIdx.z, r = blockIdx.y;
+  const int k4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (k4 >= K) return;  // K % 16 == 0
+  const int sg = sig[(long long)b * M + r];
+  const double* Ar = A + (long long)b * sA + (long long)r * lda + k4;
+  double x[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) x[u] = sg == INT_MIN ? 0.0 : rint(ldexp(Ar[u], sg));  // exact scaling
+  const long long plane = (long long)batch * M * K;
+  char4* o = reinterpret_cast<char4*>(out + ((long long)b * M + r) * K + k4);
+  for (int l = 0; l < c.n; ++l)
+    o[l * (plane / 4)] = make_char4(crt_residue(x[0], c.m[l], c.inv_m[l]), crt_residue(x[1], c.m[l], c.inv_m[l]),
+                                    crt_residue(x[2], c.m[l], c.inv_m[l]), crt_residue(x[3], c.m[l], c.inv_m[l]));
+}
+
+// residues of the scaled columns of B, transposed: out[l][b][j][k]. Tile: 32 k x 64 j through
+// shared memory.
+__global__ void __launch_bounds__(256) k_crt_split_cols(const double* __restrict__ B, long long ldb, long long sB, int K,
+                                                       int N, int batch, const int* __restrict__ tau, CrtConst c,
+                                                       signed char* __restrict__ out) {
+  __shared__ signed char sd[CRT_MAX][64][36];
+  const int b = blockIdx.z;
+  const int k0 = blockIdx.y * 32, j0 = blockIdx.x * 64;
+  const double* Bb = B + (long long)b * sB;
+  for (int idx = threadIdx.x; idx < 32 * 64; idx += blockDim.x) {
+    const int kk = idx / 64, jj = idx % 64;
+    const int k = k0 + kk, j = j0 + jj;
+    double x = 0.0;
+    if (k < K && j < N) {
+      const int tj = tau[(long long)b * N + j];
+      x = tj == INT_MIN ? 0.0 : rint(ldexp(Bb[(long long)k * ldb + j], tj));
+    }
+    for (int l = 0; l < c.n; ++l) sd[l][jj][kk] = (signed char)crt_residue(x, c.m[l], c.inv_m[l]);
+  }
+  __syncthreads();
+  const long long plane = (long long)batch * N * K;
+  signed char* ob = out + (long long)b * N * K;
+  for (int idx = threadIdx.x; idx < c.n * 64 * 8; idx += blockDim.x) {  // 4 bytes per store
+    const int k4 = (idx % 8) * 4, rest = idx / 8, jj = rest % 64, l = rest / 64;
+    const int k = k0 + k4, j = j0 + jj;
+    if (k < K && j < N)
+      *reinterpret_cast<char4*>(ob + l * plane + (long long)j * K + k) =
+          *reinterpret_cast<const char4*>(&sd[l][jj][k4]);
+  }
+}
+
+// (C_l mod m_l) + 128 in [0, 255] of an int32 product (|v| < 2^30; as mod_byte in i8gemm.cu)
+__device__ __forceinline__ unsigned crt_biased(int v, int m, int minv) {
+  const unsigned x = (unsigned)(v + m * ((1 << 30) / m + 1));
+  const int q = (int)__umulhi(x, (unsigned)minv);
+  int r = (int)x - q * m;
+  r = r >= m ? r - m : r;
+  r = r > 127 ? r - m : r;
+  return (unsigned)(r + 128);
+}
+// biased residue (0..255) -> exact double r - 128, without the conversion unit
+__device__ __forceinline__ double crt_unbias(unsigned b) {
+  return __hiloint2double(0x43300000, (int)b) - 4503599627370624.0;  // 2^52 + 128
+}
+// 2^e for |e| <= 1022 (exact scale of the outputs), else ldexp
+__device__ __forceinline__ double crt_scale(double x, int e) {
+  if (e >= -1022 && e <= 1023) return x * __longlong_as_double((long long)(e + 1023) << 52);
+  return ldexp(x, e);
+}
+
+template <typename TIn>
+struct CrtIn;
+template <>
+struct CrtIn<int> {  // cuBLASLt int32 products: reduced here
+  typedef int4 V;
+  static __device__ __forceinline__ void biased(const V& x, const CrtConst& c, int l, unsigned (&b)[4]) {
+    b[0] = crt_biased(x.x, c.mi[l], c.minv[l]);
+    b[1] = crt_biased(x.y, c.mi[l], c.minv[l]);
+    b[2] = crt_biased(x.z, c.mi[l], c.minv[l]);
+    b[3] = crt_biased(x.w, c.mi[l], c.minv[l]);
+  }
+};
+template <>
+struct CrtIn<unsigned char> {  // the tcgen05 kernel's biased residues, 4 per word
+  typedef unsigned V;
+  static __device__ __forceinline__ void biased(const V& x, const CrtConst&, int, unsigned (&b)[4]) {
+    b[0] = x & 0xFFu;
+    b[1] = (x >> 8) & 0xFFu;
+    b[2] = (x >> 16) & 0xFFu;
+    b[3] = x >> 24;
+  }
+};
+
+// Reconstruction of the output columns [j0, j0 + nc) from the NM products of that panel
+// (Cl[l][b][i][0..nc): int32 products, or biased int8 residues), with the row / column scales,
+// alpha, the merge's block-diagonal addend and the non-finite flag. Rows on blockIdx.y (grid-stride),
+// 4 columns per thread; all NM loads of a row are issued before the arithmetic (4 FP64 operations
+// per residue, no conversions).
+template <int NM, typename TIn>
+__global__ void __launch_bounds__(256) k_crt_accum(const TIn* __restrict__ Cl, int M, int nc, int j0, GemmParams p,
+                                                  CrtConst c, const int* __restrict__ sig,
+                                                  const int* __restrict__ tau) {
+  typedef typename CrtIn<TIn>::V V4;
+  const int b = blockIdx.z;
+  const int c4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const long long plane = (long long)p.batch * M * nc;
+  bool bad = false;
+  if (c4 < nc) {
+    int tj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tj[u] = tau[(long long)b * p.N + j0 + c4 + u];
+    for (int r = blockIdx.y; r < M; r += gridDim.y) {
+      const TIn* src = Cl + ((long long)b * M + r) * nc + c4;
+      V4 in[NM];
+#pragma unroll
+      for (int l = 0; l < NM; ++l) in[l] = __ldcs(reinterpret_cast<const V4*>(src + l * plane));
+      const int sr = sig[(long long)b * M + r];
+      double shi[4] = {0.0, 0.0, 0.0, 0.0}, slo[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int l = 0; l < NM; ++l) {
+        unsigned bb[4];
+        CrtIn<TIn>::biased(in[l], c, l, bb);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double rr = crt_unbias(bb[u]);
+          shi[u] = fma(rr, c.W[l], shi[u]);  // exact
+          slo[u] = fma(rr, c.wlo[l], slo[u]);
+        }
+      }
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double q = rint(fma(shi[u], c.twoE_over_M, slo[u] * c.inv_M));
+        const double cp = fma(fma(-q, c.Mh, shi[u]), c.twoE, fma(-q, c.Mlo, slo[u]));
+        double w = (sr == INT_MIN || tj[u] == INT_MIN) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                        : crt_scale(cp, -(sr + tj[u]));
+        w *= p.alpha;
+        if (p.blk_j1a) w += blk_value(p, b, r, j0 + c4 + u);
+        bad |= !isfinite(w);
+        v[u] = w;
+      }
+      double* dst = p.C + (long long)b * p.strideC + (long long)r * p.ldc + j0 + c4;
+      *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
+      *reinterpret_cast<double2*>(dst + 2) = make_double2(v[2], v[3]);
+    }
+  }
+  if (p.nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicMax(p.nonfinite, b + p.batch_offset);
+}
+
+template <typename TIn>
+static void crt_accum_launch(int n, dim3 grid, cudaStream_t st, const TIn* Cl, int M, int nc, int j0,
+                             const GemmParams& p, const CrtConst& c, const int* sig, const int* tau) {
+#define HPS_CRT_CASE(NM) \
+  case NM: k_crt_accum<NM, TIn><<<grid, 256, 0, st>>>(Cl, M, nc, j0, p, c, sig, tau); break;
+  switch (n) {
+    HPS_CRT_CASE(2) HPS_CRT_CASE(3) HPS_CRT_CASE(4) HPS_CRT_CASE(5) HPS_CRT_CASE(6) HPS_CRT_CASE(7)
+    HPS_CRT_CASE(8) HPS_CRT_CASE(9) HPS_CRT_CASE(10) HPS_CRT_CASE(11) HPS_CRT_CASE(12) HPS_CRT_CASE(13)
+    HPS_CRT_CASE(14) HPS_CRT_CASE(15) HPS_CRT_CASE(16)
+  }
+#undef HPS_CRT_CASE
+}
+
+// Plan of the panel products: C_l[b] (int32, M x nc row-major) = Ares_l[b] (M x K) * Bres_l[b]^T
+// rows [j0, j0 + nc) (each nc x K; consecutive (l, b) operands strideB = N K apart), all n * batch
+// of them in one strided-batched call. Column-major terms: C^T (nc x M) = op_T(Bw) op_N(Aw).
+static EmuPlan* crt_plan(EmuState* es, int M, int nc, int K, long long strideB, int nbatch) {
+  auto key = std::make_tuple(M, nc, K, (int)(strideB / K), -nbatch);  // negative batch: CRT plans
+  auto it = es->plans.find(key);
+  if (it != es->plans.end()) return it->second.ok ? &it->second : nullptr;
+  EmuPlan& pl = es->plans[key];
+  cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+  bool ok = cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32I, CUDA_R_32I) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta)) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb)) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatrixLayoutCreate(&pl.a, CUDA_R_8I, K, nc, K) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatrixLayoutCreate(&pl.b, CUDA_R_8I, K, M, K) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatrixLayoutCreate(&pl.c, CUDA_R_32I, nc, M, nc) == CUBLAS_STATUS_SUCCESS;
+  if (ok && nbatch > 1) {
+    const long long sa = strideB, sb = (long long)M * K, sc = (long long)M * nc;
+    ok = cublasLtMatrixLayoutSetAttribute(pl.a, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &nbatch, sizeof(nbatch)) == 0 &&
+         cublasLtMatrixLayoutSetAttribute(pl.a, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sa, sizeof(sa)) == 0 &&
+         cublasLtMatrixLayoutSetAttribute(pl.b, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &nbatch, sizeof(nbatch)) == 0 &&
+         cublasLtMatrixLayoutSetAttribute(pl.b, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sb, sizeof(sb)) == 0 &&
+         cublasLtMatrixLayoutSetAttribute(pl.c, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &nbatch, sizeof(nbatch)) == 0 &&
+         cublasLtMatrixLayoutSetAttribute(pl.c, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sc, sizeof(sc)) == 0;
+  }
+  if (ok) {
+    cublasLtMatmulPreference_t pref = nullptr;
+    ok = cublasLtMatmulPreferenceCreate(&pref) == CUBLAS_STATUS_SUCCESS;
+    ok = ok && cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &es->ws_bytes,
+                                                    sizeof(es->ws_bytes)) == CUBLAS_STATUS_SUCCESS;
+    cublasLtMatmulHeuristicResult_t res{};
+    int nres = 0;
+    ok = ok && cublasLtMatmulAlgoGetHeuristic(es->lt, pl.op, pl.a, pl.b, pl.c, pl.c, pref, 1, &res, &nres) ==
+                   CUBLAS_STATUS_SUCCESS && nres > 0;
+    if (ok) pl.algo = res.algo;
+    if (pref) cublasLtMatmulPreferenceDestroy(pref);
+  }
+  pl.ok = ok;
+  return ok ? &pl : nullptr;
+}
+
+bool i8gemm_mod_ok(int M, int N, int nc, int K, int nmod);  // i8gemm.cu
+int i8gemm_mod(const signed char* A, const signed char* B, unsigned char* R, int M, int N, int nc, int j0, int K, int nz,
+               int batch, const int* moduli, int nmod, Ctx& cx, cudaStream_t st);
+
+static int emu_gemm_crt(const GemmParams& p, Ctx& cx, cudaStream_t st) {
+  const int n = (int)cx.opt[HPS_OPT_EMU_MODULI];
+  if (!emu_eligible(p, cx) || p.K >= (1 << 16)) return 1;  // |C_l| <= K 2^14 < 2^30
+  CrtConst c;
+  if (!crt_constants(n, c)) return 1;
+  // output column panels: the n products of a panel fit the scratch cap; panel widths are multiples
+  // of 256 (the kernel's tile width) where the cap allows
+  const bool own = cx.opt[HPS_OPT_EMU_ENGINE] == 0;
+  const size_t elt = own ? 1 : sizeof(int);  // the tcgen05 kernel stores residues, cuBLASLt int32 sums
+  const size_t cap = (size_t)std::max<long long>(1, cx.opt[HPS_OPT_EMU_SCRATCH_MB]) << 20;
+  const size_t per_col = (size_t)n * p.batch * p.M * elt;
+  const size_t maxc = std::max<size_t>(32, cap / per_col);
+  int nc;
+  if (maxc >= (size_t)p.N) {
+    nc = p.N;
+  } else {
+    const int np = (int)((p.N + maxc - 1) / maxc);
+    const int q = maxc >= 256 ? 256 : 32;
+    nc = std::min<int>((int)(maxc / q * q), ((p.N + np - 1) / np + q - 1) / q * q);
+  }
+  const bool use_own = own && i8gemm_mod_ok(p.M, p.N, nc, p.K, n) && (p.N % nc == 0 || (p.N % nc) % 32 == 0);
+  const size_t per = use_own ? 1 : sizeof(int);
+  const size_t a_bytes = (size_t)n * p.batch * p.M * p.K, b_bytes = (size_t)n * p.batch * p.N * p.K;
+  const size_t c_bytes = (size_t)n * p.batch * p.M * nc * per;
+  const size_t e_bytes = (size_t)p.batch * (p.M + p.N) * sizeof(int);
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t need = (align(a_bytes) + align(b_bytes) + align(c_bytes) + e_bytes) / sizeof(double) + 1;
+  EmuState* es = use_own ? nullptr : emu_state(cx);
+  if (!use_own && !es) return 1;
+  double* scratch = cx.emu_scratch(need, st);
+  if (!scratch) return 1;
+  char* base = reinterpret_cast<char*>(scratch);
+  signed char* Ar = reinterpret_cast<signed char*>(base);
+  signed char* Br = reinterpret_cast<signed char*>(base + align(a_bytes));
+  void* Cl = base + align(a_bytes) + align(b_bytes);
+  int* sig = reinterpret_cast<int*>(reinterpret_cast<char*>(Cl) + align(c_bytes));
+  int* tau = sig + (size_t)p.batch * p.M;
+  const int nb = n * p.batch;
+  EmuPlan *full = nullptr, *tail = nullptr;
+  if (!use_own) {
+    full = crt_plan(es, p.M, nc, p.K, (long long)p.N * p.K, nb);
+    tail = (p.N % nc) ? crt_plan(es, p.M, p.N % nc, p.K, (long long)p.N * p.K, nb) : nullptr;
+    if (!full || ((p.N % nc) && !tail)) return 1;
+  }
+  k_crt_row_scale<<<dim3((p.M + 7) / 8, p.batch), 256, 0, st>>>(p.A, p.lda, p.strideA, p.M, p.K, c.PA, sig);
+  HPS_LAUNCH_CHECK();
+  k_crt_col_scale<<<dim3((p.N + 31) / 32, p.batch), 256, 0, st>>>(p.B, p.ldb, p.strideB, p.K, p.N, c.PB, tau);
+  HPS_LAUNCH_CHECK();
+  k_crt_split_rows<<<dim3((p.K / 4 + 255) / 256, p.M, p.batch), 256, 0, st>>>(p.A, p.lda, p.strideA, p.M, p.K, p.batch,
+                                                                               sig, c, Ar);
+  HPS_LAUNCH_CHECK();
+  k_crt_split_cols<<<dim3((p.N + 63) / 64, (p.K + 31) / 32, p.batch), 256, 0, st>>>(p.B, p.ldb, p.strideB, p.K, p.N,
+                                                                                  p.batch, tau, c, Br);
+  HPS_LAUNCH_CHECK();
+  const int one = 1, zero = 0;
+  for (int j0 = 0; j0 < p.N; j0 += nc) {
+    const int w = std::min(nc, p.N - j0);
+    if (use_own) {
+      const int r = i8gemm_mod(Ar, Br, reinterpret_cast<unsigned char*>(Cl), p.M, p.N, w, j0, p.K, nb, p.batch,
+                               kModuli, n, cx, st);
+      if (r != HPS_OK) return r;
+    } else {
+      const EmuPlan* pl = w == nc ? full : tail;
+      const signed char* Bw = Br + (long long)j0 * p.K;  // cuBLASLt "A": residue rows [j0, j0 + w) of B^T
+      if (cublasLtMatmul(es->lt, pl->op, &one, Bw, pl->a, Ar, pl->b, &zero, Cl, pl->c, Cl, pl->c, &pl->algo, es->ws,
+                         es->ws_bytes, st) != CUBLAS_STATUS_SUCCESS) {
+        set_error("emu_gemm_crt: cublasLtMatmul failed (M=%d N=%d K=%d panel %d)", p.M, p.N, p.K, j0);
+        return HPS_ERR_CUDA;
+      }
+      count_launch();
+    }
+    const int bx = (w / 4 + 255) / 256;
+    const dim3 grid(bx, (unsigned)std::min<long long>(p.M, std::max<long long>(1, (long long)cx.sms * 16 / bx)), p.batch);
+    if (use_own)
+      crt_accum_launch<unsigned char>(n, grid, st, reinterpret_cast<const unsigned char*>(Cl), p.M, w, j0, p, c, sig, tau);
+    else
+      crt_accum_launch<int>(n, grid, st, reinterpret_cast<const int*>(Cl), p.M, w, j0, p, c, sig, tau);
+    HPS_LAUNCH_CHECK();
+  }
+  return HPS_OK;
+}
+
+int emu_gemm(const GemmParams& p, Ctx& cx, cudaStream_t st) {
+  if (cx.opt[HPS_OPT_EMU_MODULI] > 0) return emu_gemm_crt(p, cx, st);
+  return emu_gemm_slices(p, cx, st);
 }
 
 }  // namespace hps

@@ -101,7 +101,7 @@ int dgemm_launch(const GemmParams& p, Ctx& cx, cudaStream_t stream) {
     set_error("dgemm: K=%d", p.K);
     return HPS_ERR_ARG;
   }
-  if (p.emu_ok && cx.opt[HPS_OPT_EMU_SLICES] > 0) {
+  if (p.emu_ok && (cx.opt[HPS_OPT_EMU_MODULI] > 0 || cx.opt[HPS_OPT_EMU_SLICES] > 0)) {
     const int r = emu_gemm(p, cx, stream);
     if (r != 1) return r;  // 1: not eligible here, run on DMMA
   }

@@ -1,0 +1,327 @@
+// Batched int8 GEMM with a modular epilogue on the 5th-generation tensor cores (tcgen05), for the
+// modular FP64 emulation of the merge GEMMs (emu.cu; merge.py:108, 118):
+//
+//   R[z][i][j] = ((sum_k A[z][i][k] B[z][j0 + j][k]) mod m_(z / batch)) + 128,  in [0, 255] (uint8:
+//                the symmetric residue in [-128, 127], biased),
+//   A: [nz][M][K] int8, B: [nz][N][K] int8 (both K-contiguous), j < nc (an output column panel).
+//
+// Persistent, warp-specialised, one CTA per SM (192 threads):
+//   warp 0    TMA producer: 128 x 128 B (A) and 256 x 128 B (B) boxes with the 128-byte swizzle
+//             into a 4-stage shared-memory ring (full / empty mbarriers, expect-tx byte counts);
+//   warp 1    allocates all 512 TMEM columns; one lane issues tcgen05.mma.kind::i8 (M = 128,
+//             N = 256, K = 32 per instruction; 4 per stage) into one of two 256-column int32
+//             accumulators, releases each stage with tcgen05.commit, and signals the epilogue;
+//   warps 2-5 epilogue: tcgen05.ld 32x32b (each warp its 32-lane quadrant of TMEM), the exact
+//             int32 sums reduced mod m (multiply-high quotient, no conversions), 32 bytes per row
+//             chunk stored; the accumulator is released to the MMA warp while the next tile's
+//             MMAs run in the other one.
+// Tiles are ordered in groups of 8 tile rows so that the concurrent wave's A and B panels stay in L2.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+#include "ctx.cuh"
+
+namespace hps {
+namespace i8 {
+
+constexpr int BM = 128, BN = 256, BK = 128;  // BK: bytes = int8 elements of K per stage
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK, B_BYTES = BN * BK, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 192;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int GROUP_M = 8;
+constexpr int MAX_MOD = 16;
+
+struct ModTab {
+  int m[MAX_MOD];
+  int minv[MAX_MOD];
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// Bounded wait: a protocol error traps (a launch failure) instead of hanging the device.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  for (long long i = 0;; ++i) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (i > (1LL << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor of a K-major tile with the 128-byte swizzle: rows of 128 bytes,
+// 8-row (1024-byte) core-matrix groups; start address >> 4, LBO 16 B (unused when swizzled), SBO
+// 1024 B, descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// Instruction descriptor: D s32, A / B signed int8, both K-major, N >> 3, M >> 4.
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tile_coords(long long t, int tm, int tn, int& z, int& mi, int& ni) {
+  const long long per = (long long)tm * tn;
+  z = (int)(t / per);
+  const int r = (int)(t - (long long)z * per);
+  const int g = r / (GROUP_M * tn), first = g * GROUP_M, gs = min(GROUP_M, tm - first);
+  const int rr = r - g * GROUP_M * tn;
+  mi = first + rr % gs;
+  ni = rr / gs;
+}
+
+// (v mod m) + 128 in [0, 255] for |v| < 2^30: v + m ceil(2^30 / m) is in [0, 2^31), its
+// multiply-high quotient (minv = floor(2^32 / m)) is the floor or one less, so the remainder is in
+// [0, 2m); one correction, then the symmetric representative, biased.
+__device__ __forceinline__ uint32_t mod_byte(uint32_t u, int m, int minv, int off) {
+  const unsigned v = (unsigned)((int)u + off);
+  const int q = (int)__umulhi(v, (unsigned)minv);
+  int r = (int)v - q * m;
+  r = r >= m ? r - m : r;
+  r = r > 127 ? r - m : r;
+  return (uint32_t)(r + 128);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_i8gemm_mod(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int nc, int j0,
+                 int K, int nz, int batch, ModTab mt, unsigned char* __restrict__ R) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]; then the TMEM base address
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  const uint32_t sbase = su32(smem);
+  const uint32_t full0 = su32(bars), empty0 = full0 + 8 * STAGES, tfull0 = empty0 + 8 * STAGES, tempty0 = tfull0 + 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tm = (M + BM - 1) / BM, tn = (nc + BN - 1) / BN;
+  const long long tiles = (long long)nz * tm * tn;
+  const int nk = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int z, mi, ni;
+        tile_coords(t, tm, tn, z, mi, ni);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          const uint32_t fb = full0 + 8 * s;
+          mbar_expect_tx(fb, STAGE_BYTES);
+          const uint32_t dst = sbase + s * STAGE_BYTES;
+          tma_load3(dst, &ta, fb, kb * BK, mi * BM, z);
+          tma_load3(dst + A_BYTES, &tb, fb, kb * BK, j0 + ni * BN, z);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(tempty0 + 8 * acc, aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint64_t a0 = sw128_desc(sbase + s * STAGE_BYTES);
+          const uint64_t b0 = sw128_desc(sbase + s * STAGE_BYTES + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k)  // +32 bytes along K inside the swizzle atom: +2 in the >> 4 address
+            umma_i8(d, a0 + 2 * k, b0 + 2 * k, (kb | k) != 0);
+          umma_commit(empty0 + 8 * s);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(tfull0 + 8 * acc);
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      int z, mi, ni;
+      tile_coords(t, tm, tn, z, mi, ni);
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(tfull0 + 8 * acc, aph);
+      tc_fence_after();
+      const int row = mi * BM + q * 32 + lane;
+      const int l = z / batch;
+      const int m = mt.m[l];
+      const int minv = mt.minv[l], off = m * ((1 << 30) / m + 1);
+      unsigned char* dst = R + ((long long)z * M + row) * nc + ni * BN;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + c * 32, v);
+        if (row < M && ni * BN + c * 32 < nc) {
+          uint32_t w[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            w[i] = mod_byte(v[4 * i], m, minv, off) | (mod_byte(v[4 * i + 1], m, minv, off) << 8) |
+                   (mod_byte(v[4 * i + 2], m, minv, off) << 16) | (mod_byte(v[4 * i + 3], m, minv, off) << 24);
+          uint4* o = reinterpret_cast<uint4*>(dst + c * 32);
+          o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// [nz][rows][K] int8, boxes of 128 K-bytes x box_rows rows x 1, 128-byte swizzle, zero fill out of bounds
+static bool make_map(CUtensorMap* map, const void* base, int K, int rows, int nz, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)K, (cuuint64_t)K * (cuuint64_t)rows};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace i8
+
+// Eligibility of the tcgen05 path for a panel product (the caller falls back to cuBLASLt otherwise).
+bool i8gemm_mod_ok(int M, int N, int nc, int K, int nmod) {
+  return i8::encode_fn() != nullptr && nmod <= i8::MAX_MOD && K % 16 == 0 && N % 16 == 0 && nc % 32 == 0 && M > 0 &&
+         nc > 0;
+}
+
+// R[z][i][j] (uint8, [nz][M][nc]) = (A[z] B[z][j0 + j]^T) mod moduli[z / batch] + 128; see the top of the file.
+int i8gemm_mod(const signed char* A, const signed char* B, unsigned char* R, int M, int N, int nc, int j0, int K, int nz,
+               int batch, const int* moduli, int nmod, Ctx& cx, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  if (!i8::make_map(&ta, A, K, M, nz, i8::BM) || !i8::make_map(&tb, B, K, N, nz, i8::BN)) {
+    set_error("i8gemm_mod: cuTensorMapEncodeTiled failed (M=%d N=%d K=%d nz=%d)", M, N, K, nz);
+    return HPS_ERR_CUDA;
+  }
+  i8::ModTab mt;
+  for (int l = 0; l < i8::MAX_MOD; ++l) {
+    mt.m[l] = l < nmod ? moduli[l] : 1;
+    mt.minv[l] = (int)((1ULL << 32) / (unsigned long long)mt.m[l]);
+  }
+  int st_attr = ensure_smem_attr(reinterpret_cast<const void*>(&i8::k_i8gemm_mod), cx.device, i8::SMEM);
+  if (st_attr != HPS_OK) return st_attr;
+  const long long tiles = (long long)nz * ((M + i8::BM - 1) / i8::BM) * ((nc + i8::BN - 1) / i8::BN);
+  const int grid = (int)std::min<long long>(tiles, cx.sms);
+  i8::k_i8gemm_mod<<<grid, i8::THREADS, i8::SMEM, st>>>(ta, tb, M, nc, j0, K, nz, batch, mt, R);
+  HPS_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+}  // namespace hps

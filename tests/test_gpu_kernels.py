@@ -183,21 +183,93 @@ def test_lookahead_refuses_odd_batch():
     assert r == _native.HPS_ERR_ARG and "even nbatch" in _native.last_error()
 
 
-@pytest.mark.parametrize("slices", [8, 6])
+@pytest.mark.parametrize("scheme,count", [("slices", 8), ("slices", 6), ("moduli", 14), ("moduli", 12)])
 @pytest.mark.parametrize("M,N,K,B", [(512, 768, 256, 1), (1024, 256, 512, 3), (256, 4096, 1024, 2)])
-def test_emulated_dgemm_accuracy(M, N, K, B, slices):
-    """FP64 GEMM on the int8 tensor cores (emu.cu): with 8 slices the error is at or below the DMMA
-    GEMM's against an exact (long double) reference, with rows / columns spanning 16 decades; with 6
-    slices it is within 2^-40 of the row x column scale."""
+def test_emulated_dgemm_accuracy(M, N, K, B, scheme, count):
+    """FP64 GEMM on the int8 tensor cores (emu.cu): with 8 slices or 14 moduli the error is at or
+    below the DMMA GEMM's against an exact (long double) reference, with rows / columns spanning 16
+    decades; with 6 slices or 12 moduli it is within 2^-40 of the row x column scale."""
     lib = _native.load()
-    rng = np.random.default_rng(M + N + K + slices)
+    rng = np.random.default_rng(M + N + K + count)
     A = rng.standard_normal((B, M, K)) * 10.0 ** rng.uniform(-8, 8, (B, M, 1))
     Bm = rng.standard_normal((B, K, N)) * 10.0 ** rng.uniform(-8, 8, (B, 1, N))
     exact = np.einsum("bmk,bkn->bmn", A.astype(np.longdouble), Bm.astype(np.longdouble))
     scale = np.abs(A).max(axis=2)[:, :, None] * np.abs(Bm).max(axis=1)[:, None, :] * K
     errs = {}
-    for name, nsl in (("dmma", 0), ("emu", slices)):
-        cx = _native.Context(0, emu_slices=nsl, emu_min_work=1, emu_min_k=16)
+    opts = {"dmma": dict(emu_slices=0, emu_moduli=0),
+            "emu": dict(emu_slices=count, emu_moduli=0) if scheme == "slices" else dict(emu_slices=0, emu_moduli=count)}
+    for name, o in opts.items():
+        cx = _native.Context(0, emu_min_work=1, emu_min_k=16, **o)
+        try:
+            tA, tB = cuda(A), cuda(Bm)
+            tC = torch.zeros((B, M, N), dtype=torch.float64, device="cuda")
+            n0 = lib.hps_launch_count()
+            _native.check(lib.hps_dgemm_batched(cx, M, N, K, B, 1.0, _native.ptr(tA), K, M * K, _native.ptr(tB), N,
+                                                K * N, None, 0, 0.0, _native.ptr(tC), N, M * N, _native.stream_ptr()),
+                          "gemm")
+            torch.cuda.synchronize()
+            launches = lib.hps_launch_count() - n0
+            errs[name] = float((np.abs(tC.cpu().numpy() - exact) / scale).max())
+        finally:
+            cx.close()
+        if name == "emu":
+            assert launches >= 5, launches  # the emulated path ran (scales, residues / digits, products, accumulation)
+    print(f"M={M} N={N} K={K}: max error / (K max|a_i| max|b_j|): DMMA {errs['dmma']:.2e}, "
+          f"emulated ({count} {scheme}) {errs['emu']:.2e}")
+    if count in (8, 14):
+        assert errs["emu"] <= max(2 * errs["dmma"], 2.0 ** -52), errs
+    else:
+        assert errs["emu"] <= 2.0 ** -40, errs
+
+
+@pytest.mark.parametrize("moduli", [14, 16])
+def test_emulated_dgemm_nonfinite_and_panels(moduli):
+    """Modular emulation: output column panels (a small scratch cap forces several), the merge's
+    alpha, a non-finite row (NaN row of the output, flagged like the DMMA path) and zero rows."""
+    lib = _native.load()
+    M, N, K, B = 256, 1040, 512, 2
+    rng = np.random.default_rng(moduli)
+    A = rng.standard_normal((B, M, K))
+    Bm = rng.standard_normal((B, K, N))
+    A[1, 5, 7] = np.inf
+    A[0, 9, :] = 0.0
+    exact = np.einsum("bmk,bkn->bmn", A.astype(np.longdouble), Bm.astype(np.longdouble)) * -2.0
+    cx = _native.Context(0, emu_min_work=1, emu_min_k=16, emu_slices=0, emu_moduli=moduli, emu_scratch_mb=1)
+    try:
+        tA, tB = cuda(A), cuda(Bm)
+        tC = torch.zeros((B, M, N), dtype=torch.float64, device="cuda")
+        _native.check(lib.hps_dgemm_batched(cx, M, N, K, B, -2.0, _native.ptr(tA), K, M * K, _native.ptr(tB), N,
+                                            K * N, None, 0, 0.0, _native.ptr(tC), N, M * N, _native.stream_ptr()),
+                      "gemm")
+        C = tC.cpu().numpy()
+    finally:
+        cx.close()
+    assert np.isnan(C[1, 5]).all()
+    assert (C[0, 9] == 0.0).all()
+    ok = np.ones(C.shape, bool)
+    ok[1, 5] = False
+    scale = np.abs(A[..., :]).max(axis=2)[:, :, None] * np.abs(Bm).max(axis=1)[:, None, :] * K
+    scale[1, 5] = 1.0
+    scale[0, 9] = 1.0
+    err = float((np.abs(C - exact)[ok] / scale[ok]).max())
+    assert err <= 2.0 ** -50, err
+
+
+@pytest.mark.parametrize("M,N,K,B,mb", [(200, 544, 272, 3, 8192), (200, 544, 272, 3, 1), (1024, 1024, 1024, 2, 8192),
+                                        (384, 4096, 2048, 1, 8192), (130, 96, 1040, 5, 8192)])
+def test_emulated_dgemm_engines_bitwise(M, N, K, B, mb):
+    """Modular emulation: the hand-written tcgen05 int8 kernel (TMA, TMEM accumulators, residues
+    reduced in its epilogue) and cuBLASLt's IMMA GEMM compute the same exact integer residues, so
+    the reconstructed FP64 products are bitwise equal; partial tiles in M, N and K, batches and
+    output column panels (mb: scratch cap in MB) included."""
+    lib = _native.load()
+    rng = np.random.default_rng(M * N + K)
+    A = rng.standard_normal((B, M, K)) * 10.0 ** rng.uniform(-4, 4, (B, M, 1))
+    Bm = rng.standard_normal((B, K, N))
+    out = {}
+    for engine in (0, 1):
+        cx = _native.Context(0, emu_min_work=1, emu_min_k=16, emu_slices=0, emu_moduli=14, emu_engine=engine,
+                             emu_scratch_mb=mb)
         try:
             tA, tB = cuda(A), cuda(Bm)
             tC = torch.zeros((B, M, N), dtype=torch.float64, device="cuda")
@@ -205,12 +277,13 @@ def test_emulated_dgemm_accuracy(M, N, K, B, slices):
                                                 K * N, None, 0, 0.0, _native.ptr(tC), N, M * N, _native.stream_ptr()),
                           "gemm")
             torch.cuda.synchronize()
-            errs[name] = float((np.abs(tC.cpu().numpy() - exact) / scale).max())
+            out[engine] = tC.cpu().numpy()
         finally:
             cx.close()
-    print(f"M={M} N={N} K={K}: max error / (K max|a_i| max|b_j|): DMMA {errs['dmma']:.2e}, "
-          f"emulated ({slices} slices) {errs['emu']:.2e}")
-    if slices == 8:
-        assert errs["emu"] <= max(2 * errs["dmma"], 2.0 ** -52), errs
-    else:
-        assert errs["emu"] <= 2.0 ** -40, errs
+    exact = np.einsum("bmk,bkn->bmn", A.astype(np.longdouble), Bm.astype(np.longdouble))
+    scale = np.abs(A).max(axis=2)[:, :, None] * np.abs(Bm).max(axis=1)[:, None, :] * K
+    err = float((np.abs(out[0] - exact) / scale).max())
+    print(f"M={M} N={N} K={K} B={B}: tcgen05 vs cuBLASLt max |diff| {np.abs(out[0] - out[1]).max():.1e}, "
+          f"error {err:.2e}")
+    assert np.array_equal(out[0], out[1])
+    assert err <= 2.0 ** -52
