@@ -57,7 +57,14 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="enqueue the build eagerly instead of replaying CUDA graphs")
     ap.add_argument("--emu-slices", type=int, default=None,
-                    help="FP64 GEMM emulation on the int8 tensor cores: slices per operand (0 = DMMA only)")
+                    help="FP64 GEMM emulation on the int8 tensor cores, slice scheme: slices per operand (used when "
+                         "--emu-moduli is 0)")
+    ap.add_argument("--emu-moduli", type=int, default=None,
+                    help="FP64 GEMM emulation, modular scheme: moduli (default 14; 0 = slice scheme or, with "
+                         "--emu-slices 0, DMMA only)")
+    ap.add_argument("--emu-engine", type=int, default=None,
+                    help="int8 products of the modular scheme: 0 = the library's tcgen05 kernel (default), 1 = cuBLASLt")
+    ap.add_argument("--emu-min-k", type=int, default=None, help="emulate merge GEMMs with K >= this (default 1024)")
     ap.add_argument("--validate-reference-model", action="store_true",
                     help="time whole oracle-port steps at configs 2 (L=6) and 3 (L=7) against the sampled model")
     ap.add_argument("--full-reference", action="store_true",
@@ -105,6 +112,28 @@ def int8_peak():
             return 2.0 * float(json.load(f)["bf16_tflops"]), "2 x MEASURED_PEAKS.json bf16_tflops (int8 = 2x bf16 on sm_100)"
     except Exception:
         return 2.0 * 1590.0, "2 x fallback bf16 1.59 PFLOP/s (B200_PROFILING.md)"
+
+
+def configure_emulation(args):
+    """Apply the --emu-* options to every context slot; return the scheme that runs (csrc/emu.cu)."""
+    from paper_1307_2665_b200 import _native
+
+    for name in ("emu_slices", "emu_moduli", "emu_engine", "emu_min_k"):
+        v = getattr(args, name)
+        if v is not None:
+            for slot in range(4):
+                _native.context(slot).set(name, v)
+    cx = _native.context()
+    moduli, slices = cx.get("emu_moduli"), cx.get("emu_slices")
+    engine = cx.get("emu_engine")
+    if moduli > 0:
+        return {"scheme": "modular", "moduli": moduli, "int8_products_per_gemm": moduli,
+                "engine": "hps::i8::k_i8gemm_mod (tcgen05.mma.kind::i8, TMA, TMEM)" if engine == 0 else "cuBLASLt IMMA",
+                "min_k": cx.get("emu_min_k")}
+    if slices > 0:
+        return {"scheme": "slices", "slices": slices, "int8_products_per_gemm": slices * (slices + 1) // 2,
+                "engine": "cuBLASLt IMMA", "min_k": cx.get("emu_min_k")}
+    return {"scheme": "off", "int8_products_per_gemm": 0}
 
 
 def hbm_peak():
@@ -256,10 +285,7 @@ def main():
         return bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, world)
     dev = torch.device("cuda")
     lib = _native.load()
-    if args.emu_slices is not None:
-        for slot in range(4):
-            _native.context(slot).set("emu_slices", args.emu_slices)
-    emu_slices = _native.context().get("emu_slices")
+    emu = configure_emulation(args)
     tree, nodes = P.build_tree(P.Rectangle(0.0, 1.0, 0.0, 1.0), L, q)
     co = c.coefficients()
     F_host = problems.boundary_data(cfg, nodes.points[tree.root.I_e], seed=0, batch=b)
@@ -358,20 +384,24 @@ def main():
         "solve": {"tflops": solve_flops / ts / 1e12, "frac_fp64": solve_flops / ts / 1e12 / peak,
                   "gbs_S_stream": S_bytes / ts / 1e9, "frac_hbm": S_bytes / ts / 1e9 / hpeak, "hbm_peak_source": hsrc},
     }
-    if dom.startswith("merge_d") and emu_slices > 0:
+    if dom.startswith("merge_d") and emu["int8_products_per_gemm"] > 0:
         dd = int(dom.split("_d")[-1])
-        ops = Wk.emulated_int8_ops(L, q, dd, emu_slices)
+        ops = Wk.emulated_int8_ops(L, q, dd, emu["int8_products_per_gemm"], min_k=emu["min_k"])
         if ops > 0:
             # the dominant stage's bulk runs on the int8 tensor cores: its roofline is the int8 rate;
             # its FP64-equivalent rate (the algorithmic FP64 flops over the stage time) goes beside it
             i8peak, i8src = int8_peak()
             i8 = ops / (stage_ms[dom] / 1e3) / 1e12
+            if emu["scheme"] == "modular":
+                how = (f"{emu['moduli']} int8 products (one per modulus) on {emu['engine']}, residues reduced in its "
+                       f"epilogue; hps::k_crt_split_rows/cols (residues), k_crt_accum (CRT reconstruction + merge epilogue)")
+            else:
+                how = (f"{emu['slices']} slices, {emu['int8_products_per_gemm']} int8 products each on cuBLASLt IMMA; "
+                       f"hps::k_emu_split_* / k_emu_accum")
             roofline.update({
                 "bound": "tensor", "achieved": i8, "peak": i8peak, "unit": "TOPS (int8)", "frac": i8 / i8peak,
                 "peak_source": i8src,
-                "kernels": (f"{dom}: S and T GEMMs as FP64 emulation on the int8 tensor cores ({emu_slices} slices, "
-                            f"{emu_slices * (emu_slices + 1) // 2} int8 products each, cuBLASLt IMMA) + hps::k_emu_split_* "
-                            f"/ k_emu_accum; interface inverse on DMMA"),
+                "kernels": f"{dom}: S and T GEMMs as FP64 emulation on the int8 tensor cores ({how}); interface inverse on DMMA",
                 "fp64_equivalent": {"achieved_tflops": ach, "fp64_dmma_peak_tflops": peak, "ratio_to_fp64_peak": ach / peak,
                                     "note": "algorithmic FP64 flops of the stage / stage time"}})
     # ---- end-to-end through the public API (solver.Pipeline), pinned host memory ----
@@ -443,7 +473,7 @@ def main():
             "launch": launch_mode,
             "stages": {"unknowns": unknowns, "batch": b, "leaf_groups": inp.ngroups,
                        "pivoted_lu_depths": sorted(pivoted),
-                       "fp64_gemm_emulation_slices": emu_slices,
+                       "fp64_gemm_emulation": emu,
                        "build_ms": tb * 1e3, "solve_ms": ts * 1e3,
                        "build_unknowns_per_s": unknowns / tb, "solve_unknowns_per_s": unknowns * b / ts,
                        "build_fp64_tflops": roofline["build_tflops"], "build_fp64_frac": roofline["build_frac"],
@@ -464,10 +494,7 @@ def bench_distributed(args, cfg, c, L, b, q, unknowns, workload, metric, rank, w
 
     dev = torch.device("cuda")
     lib = _native.load()
-    if args.emu_slices is not None:
-        for slot in range(4):
-            _native.context(slot).set("emu_slices", args.emu_slices)
-    emu_slices = _native.context().get("emu_slices")
+    emu = configure_emulation(args)
     tree, nodes = P.build_tree(P.Rectangle(0.0, 1.0, 0.0, 1.0), L, q)
     co = c.coefficients()
     F = None

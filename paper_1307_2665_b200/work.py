@@ -71,7 +71,7 @@ def build_roofline_seconds(L, q, ngroups, f64_tflops, hbm_gbs):
 
 
 def emulated_gemms(L, q, d, min_k=1024, min_work=2 ** 32):
-    """(M, N, K, batch) of the merge GEMMs of depth d that run as the int8-sliced FP64 emulation
+    """(M, N, K, batch) of the merge GEMMs of depth d that run as the FP64 emulation on int8
     (csrc/emu.cu: K >= min_k and M N K batch >= min_work): S = X^-1 R (n3 x ne x n3) and
     T = blk + C S (ne x ne x n3), 2^d merges."""
     n3, ne = depth_sizes(L, q, d)
@@ -82,8 +82,9 @@ def emulated_gemms(L, q, d, min_k=1024, min_work=2 ** 32):
     return out
 
 
-def emulated_int8_ops(L, q, d, slices, **kw):
-    """int8 tensor operations of depth d's emulated GEMMs: slices (slices + 1) / 2 products of 2 M N K."""
-    if slices <= 0:
+def emulated_int8_ops(L, q, d, products, **kw):
+    """int8 tensor operations of depth d's emulated GEMMs: `products` int8 products of 2 M N K each
+    (the modular scheme: one per modulus; the slice scheme: s (s + 1) / 2)."""
+    if products <= 0:
         return 0.0
-    return sum(slices * (slices + 1) / 2 * 2.0 * M * N * K * b for M, N, K, b in emulated_gemms(L, q, d, **kw))
+    return sum(products * 2.0 * M * N * K * b for M, N, K, b in emulated_gemms(L, q, d, **kw))
