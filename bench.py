@@ -63,7 +63,8 @@ def parse():
                     help="FP64 GEMM emulation, modular scheme: moduli (default 14; 0 = slice scheme or, with "
                          "--emu-slices 0, DMMA only)")
     ap.add_argument("--emu-engine", type=int, default=None,
-                    help="int8 products of the modular scheme: 0 = the library's tcgen05 kernel (default), 1 = cuBLASLt")
+                    help="int8 products of the modular scheme: 0 = the library's tcgen05 kernel (default), 2 = its "
+                         "CTA-pair variant, 1 = cuBLASLt")
     ap.add_argument("--emu-min-k", type=int, default=None, help="emulate merge GEMMs with K >= this (default 1024)")
     ap.add_argument("--validate-reference-model", action="store_true",
                     help="time whole oracle-port steps at configs 2 (L=6) and 3 (L=7) against the sampled model")
@@ -128,7 +129,9 @@ def configure_emulation(args):
     engine = cx.get("emu_engine")
     if moduli > 0:
         return {"scheme": "modular", "moduli": moduli, "int8_products_per_gemm": moduli,
-                "engine": "hps::i8::k_i8gemm_mod (tcgen05.mma.kind::i8, TMA, TMEM)" if engine == 0 else "cuBLASLt IMMA",
+                "engine": {0: "hps::i8::k_i8gemm_mod (tcgen05.mma.kind::i8, TMA, TMEM; single CTAs)",
+                           2: "hps::i8::k_i8gemm_mod_pair (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM; CTA pairs)"
+                           }.get(engine, "cuBLASLt IMMA"),
                 "min_k": cx.get("emu_min_k")}
     if slices > 0:
         return {"scheme": "slices", "slices": slices, "int8_products_per_gemm": slices * (slices + 1) // 2,

@@ -60,8 +60,9 @@ typedef struct hps_ctx_s* hps_ctx_t;
                                        (14, FP64-equivalent; 6..16; 0 = off) with Chinese-remainder
                                        reconstruction; takes precedence over HPS_OPT_EMU_SLICES */
 #define HPS_OPT_EMU_SCRATCH_MB 10   /* cap on the modular scheme's product scratch (8192 MB) */
-#define HPS_OPT_EMU_ENGINE 11       /* int8 products of the modular scheme: 0 = this library's tcgen05 kernel
-                                       (TMA + TMEM, residues reduced in its epilogue), 1 = cuBLASLt IMMA */
+#define HPS_OPT_EMU_ENGINE 11       /* int8 products of the modular scheme: this library's tcgen05 kernel (TMA +
+                                       TMEM, residues reduced in its epilogue) on single CTAs, 128 x 256 tiles (0)
+                                       or CTA pairs, 256 x 256 tiles (2); cuBLASLt IMMA (1) */
 #define HPS_OPT_COUNT 12
 int hps_ctx_create(int device, hps_ctx_t* out);
 int hps_ctx_destroy(hps_ctx_t ctx);

@@ -104,6 +104,23 @@ double* Ctx::emu_scratch(size_t n, cudaStream_t st) {
   return emu_buf[r];
 }
 
+double* Ctx::gather_scratch(size_t n, cudaStream_t st) {
+  const int r = role(st);
+  if (n > gather_n[r]) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    double* fresh = nullptr;
+    if (cudaMalloc(&fresh, n * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    if (gather_buf[r]) retired.push_back(gather_buf[r]);
+    gather_buf[r] = fresh;
+    gather_n[r] = n;
+  }
+  return gather_buf[r];
+}
+
 int ensure_smem_attr(const void* kernel, int device, int bytes) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> done;
@@ -167,6 +184,8 @@ extern "C" int hps_ctx_destroy(hps_ctx_t handle) {
   for (auto p : c->splitk)
     if (p) cudaFree(p);
   for (auto p : c->emu_buf)
+    if (p) cudaFree(p);
+  for (auto p : c->gather_buf)
     if (p) cudaFree(p);
   if (c->emu && c->emu_free) c->emu_free(c->emu);
   for (auto p : c->retired) cudaFree(p);

@@ -54,6 +54,10 @@ struct Ctx {
   double* emu_buf[4] = {};
   size_t emu_n[4] = {};
   double* emu_scratch(size_t n, cudaStream_t st);
+  // gathered operands (the batched solve's boundary rows), per stream role
+  double* gather_buf[4] = {};
+  size_t gather_n[4] = {};
+  double* gather_scratch(size_t n, cudaStream_t st);
 };
 
 // Context of a C-ABI call: a valid handle whose device is the caller's current device.

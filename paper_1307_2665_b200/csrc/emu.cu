@@ -16,7 +16,8 @@
 // (~K 2^-53 |A||B|). The products run on cuBLASLt's int8 GEMM (a plain library GEMM); the scaling,
 // digit splitting, fp64 accumulation and the merge epilogue (the block-diagonal addend, the
 // non-finite flag) are the kernels here. Used by dgemm_launch when the context enables it
-// (HPS_OPT_EMU_SLICES) and the GEMM is large and plain (beta = 0, no row gather).
+// (HPS_OPT_EMU_SLICES) and the GEMM is large and plain (beta = 0, no row gather; the modular scheme
+// also takes beta != 0).
 #include <cublasLt.h>
 
 #include <algorithm>
@@ -258,8 +259,8 @@ static EmuPlan* emu_plan(EmuState* es, int M, int N, int kp, int sK, int batch) 
 // Shape / alignment test shared by both schemes: it pays where a GEMM is FP64-bound, K >=
 // HPS_OPT_EMU_MIN_K (each output element costs 2 K DMMA flops against the per-element conversion
 // and reconstruction traffic).
-static bool emu_eligible(const GemmParams& p, const Ctx& cx) {
-  if (p.Bidx || p.beta != 0.0 || p.split > 1) return false;
+static bool emu_eligible(const GemmParams& p, const Ctx& cx, bool beta_ok = false) {
+  if (p.Bidx || (p.beta != 0.0 && !beta_ok) || (p.beta != 0.0 && p.blk_j1a) || p.split > 1) return false;
   const double work = (double)p.M * p.N * p.K;
   if (work * p.batch < (double)cx.opt[HPS_OPT_EMU_MIN_WORK] || p.K < cx.opt[HPS_OPT_EMU_MIN_K] || p.M % 4 ||
       p.N % 4 || p.K % 16)
@@ -634,10 +635,18 @@ __global__ void __launch_bounds__(256) k_crt_accum(const TIn* __restrict__ Cl, i
                                                         : crt_scale(cp, -(sr + tj[u]));
         w *= p.alpha;
         if (p.blk_j1a) w += blk_value(p, b, r, j0 + c4 + u);
-        bad |= !isfinite(w);
         v[u] = w;
       }
       double* dst = p.C + (long long)b * p.strideC + (long long)r * p.ldc + j0 + c4;
+      if (p.beta != 0.0) {  // C = alpha A B + beta C
+        const double2 o0 = *reinterpret_cast<const double2*>(dst), o1 = *reinterpret_cast<const double2*>(dst + 2);
+        v[0] = fma(p.beta, o0.x, v[0]);
+        v[1] = fma(p.beta, o0.y, v[1]);
+        v[2] = fma(p.beta, o1.x, v[2]);
+        v[3] = fma(p.beta, o1.y, v[3]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bad |= !isfinite(v[u]);
       *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
       *reinterpret_cast<double2*>(dst + 2) = make_double2(v[2], v[3]);
     }
@@ -700,16 +709,16 @@ static EmuPlan* crt_plan(EmuState* es, int M, int nc, int K, long long strideB, 
 
 bool i8gemm_mod_ok(int M, int N, int nc, int K, int nmod);  // i8gemm.cu
 int i8gemm_mod(const signed char* A, const signed char* B, unsigned char* R, int M, int N, int nc, int j0, int K, int nz,
-               int batch, const int* moduli, int nmod, Ctx& cx, cudaStream_t st);
+               int batch, const int* moduli, int nmod, bool pair, Ctx& cx, cudaStream_t st);
 
 static int emu_gemm_crt(const GemmParams& p, Ctx& cx, cudaStream_t st) {
   const int n = (int)cx.opt[HPS_OPT_EMU_MODULI];
-  if (!emu_eligible(p, cx) || p.K >= (1 << 16)) return 1;  // |C_l| <= K 2^14 < 2^30
+  if (!emu_eligible(p, cx, true) || p.K >= (1 << 16)) return 1;  // |C_l| <= K 2^14 < 2^30
   CrtConst c;
   if (!crt_constants(n, c)) return 1;
   // output column panels: the n products of a panel fit the scratch cap; panel widths are multiples
   // of 256 (the kernel's tile width) where the cap allows
-  const bool own = cx.opt[HPS_OPT_EMU_ENGINE] == 0;
+  const bool own = cx.opt[HPS_OPT_EMU_ENGINE] != 1;  // 0: tcgen05 single CTAs, 2: CTA pairs, 1: cuBLASLt
   const size_t elt = own ? 1 : sizeof(int);  // the tcgen05 kernel stores residues, cuBLASLt int32 sums
   const size_t cap = (size_t)std::max<long long>(1, cx.opt[HPS_OPT_EMU_SCRATCH_MB]) << 20;
   const size_t per_col = (size_t)n * p.batch * p.M * elt;
@@ -761,7 +770,7 @@ static int emu_gemm_crt(const GemmParams& p, Ctx& cx, cudaStream_t st) {
     const int w = std::min(nc, p.N - j0);
     if (use_own) {
       const int r = i8gemm_mod(Ar, Br, reinterpret_cast<unsigned char*>(Cl), p.M, p.N, w, j0, p.K, nb, p.batch,
-                               kModuli, n, cx, st);
+                               kModuli, n, cx.opt[HPS_OPT_EMU_ENGINE] == 2, cx, st);
       if (r != HPS_OK) return r;
     } else {
       const EmuPlan* pl = w == nc ? full : tail;

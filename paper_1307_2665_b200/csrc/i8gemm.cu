@@ -261,6 +261,194 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a 256 x 256 tile. Each
+// CTA stages its 128 rows of A and its 128 rows (half) of B per k-block (32 KB; 6 stages), so the
+// L2 -> SM traffic per MMA is 2/3 of the single-CTA tile's; the even CTA's one lane issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256) over both CTAs' shared memory, and each CTA's TMEM
+// holds its 128 accumulator rows. Both CTAs' TMA loads complete on the even CTA's full barrier;
+// the MMA commits are multicast to both CTAs' empty / tmem-full barriers; both CTAs' epilogue warps
+// release an accumulator on the even CTA's tmem-empty barrier (8 arrivals).
+// ------------------------------------------------------------------------------------------------
+namespace pair {
+constexpr int BM = 256, BN = 256, BK = 128;  // pair tile; per CTA: 128 rows of A, 128 rows of B
+constexpr int STAGES = 6;
+constexpr int A_BYTES = 128 * BK, B_BYTES = 128 * BK, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}  // namespace pair
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank0(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void tma_load3_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_rank0, int c0, int c1,
+                                               int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_rank0), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma_i8_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(pair::kIdesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {  // arrive on `bar` in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((unsigned short)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_i8gemm_mod_pair(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int nc,
+                      int j0, int K, int nz, int batch, ModTab mt, unsigned char* __restrict__ R) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + pair::STAGES * pair::STAGE_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * pair::STAGES + 4);
+  const uint32_t sbase = su32(smem);
+  const uint32_t full0 = su32(bars), empty0 = full0 + 8 * pair::STAGES, tfull0 = empty0 + 8 * pair::STAGES, tempty0 = tfull0 + 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int tm = (M + pair::BM - 1) / pair::BM, tn = (nc + pair::BN - 1) / pair::BN;
+  const long long tiles = (long long)nz * tm * tn;
+  const int nk = (K + pair::BK - 1) / pair::BK;
+  const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < pair::STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);   // used in the even CTA: its producer's expect-tx arrival
+      mbar_init(empty0 + 8 * s, 1);  // one multicast commit per use
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 8);  // even CTA: 4 epilogue warps of each CTA
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long t = cid; t < tiles; t += ncl) {
+        int z, mi, ni;
+        tile_coords(t, tm, tn, z, mi, ni);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          const uint32_t fb = full0 + 8 * s;
+          if (rank == 0) mbar_expect_tx(fb, 2 * pair::STAGE_BYTES);  // both CTAs' bytes land on the even CTA's barrier
+          const uint32_t fb0 = map_to_rank0(fb);
+          const uint32_t dst = sbase + s * pair::STAGE_BYTES;
+          tma_load3_pair(dst, &ta, fb0, kb * pair::BK, mi * pair::BM + (int)rank * 128, z);
+          tma_load3_pair(dst + pair::A_BYTES, &tb, fb0, kb * pair::BK, j0 + ni * pair::BN + (int)rank * 128, z);
+          if (++s == pair::STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (long long t = cid; t < tiles; t += ncl, ++it) {
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(tempty0 + 8 * acc, aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * pair::BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint64_t a0 = sw128_desc(sbase + s * pair::STAGE_BYTES);
+          const uint64_t b0 = sw128_desc(sbase + s * pair::STAGE_BYTES + pair::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < pair::BK / 32; ++k) umma_i8_pair(d, a0 + 2 * k, b0 + 2 * k, (kb | k) != 0);
+          umma_commit_pair(empty0 + 8 * s);
+          if (++s == pair::STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit_pair(tfull0 + 8 * acc);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const uint32_t tempty_rank0 = map_to_rank0(tempty0);
+    int it = 0;
+    for (long long t = cid; t < tiles; t += ncl, ++it) {
+      int z, mi, ni;
+      tile_coords(t, tm, tn, z, mi, ni);
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(tfull0 + 8 * acc, aph);
+      tc_fence_after();
+      const int row = mi * pair::BM + (int)rank * 128 + q * 32 + lane;
+      const int l = z / batch;
+      const int m = mt.m[l];
+      const int minv = mt.minv[l], off = m * ((1 << 30) / m + 1);
+      unsigned char* dst = R + ((long long)z * M + row) * nc + ni * pair::BN;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * pair::BN;
+#pragma unroll 1
+      for (int c = 0; c < pair::BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + c * 32, v);
+        if (row < M && ni * pair::BN + c * 32 < nc) {
+          uint32_t w[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            w[i] = mod_byte(v[4 * i], m, minv, off) | (mod_byte(v[4 * i + 1], m, minv, off) << 8) |
+                   (mod_byte(v[4 * i + 2], m, minv, off) << 16) | (mod_byte(v[4 * i + 3], m, minv, off) << 24);
+          uint4* o = reinterpret_cast<uint4*>(dst + c * 32);
+          o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_rank0 + 8 * acc);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -302,11 +490,13 @@ bool i8gemm_mod_ok(int M, int N, int nc, int K, int nmod) {
          nc > 0;
 }
 
-// R[z][i][j] (uint8, [nz][M][nc]) = (A[z] B[z][j0 + j]^T) mod moduli[z / batch] + 128; see the top of the file.
+// R[z][i][j] (uint8, [nz][M][nc]) = (A[z] B[z][j0 + j]^T) mod moduli[z / batch] + 128; see the top of
+// the file. pair: the CTA-pair kernel (256 x 256 tiles), else the single-CTA one (128 x 256).
 int i8gemm_mod(const signed char* A, const signed char* B, unsigned char* R, int M, int N, int nc, int j0, int K, int nz,
-               int batch, const int* moduli, int nmod, Ctx& cx, cudaStream_t st) {
+               int batch, const int* moduli, int nmod, bool pair, Ctx& cx, cudaStream_t st) {
   CUtensorMap ta, tb;
-  if (!i8::make_map(&ta, A, K, M, nz, i8::BM) || !i8::make_map(&tb, B, K, N, nz, i8::BN)) {
+  const int abox = pair ? 128 : i8::BM, bbox = pair ? 128 : i8::BN;
+  if (!i8::make_map(&ta, A, K, M, nz, abox) || !i8::make_map(&tb, B, K, N, nz, bbox)) {
     set_error("i8gemm_mod: cuTensorMapEncodeTiled failed (M=%d N=%d K=%d nz=%d)", M, N, K, nz);
     return HPS_ERR_CUDA;
   }
@@ -315,11 +505,19 @@ int i8gemm_mod(const signed char* A, const signed char* B, unsigned char* R, int
     mt.m[l] = l < nmod ? moduli[l] : 1;
     mt.minv[l] = (int)((1ULL << 32) / (unsigned long long)mt.m[l]);
   }
-  int st_attr = ensure_smem_attr(reinterpret_cast<const void*>(&i8::k_i8gemm_mod), cx.device, i8::SMEM);
-  if (st_attr != HPS_OK) return st_attr;
-  const long long tiles = (long long)nz * ((M + i8::BM - 1) / i8::BM) * ((nc + i8::BN - 1) / i8::BN);
-  const int grid = (int)std::min<long long>(tiles, cx.sms);
-  i8::k_i8gemm_mod<<<grid, i8::THREADS, i8::SMEM, st>>>(ta, tb, M, nc, j0, K, nz, batch, mt, R);
+  if (pair) {
+    int st_attr = ensure_smem_attr(reinterpret_cast<const void*>(&i8::k_i8gemm_mod_pair), cx.device, i8::pair::SMEM);
+    if (st_attr != HPS_OK) return st_attr;
+    const long long tiles = (long long)nz * ((M + i8::pair::BM - 1) / i8::pair::BM) * ((nc + i8::pair::BN - 1) / i8::pair::BN);
+    const int grid = 2 * (int)std::min<long long>(tiles, cx.sms / 2);
+    i8::k_i8gemm_mod_pair<<<grid, i8::THREADS, i8::pair::SMEM, st>>>(ta, tb, M, nc, j0, K, nz, batch, mt, R);
+  } else {
+    int st_attr = ensure_smem_attr(reinterpret_cast<const void*>(&i8::k_i8gemm_mod), cx.device, i8::SMEM);
+    if (st_attr != HPS_OK) return st_attr;
+    const long long tiles = (long long)nz * ((M + i8::BM - 1) / i8::BM) * ((nc + i8::BN - 1) / i8::BN);
+    const int grid = (int)std::min<long long>(tiles, cx.sms);
+    i8::k_i8gemm_mod<<<grid, i8::THREADS, i8::SMEM, st>>>(ta, tb, M, nc, j0, K, nz, batch, mt, R);
+  }
   HPS_LAUNCH_CHECK();
   return HPS_OK;
 }

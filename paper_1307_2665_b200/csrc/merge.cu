@@ -620,6 +620,7 @@ static int gemm(Ctx& cx, int M, int N, int K, int batch, double alpha, const dou
                 const double* B, long long ldb, long long sB, double beta, double* C, long long ldc, long long sC,
                 cudaStream_t st, int* nonfinite = nullptr) {
   GemmParams p{M, N, K, batch, A, lda, sA, B, ldb, sB, nullptr, 0, C, ldc, sC, alpha, beta, nonfinite};
+  p.emu_ok = true;  // the block inverse's large GEMMs may run emulated on the int8 tensor cores
   return dgemm_launch(p, cx, st);
 }
 

@@ -54,6 +54,19 @@ __global__ void __launch_bounds__(256) k_solve_small(const double* __restrict__ 
   }
 }
 
+// Bg[b][k][0..nrhs) = u[Ie[b][k]][0..nrhs): the boundary values of every box at one depth as a
+// plain (ne x nrhs) operand, so the batched product can run as the FP64 emulation on the int8
+// tensor cores (emu.cu), which takes no row gather. One warp per row.
+__global__ void __launch_bounds__(256) k_solve_gather(const double* __restrict__ u, int ldu, const int* __restrict__ Ie,
+                                                      int ne, int nrhs, long long rows, double* __restrict__ Bg) {
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const double* src = u + (long long)__ldg(Ie + row) * ldu;
+  double* dst = Bg + row * nrhs;
+  for (int j = lane; j < nrhs; j += 32) dst[j] = src[j];
+}
+
 }  // namespace hps
 
 using namespace hps;
@@ -82,5 +95,24 @@ extern "C" int hps_solve_level(hps_ctx_t ctx, int nbatch, int n3, int ne, const 
   // GEMM: C = u rows [start0 + b*n3, +n3), A = S[b] (n3 x ne), B = u[Ie[b]] (ne x nrhs)
   GemmParams p{n3, nrhs, ne, nbatch, S, ne, (long long)n3 * ne, u, ldu, 0, Ie, ne,
                u + ii_start0 * ldu, ldu, (long long)n3 * ldu, 1.0, 0.0, nullptr};
+  // Large FP64-bound depths (many right-hand sides, K = ne >= the emulation threshold): gather B
+  // once and run the product as the FP64 emulation on the int8 tensor cores.
+  const bool emu_on = cx->opt[HPS_OPT_EMU_MODULI] > 0;
+  const double work = (double)n3 * nrhs * ne * nbatch;
+  if (emu_on && nrhs >= 64 && ne >= cx->opt[HPS_OPT_EMU_MIN_K] && work >= (double)cx->opt[HPS_OPT_EMU_MIN_WORK] &&
+      n3 % 4 == 0 && nrhs % 4 == 0 && ne % 16 == 0) {
+    const long long rows = (long long)nbatch * ne;
+    double* Bg = cx->gather_scratch((size_t)rows * nrhs, st);
+    if (Bg) {
+      k_solve_gather<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(u, ldu, Ie, ne, nrhs, rows, Bg);
+      HPS_LAUNCH_CHECK();
+      p.B = Bg;
+      p.ldb = nrhs;
+      p.strideB = (long long)ne * nrhs;
+      p.Bidx = nullptr;
+      p.strideBidx = 0;
+      p.emu_ok = true;
+    }
+  }
   return dgemm_launch(p, *cx, st);
 }

@@ -258,16 +258,17 @@ def test_emulated_dgemm_nonfinite_and_panels(moduli):
 @pytest.mark.parametrize("M,N,K,B,mb", [(200, 544, 272, 3, 8192), (200, 544, 272, 3, 1), (1024, 1024, 1024, 2, 8192),
                                         (384, 4096, 2048, 1, 8192), (130, 96, 1040, 5, 8192)])
 def test_emulated_dgemm_engines_bitwise(M, N, K, B, mb):
-    """Modular emulation: the hand-written tcgen05 int8 kernel (TMA, TMEM accumulators, residues
-    reduced in its epilogue) and cuBLASLt's IMMA GEMM compute the same exact integer residues, so
-    the reconstructed FP64 products are bitwise equal; partial tiles in M, N and K, batches and
-    output column panels (mb: scratch cap in MB) included."""
+    """Modular emulation: the hand-written tcgen05 int8 kernels (TMA, TMEM accumulators, residues
+    reduced in the epilogue; single CTAs = engine 0, CTA pairs = engine 2) and cuBLASLt's IMMA GEMM
+    (engine 1) compute the same exact integer residues, so the reconstructed FP64 products are
+    bitwise equal; partial tiles in M, N and K, batches and output column panels (mb: scratch cap in
+    MB) included."""
     lib = _native.load()
     rng = np.random.default_rng(M * N + K)
     A = rng.standard_normal((B, M, K)) * 10.0 ** rng.uniform(-4, 4, (B, M, 1))
     Bm = rng.standard_normal((B, K, N))
     out = {}
-    for engine in (0, 1):
+    for engine in (0, 1, 2):
         cx = _native.Context(0, emu_min_work=1, emu_min_k=16, emu_slices=0, emu_moduli=14, emu_engine=engine,
                              emu_scratch_mb=mb)
         try:
@@ -283,7 +284,8 @@ def test_emulated_dgemm_engines_bitwise(M, N, K, B, mb):
     exact = np.einsum("bmk,bkn->bmn", A.astype(np.longdouble), Bm.astype(np.longdouble))
     scale = np.abs(A).max(axis=2)[:, :, None] * np.abs(Bm).max(axis=1)[:, None, :] * K
     err = float((np.abs(out[0] - exact) / scale).max())
-    print(f"M={M} N={N} K={K} B={B}: tcgen05 vs cuBLASLt max |diff| {np.abs(out[0] - out[1]).max():.1e}, "
-          f"error {err:.2e}")
+    print(f"M={M} N={N} K={K} B={B}: tcgen05 single / pair vs cuBLASLt max |diff| {np.abs(out[0] - out[1]).max():.1e} "
+          f"/ {np.abs(out[2] - out[1]).max():.1e}, error {err:.2e}")
     assert np.array_equal(out[0], out[1])
+    assert np.array_equal(out[2], out[1])
     assert err <= 2.0 ** -52
