@@ -63,7 +63,10 @@ typedef struct hps_ctx_s* hps_ctx_t;
 #define HPS_OPT_EMU_ENGINE 11       /* int8 products of the modular scheme: this library's tcgen05 kernel (TMA +
                                        TMEM, residues reduced in its epilogue) on single CTAs, 128 x 256 tiles (0)
                                        or CTA pairs, 256 x 256 tiles (2); cuBLASLt IMMA (1) */
-#define HPS_OPT_COUNT 12
+#define HPS_OPT_EMU_TILE_GROUP 12   /* tile rows per group of the tcgen05 kernel's tile order (0: ~32 MB of A) */
+#define HPS_OPT_EMU_SOLVE 13        /* batched solve (b >= 64) through the emulation too (0: DMMA; measured slower
+                                       at b = 256: S is read once, its residues cost about what DMMA saves) */
+#define HPS_OPT_COUNT 14
 int hps_ctx_create(int device, hps_ctx_t* out);
 int hps_ctx_destroy(hps_ctx_t ctx);
 int hps_ctx_set_option(hps_ctx_t ctx, int option, long long value);

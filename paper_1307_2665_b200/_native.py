@@ -42,6 +42,8 @@ HPS_OPT_EMU_MIN_K = 8
 HPS_OPT_EMU_MODULI = 9
 HPS_OPT_EMU_SCRATCH_MB = 10
 HPS_OPT_EMU_ENGINE = 11
+HPS_OPT_EMU_TILE_GROUP = 12
+HPS_OPT_EMU_SOLVE = 13
 
 HPS_MERGE_PIVOTED = 1
 HPS_MERGE_PARENT_PIVOTED = 2

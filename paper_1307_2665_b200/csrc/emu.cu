@@ -490,18 +490,22 @@ __global__ void __launch_bounds__(256) k_crt_col_scale(const double* __restrict_
   }
 }
 
-// symmetric residue of the integer x (|x| <= 2^55, exact in fp64) modulo m, in [-128, 127]
-__device__ __forceinline__ int crt_residue(double x, double m, double inv_m) {
-  const double q = rint(x * inv_m);
-  double r = fma(-m, q, x);  // exact: a small integer
-  if (r > 127.0) r -= m;
-  if (r < -128.0) r += m;
-  return (int)r;
+// symmetric residue of the integer x (|x| <= 2^55, exact in fp64) modulo m, in [-128, 127]; the
+// quotient is rounded and the remainder read out through the 1.5 * 2^52 shift (no conversion unit).
+__device__ __forceinline__ int crt_residue(double x, double m, double inv_m, int mi) {
+  const double kShift = 6755399441055744.0;          // 1.5 * 2^52
+  const double q = (x * inv_m + kShift) - kShift;    // rint(x / m), |x / m| < 2^51
+  const double r = fma(-m, q, x);                    // exact: a small integer
+  int ri = __double2loint(r + kShift);               // r, two's complement in the low word
+  ri = ri > 127 ? ri - mi : ri;
+  return ri < -128 ? ri + mi : ri;
 }
 
 // residues of the scaled rows of A: out[l][b][i][k]; 4 k per thread
-__global__ void k_crt_split_rows(const double* __restrict__ A, long long lda, long long sA, int M, int K, int batch,
-                                 const int* __restrict__ sig, CrtConst c, signed char* __restrict__ out) {
+template <int NM>
+__global__ void __launch_bounds__(256) k_crt_split_rows(const double* __restrict__ A, long long lda, long long sA, int M,
+                                                       int K, int batch, const int* __restrict__ sig, CrtConst c,
+                                                       signed char* __restrict__ out) {
   const int b = blockIdx.z, r = blockIdx.y;
   const int k4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (k4 >= K) return;  // K % 16 == 0
@@ -512,17 +516,21 @@ __global__ void k_crt_split_rows(const double* __restrict__ A, long long lda, lo
   for (int u = 0; u < 4; ++u) x[u] = sg == INT_MIN ? 0.0 : rint(ldexp(Ar[u], sg));  // exact scaling
   const long long plane = (long long)batch * M * K;
   char4* o = reinterpret_cast<char4*>(out + ((long long)b * M + r) * K + k4);
-  for (int l = 0; l < c.n; ++l)
-    o[l * (plane / 4)] = make_char4(crt_residue(x[0], c.m[l], c.inv_m[l]), crt_residue(x[1], c.m[l], c.inv_m[l]),
-                                    crt_residue(x[2], c.m[l], c.inv_m[l]), crt_residue(x[3], c.m[l], c.inv_m[l]));
+#pragma unroll
+  for (int l = 0; l < NM; ++l)
+    o[l * (plane / 4)] = make_char4(crt_residue(x[0], c.m[l], c.inv_m[l], c.mi[l]),
+                                    crt_residue(x[1], c.m[l], c.inv_m[l], c.mi[l]),
+                                    crt_residue(x[2], c.m[l], c.inv_m[l], c.mi[l]),
+                                    crt_residue(x[3], c.m[l], c.inv_m[l], c.mi[l]));
 }
 
 // residues of the scaled columns of B, transposed: out[l][b][j][k]. Tile: 32 k x 64 j through
 // shared memory.
+template <int NM>
 __global__ void __launch_bounds__(256) k_crt_split_cols(const double* __restrict__ B, long long ldb, long long sB, int K,
                                                        int N, int batch, const int* __restrict__ tau, CrtConst c,
                                                        signed char* __restrict__ out) {
-  __shared__ signed char sd[CRT_MAX][64][36];
+  __shared__ signed char sd[NM][64][36];
   const int b = blockIdx.z;
   const int k0 = blockIdx.y * 32, j0 = blockIdx.x * 64;
   const double* Bb = B + (long long)b * sB;
@@ -534,12 +542,13 @@ __global__ void __launch_bounds__(256) k_crt_split_cols(const double* __restrict
       const int tj = tau[(long long)b * N + j];
       x = tj == INT_MIN ? 0.0 : rint(ldexp(Bb[(long long)k * ldb + j], tj));
     }
-    for (int l = 0; l < c.n; ++l) sd[l][jj][kk] = (signed char)crt_residue(x, c.m[l], c.inv_m[l]);
+#pragma unroll
+    for (int l = 0; l < NM; ++l) sd[l][jj][kk] = (signed char)crt_residue(x, c.m[l], c.inv_m[l], c.mi[l]);
   }
   __syncthreads();
   const long long plane = (long long)batch * N * K;
   signed char* ob = out + (long long)b * N * K;
-  for (int idx = threadIdx.x; idx < c.n * 64 * 8; idx += blockDim.x) {  // 4 bytes per store
+  for (int idx = threadIdx.x; idx < NM * 64 * 8; idx += blockDim.x) {  // 4 bytes per store
     const int k4 = (idx % 8) * 4, rest = idx / 8, jj = rest % 64, l = rest / 64;
     const int k = k0 + k4, j = j0 + jj;
     if (k < K && j < N)
@@ -547,6 +556,14 @@ __global__ void __launch_bounds__(256) k_crt_split_cols(const double* __restrict
           *reinterpret_cast<const char4*>(&sd[l][jj][k4]);
   }
 }
+
+#define HPS_CRT_SWITCH(n, CALL)                                                                            \
+  switch (n) {                                                                                             \
+    case 2: CALL(2); break; case 3: CALL(3); break; case 4: CALL(4); break; case 5: CALL(5); break;        \
+    case 6: CALL(6); break; case 7: CALL(7); break; case 8: CALL(8); break; case 9: CALL(9); break;        \
+    case 10: CALL(10); break; case 11: CALL(11); break; case 12: CALL(12); break; case 13: CALL(13); break; \
+    case 14: CALL(14); break; case 15: CALL(15); break; case 16: CALL(16); break;                          \
+  }
 
 // (C_l mod m_l) + 128 in [0, 255] of an int32 product (|v| < 2^30; as mod_byte in i8gemm.cu)
 __device__ __forceinline__ unsigned crt_biased(int v, int m, int minv) {
@@ -759,11 +776,17 @@ static int emu_gemm_crt(const GemmParams& p, Ctx& cx, cudaStream_t st) {
   HPS_LAUNCH_CHECK();
   k_crt_col_scale<<<dim3((p.N + 31) / 32, p.batch), 256, 0, st>>>(p.B, p.ldb, p.strideB, p.K, p.N, c.PB, tau);
   HPS_LAUNCH_CHECK();
-  k_crt_split_rows<<<dim3((p.K / 4 + 255) / 256, p.M, p.batch), 256, 0, st>>>(p.A, p.lda, p.strideA, p.M, p.K, p.batch,
-                                                                               sig, c, Ar);
+#define HPS_SPLIT_ROWS(NM)                                                                                   \
+  k_crt_split_rows<NM><<<dim3((p.K / 4 + 255) / 256, p.M, p.batch), 256, 0, st>>>(p.A, p.lda, p.strideA, p.M, p.K, \
+                                                                                 p.batch, sig, c, Ar)
+  HPS_CRT_SWITCH(n, HPS_SPLIT_ROWS)
+#undef HPS_SPLIT_ROWS
   HPS_LAUNCH_CHECK();
-  k_crt_split_cols<<<dim3((p.N + 63) / 64, (p.K + 31) / 32, p.batch), 256, 0, st>>>(p.B, p.ldb, p.strideB, p.K, p.N,
-                                                                                  p.batch, tau, c, Br);
+#define HPS_SPLIT_COLS(NM)                                                                                        \
+  k_crt_split_cols<NM><<<dim3((p.N + 63) / 64, (p.K + 31) / 32, p.batch), 256, 0, st>>>(p.B, p.ldb, p.strideB, p.K, \
+                                                                                      p.N, p.batch, tau, c, Br)
+  HPS_CRT_SWITCH(n, HPS_SPLIT_COLS)
+#undef HPS_SPLIT_COLS
   HPS_LAUNCH_CHECK();
   const int one = 1, zero = 0;
   for (int j0 = 0; j0 < p.N; j0 += nc) {

@@ -5,17 +5,18 @@
 //                the symmetric residue in [-128, 127], biased),
 //   A: [nz][M][K] int8, B: [nz][N][K] int8 (both K-contiguous), j < nc (an output column panel).
 //
-// Persistent, warp-specialised, one CTA per SM (192 threads):
+// Persistent, warp-specialised, one CTA per SM (320 threads):
 //   warp 0    TMA producer: 128 x 128 B (A) and 256 x 128 B (B) boxes with the 128-byte swizzle
 //             into a 4-stage shared-memory ring (full / empty mbarriers, expect-tx byte counts);
 //   warp 1    allocates all 512 TMEM columns; one lane issues tcgen05.mma.kind::i8 (M = 128,
 //             N = 256, K = 32 per instruction; 4 per stage) into one of two 256-column int32
 //             accumulators, releases each stage with tcgen05.commit, and signals the epilogue;
-//   warps 2-5 epilogue: tcgen05.ld 32x32b (each warp its 32-lane quadrant of TMEM), the exact
+//   warps 2-9 epilogue: tcgen05.ld 32x32b (two warps per 32-lane quadrant of TMEM, each half of the
+//             columns; warp w may only touch quadrant w % 4), the exact
 //             int32 sums reduced mod m (multiply-high quotient, no conversions), 32 bytes per row
 //             chunk stored; the accumulator is released to the MMA warp while the next tile's
 //             MMAs run in the other one.
-// Tiles are ordered in groups of 8 tile rows so that the concurrent wave's A and B panels stay in L2.
+// Tiles are ordered in groups of G tile rows so that the concurrent wave's A panels stay in L2.
 #include <cuda.h>
 
 #include <algorithm>
@@ -30,9 +31,9 @@ namespace i8 {
 constexpr int BM = 128, BN = 256, BK = 128;  // BK: bytes = int8 elements of K per stage
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK, B_BYTES = BN * BK, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quadrant, each half of the tile's columns
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-constexpr int GROUP_M = 8;
 constexpr int MAX_MOD = 16;
 
 struct ModTab {
@@ -109,12 +110,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void tile_coords(long long t, int tm, int tn, int& z, int& mi, int& ni) {
+// Tile t -> (z, tile row, tile column): z outermost, then groups of G tile rows swept column by column,
+// so a wave's A row panels (G x BM x K bytes, sized on the host to ~32 MB) stay in L2 while B streams.
+__device__ __forceinline__ void tile_coords(long long t, int tm, int tn, int G, int& z, int& mi, int& ni) {
   const long long per = (long long)tm * tn;
   z = (int)(t / per);
   const int r = (int)(t - (long long)z * per);
-  const int g = r / (GROUP_M * tn), first = g * GROUP_M, gs = min(GROUP_M, tm - first);
-  const int rr = r - g * GROUP_M * tn;
+  const int g = r / (G * tn), first = g * G, gs = min(G, tm - first);
+  const int rr = r - g * G * tn;
   mi = first + rr % gs;
   ni = rr / gs;
 }
@@ -133,7 +136,7 @@ __device__ __forceinline__ uint32_t mod_byte(uint32_t u, int m, int minv, int of
 
 __global__ void __launch_bounds__(THREADS, 1)
     k_i8gemm_mod(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int nc, int j0,
-                 int K, int nz, int batch, ModTab mt, unsigned char* __restrict__ R) {
+                 int K, int nz, int batch, int G, ModTab mt, unsigned char* __restrict__ R) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 4);
+      mbar_init(tempty0 + 8 * a, EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
         int z, mi, ni;
-        tile_coords(t, tm, tn, z, mi, ni);
+        tile_coords(t, tm, tn, G, z, mi, ni);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty0 + 8 * s, ph ^ 1);
           const uint32_t fb = full0 + 8 * s;
@@ -218,11 +221,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int q = warp & 3;                  // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) / 4;         // which half of the columns
     int it = 0;
     for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       int z, mi, ni;
-      tile_coords(t, tm, tn, z, mi, ni);
+      tile_coords(t, tm, tn, G, z, mi, ni);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(tfull0 + 8 * acc, aph);
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       unsigned char* dst = R + ((long long)z * M + row) * nc + ni * BN;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         uint32_t v[32];
         tmem_ld32(tbase + c * 32, v);
         if (row < M && ni * BN + c * 32 < nc) {
@@ -319,7 +323,7 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     k_i8gemm_mod_pair(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int nc,
-                      int j0, int K, int nz, int batch, ModTab mt, unsigned char* __restrict__ R) {
+                      int j0, int K, int nz, int batch, int G, ModTab mt, unsigned char* __restrict__ R) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + pair::STAGES * pair::STAGE_BYTES);
@@ -340,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 8);  // even CTA: 4 epilogue warps of each CTA
+      mbar_init(tempty0 + 8 * a, 2 * EPI_WARPS);  // even CTA: the epilogue warps of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -361,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       for (long long t = cid; t < tiles; t += ncl) {
         int z, mi, ni;
-        tile_coords(t, tm, tn, z, mi, ni);
+        tile_coords(t, tm, tn, G, z, mi, ni);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty0 + 8 * s, ph ^ 1);
           const uint32_t fb = full0 + 8 * s;
@@ -406,11 +410,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   } else {
     const int q = warp & 3;
+    const int half = (warp - 2) / 4;
     const uint32_t tempty_rank0 = map_to_rank0(tempty0);
     int it = 0;
     for (long long t = cid; t < tiles; t += ncl, ++it) {
       int z, mi, ni;
-      tile_coords(t, tm, tn, z, mi, ni);
+      tile_coords(t, tm, tn, G, z, mi, ni);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(tfull0 + 8 * acc, aph);
@@ -422,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       unsigned char* dst = R + ((long long)z * M + row) * nc + ni * pair::BN;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * pair::BN;
 #pragma unroll 1
-      for (int c = 0; c < pair::BN / 32; ++c) {
+      for (int c = half * (pair::BN / 64); c < (half + 1) * (pair::BN / 64); ++c) {
         uint32_t v[32];
         tmem_ld32(tbase + c * 32, v);
         if (row < M && ni * pair::BN + c * 32 < nc) {
@@ -505,18 +510,24 @@ int i8gemm_mod(const signed char* A, const signed char* B, unsigned char* R, int
     mt.m[l] = l < nmod ? moduli[l] : 1;
     mt.minv[l] = (int)((1ULL << 32) / (unsigned long long)mt.m[l]);
   }
+  // tile-row group: ~32 MB of A row panels (or the option's override)
+  const int bm = pair ? i8::pair::BM : i8::BM;
+  const int tm = (M + bm - 1) / bm;
+  int G = cx.opt[HPS_OPT_EMU_TILE_GROUP] > 0 ? (int)cx.opt[HPS_OPT_EMU_TILE_GROUP]
+                                              : (int)std::max<long long>(1, (32LL << 20) / ((long long)bm * K));
+  G = std::max(1, std::min(G, tm));
   if (pair) {
     int st_attr = ensure_smem_attr(reinterpret_cast<const void*>(&i8::k_i8gemm_mod_pair), cx.device, i8::pair::SMEM);
     if (st_attr != HPS_OK) return st_attr;
     const long long tiles = (long long)nz * ((M + i8::pair::BM - 1) / i8::pair::BM) * ((nc + i8::pair::BN - 1) / i8::pair::BN);
     const int grid = 2 * (int)std::min<long long>(tiles, cx.sms / 2);
-    i8::k_i8gemm_mod_pair<<<grid, i8::THREADS, i8::pair::SMEM, st>>>(ta, tb, M, nc, j0, K, nz, batch, mt, R);
+    i8::k_i8gemm_mod_pair<<<grid, i8::THREADS, i8::pair::SMEM, st>>>(ta, tb, M, nc, j0, K, nz, batch, G, mt, R);
   } else {
     int st_attr = ensure_smem_attr(reinterpret_cast<const void*>(&i8::k_i8gemm_mod), cx.device, i8::SMEM);
     if (st_attr != HPS_OK) return st_attr;
     const long long tiles = (long long)nz * ((M + i8::BM - 1) / i8::BM) * ((nc + i8::BN - 1) / i8::BN);
     const int grid = (int)std::min<long long>(tiles, cx.sms);
-    i8::k_i8gemm_mod<<<grid, i8::THREADS, i8::SMEM, st>>>(ta, tb, M, nc, j0, K, nz, batch, mt, R);
+    i8::k_i8gemm_mod<<<grid, i8::THREADS, i8::SMEM, st>>>(ta, tb, M, nc, j0, K, nz, batch, G, mt, R);
   }
   HPS_LAUNCH_CHECK();
   return HPS_OK;

@@ -97,7 +97,7 @@ extern "C" int hps_solve_level(hps_ctx_t ctx, int nbatch, int n3, int ne, const 
                u + ii_start0 * ldu, ldu, (long long)n3 * ldu, 1.0, 0.0, nullptr};
   // Large FP64-bound depths (many right-hand sides, K = ne >= the emulation threshold): gather B
   // once and run the product as the FP64 emulation on the int8 tensor cores.
-  const bool emu_on = cx->opt[HPS_OPT_EMU_MODULI] > 0;
+  const bool emu_on = cx->opt[HPS_OPT_EMU_SOLVE] && cx->opt[HPS_OPT_EMU_MODULI] > 0;
   const double work = (double)n3 * nrhs * ne * nbatch;
   if (emu_on && nrhs >= 64 && ne >= cx->opt[HPS_OPT_EMU_MIN_K] && work >= (double)cx->opt[HPS_OPT_EMU_MIN_WORK] &&
       n3 % 4 == 0 && nrhs % 4 == 0 && ne % 16 == 0) {

@@ -1,6 +1,6 @@
 """Per-kernel device times of one emulated (or DMMA) merge-shaped GEMM through hps_dgemm_batched,
 from torch.profiler (CUPTI): which of scales / residues / int8 products / reconstruction dominate
-(dev tool). Usage: python tools/emu_profile.py M N K batch [moduli slices scratch_mb engine]"""
+(dev tool). Usage: python tools/emu_profile.py M N K batch [moduli slices scratch_mb engine tile_group]"""
 import sys
 from collections import defaultdict
 
@@ -16,7 +16,9 @@ moduli = int(sys.argv[5]) if len(sys.argv) > 5 else 14
 slices = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 scratch = int(sys.argv[7]) if len(sys.argv) > 7 else 8192
 engine = int(sys.argv[8]) if len(sys.argv) > 8 else 0
-cx = _native.Context(0, emu_moduli=moduli, emu_slices=slices, emu_scratch_mb=scratch, emu_engine=engine)
+group = int(sys.argv[9]) if len(sys.argv) > 9 else 0
+cx = _native.Context(0, emu_moduli=moduli, emu_slices=slices, emu_scratch_mb=scratch, emu_engine=engine,
+                     emu_tile_group=group)
 A = torch.randn(B, M, K, dtype=torch.float64, device="cuda")
 Bm = torch.randn(B, K, N, dtype=torch.float64, device="cuda")
 C = torch.empty(B, M, N, dtype=torch.float64, device="cuda")
@@ -38,7 +40,7 @@ e1.record()
 e1.synchronize()
 ms = e0.elapsed_time(e1) / 3
 fl = 2.0 * M * N * K * B
-print(f"M={M} N={N} K={K} B={B} moduli={moduli} slices={slices} engine={engine}: {ms:.3f} ms, {fl / ms / 1e9:.1f} TF/s FP64-equivalent")
+print(f"M={M} N={N} K={K} B={B} moduli={moduli} slices={slices} engine={engine} group={group}: {ms:.3f} ms, {fl / ms / 1e9:.1f} TF/s FP64-equivalent")
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
     run()
     torch.cuda.synchronize()
