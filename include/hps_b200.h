@@ -185,6 +185,16 @@ int hps_dgemm_batched(hps_ctx_t ctx, int M, int N, int K, int batch, double alph
                       const int* Bidx, long long strideBidx, double beta, double* C, long long ldc,
                       long long strideC, void* stream);
 
+/* The int8 residue products of the modular FP64 emulation (the core of hps_dgemm_batched's emulated
+ * path, merge.py:108/118), exposed for tests and benchmarks: for z < nz and the output column panel
+ * [j0, j0 + nc),
+ *   R[z][i][j] = ((sum_k A[z][i][k] B[z][j0 + j][k]) mod moduli[z / batch]) + 128   (uint8, [nz][M][nc])
+ * with A int8 [nz][M][K], B int8 [nz][N][K] (K contiguous), 2 <= moduli[l] <= 256, K % 16 == 0,
+ * N % 16 == 0, nc % 32 == 0, K < 65536. engine: 0 = tcgen05 single-CTA kernel, 2 = CTA-pair
+ * kernel. Device pointers; stream is a cudaStream_t. */
+int hps_i8gemm_mod(hps_ctx_t ctx, const signed char* A, const signed char* B, unsigned char* R, int M, int N, int nc,
+                   int j0, int K, int nz, int batch, const int* moduli, int nmod, int engine, void* stream);
+
 /* Leaf grouping (solver.py:208-222). fields: HOST array of nfields (1..6) DEVICE pointers, each to
  * n_leaf x row_len fp64 samples. hps_leaf_hash writes a 64-bit hash of every leaf's rows;
  * hps_leaf_verify sets *mismatch (device int) to 1 if some leaf's rows differ bitwise from those of

@@ -28,7 +28,8 @@ EXPORTS = ("hps_ctx_create", "hps_ctx_destroy", "hps_ctx_set_option", "hps_ctx_g
            "hps_dgemm_batched", "hps_inverse_workspace_bytes", "hps_inverse_batched", "hps_leaf_hash",
            "hps_leaf_verify", "hps_leaf_fields", "hps_eval_points", "hps_gauge_sides", "hps_gauge_gather",
            "hps_merge_level_ahead", "hps_tree_sizes", "hps_tree_layout", "hps_lu_workspace_bytes",
-           "hps_lu_solve_batched", "hps_merge_interface", "hps_interface_solve", "hps_merge_assemble")
+           "hps_lu_solve_batched", "hps_merge_interface", "hps_interface_solve", "hps_merge_assemble",
+           "hps_i8gemm_mod")
 
 HPS_OPT_SPLITK = 0
 HPS_OPT_GEMM_GROUP_M = 1
@@ -112,6 +113,9 @@ def load():
     lib.hps_dgemm_batched.argtypes = [c_dp, c_int, c_int, c_int, c_int, c_d, c_dp, c_ll, c_ll, c_dp, c_ll, c_ll, c_dp,
                                       c_ll, c_d, c_dp, c_ll, c_ll, c_dp]
     lib.hps_dgemm_batched.restype = c_int
+    lib.hps_i8gemm_mod.argtypes = [c_dp, c_dp, c_dp, c_dp, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                   ctypes.POINTER(c_int), c_int, c_int, c_dp]
+    lib.hps_i8gemm_mod.restype = c_int
     lib.hps_inverse_workspace_bytes.argtypes = [c_int, c_int]
     lib.hps_inverse_workspace_bytes.restype = c_sz
     lib.hps_inverse_batched.argtypes = [c_dp, c_int, c_int, c_dp, c_ll, c_ll, c_dp, c_sz, c_dp, c_dp]

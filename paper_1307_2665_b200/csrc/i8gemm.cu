@@ -534,3 +534,22 @@ int i8gemm_mod(const signed char* A, const signed char* B, unsigned char* R, int
 }
 
 }  // namespace hps
+
+extern "C" int hps_i8gemm_mod(hps_ctx_t ctx, const signed char* A, const signed char* B, unsigned char* R, int M, int N,
+                              int nc, int j0, int K, int nz, int batch, const int* moduli, int nmod, int engine,
+                              void* stream) {
+  HPS_CTX(cx, ctx);
+  if (!hps::i8gemm_mod_ok(M, N, nc, K, nmod) || nz <= 0 || batch <= 0 || nz % batch || nz / batch > nmod ||
+      j0 < 0 || j0 + nc > N || K >= (1 << 16) || (engine != 0 && engine != 2)) {
+    hps::set_error("hps_i8gemm_mod: unsupported arguments (M=%d N=%d nc=%d j0=%d K=%d nz=%d batch=%d engine=%d)", M, N,
+                   nc, j0, K, nz, batch, engine);
+    return HPS_ERR_ARG;
+  }
+  for (int l = 0; l < nmod; ++l)
+    if (moduli[l] < 2 || moduli[l] > 256) {
+      hps::set_error("hps_i8gemm_mod: modulus %d out of range", moduli[l]);
+      return HPS_ERR_ARG;
+    }
+  return hps::i8gemm_mod(A, B, R, M, N, nc, j0, K, nz, batch, moduli, nmod, engine == 2, *cx,
+                         static_cast<cudaStream_t>(stream));
+}

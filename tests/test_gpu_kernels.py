@@ -289,3 +289,43 @@ def test_emulated_dgemm_engines_bitwise(M, N, K, B, mb):
     assert np.array_equal(out[0], out[1])
     assert np.array_equal(out[2], out[1])
     assert err <= 2.0 ** -52
+
+
+@pytest.mark.parametrize("engine", [0, 2])
+@pytest.mark.parametrize("M,N,nc,j0,K,batch,nmod", [(300, 640, 320, 256, 1040, 2, 3), (128, 256, 256, 0, 128, 1, 14),
+                                                   (520, 1024, 512, 512, 4096, 1, 2), (64, 96, 64, 32, 16, 3, 4)])
+def test_i8gemm_mod_exact(engine, M, N, nc, j0, K, batch, nmod):
+    """The tcgen05 int8 kernel through the C ABI against exact int64 products: every residue
+    ((A B^T) mod m) + 128 bitwise, for partial tiles in M / N / K, an output column panel at j0,
+    several moduli x batches, both the single-CTA and the CTA-pair kernel."""
+    import ctypes
+
+    lib = _native.load()
+    rng = np.random.default_rng(M + N + K + nmod)
+    moduli = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199][:nmod]
+    nz = nmod * batch
+    A = rng.integers(-128, 128, (nz, M, K), dtype=np.int8)
+    B = rng.integers(-128, 128, (nz, N, K), dtype=np.int8)
+    tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    tR = torch.zeros((nz, M, nc), dtype=torch.uint8, device="cuda")
+    mods = (ctypes.c_int * nmod)(*moduli)
+    _native.check(lib.hps_i8gemm_mod(_native.context(), _native.ptr(tA), _native.ptr(tB), _native.ptr(tR), M, N, nc, j0,
+                                     K, nz, batch, mods, nmod, engine, _native.stream_ptr()), "i8gemm")
+    R = tR.cpu().numpy()
+    for z in range(nz):
+        m = moduli[z // batch]
+        C = A[z].astype(np.int64) @ B[z, j0:j0 + nc].astype(np.int64).T
+        r = np.mod(C, m)
+        r = np.where(r > 127, r - m, r) + 128
+        assert np.array_equal(R[z], r.astype(np.uint8)), (z, m)
+
+
+def test_i8gemm_mod_rejects_bad_arguments():
+    import ctypes
+
+    lib = _native.load()
+    mods = (ctypes.c_int * 2)(256, 255)
+    t = torch.zeros(1 << 16, dtype=torch.int8, device="cuda")
+    r = lib.hps_i8gemm_mod(_native.context(), _native.ptr(t), _native.ptr(t), _native.ptr(t), 16, 64, 48, 0, 32, 2, 1,
+                           mods, 2, 0, _native.stream_ptr())  # nc % 32 != 0
+    assert r == _native.HPS_ERR_ARG and "unsupported" in _native.last_error()
