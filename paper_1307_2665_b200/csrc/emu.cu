@@ -416,15 +416,27 @@ static bool crt_constants(int n, CrtConst& c) {
 // sig[b][i] (tau[b][j]): the power of two that brings row i of A (column j of B) to 2-norm < 2^P;
 // INT_MIN marks a non-finite row / column (its outputs become NaN, as a DGEMM's would be non-finite).
 // The squares are summed after an exact power-of-two prescale by the maximum (no overflow).
-__device__ __forceinline__ int crt_prescale(double mx, int& em) {  // 0: zero row, -1: non-finite, 1: ok
-  if (!isfinite(mx)) return -1;
-  if (mx == 0.0) return 0;
-  frexp(mx, &em);  // mx < 2^em
-  return 1;
+// x 2^e, exact for |e| <= 1022 (one multiply by a constructed power of two), else ldexp
+__device__ __forceinline__ double crt_ldexp(double x, int e) {
+  if (e >= -1022 && e <= 1023) return x * __longlong_as_double((long long)(e + 1023) << 52);
+  return ldexp(x, e);
 }
-__device__ __forceinline__ int crt_exponent(double ss, int em, int P) {
+// The exponent from the maximum mx and the sum of squares ss of a row / column, accumulated unscaled
+// in one pass; valid when mx is in [2^-450, 2^450] (no square overflows, every square that matters
+// for the norm stays normal). Returns INT_MIN for a non-finite row, 0 for a zero row, INT_MAX when
+// the caller must rescale (mx outside that range).
+__device__ __forceinline__ int crt_exponent_1pass(double mx, double ss, int P) {
+  if (!isfinite(mx) || !isfinite(ss)) return isfinite(mx) ? INT_MAX : INT_MIN;
+  if (mx == 0.0) return 0;
+  if (mx < 0x1p-450 || mx > 0x1p450) return INT_MAX;
   int ex;
-  frexp(sqrt(ss) * (1.0 + 0x1p-30), &ex);  // ||row|| 2^-em < 2^ex (an upper bound despite rounding)
+  frexp(sqrt(ss) * (1.0 + 0x1p-30), &ex);  // ||row|| < 2^ex (an upper bound despite rounding)
+  return P - ex;
+}
+// Rescaled second pass (rare): squares of x 2^-em, mx < 2^em
+__device__ __forceinline__ int crt_exponent_scaled(double ss_scaled, int em, int P) {
+  int ex;
+  frexp(sqrt(ss_scaled) * (1.0 + 0x1p-30), &ex);
   return P - ex - em;
 }
 
@@ -434,59 +446,86 @@ __global__ void k_crt_row_scale(const double* __restrict__ A, long long lda, lon
   const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= M) return;
   const double* Ar = A + (long long)b * sA + (long long)r * lda;
-  double mx = 0.0;
-  for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(Ar[k]));
-  mx = warp_max(mx);
-  int em = 0;
-  const int kind = crt_prescale(mx, em);
-  if (kind <= 0) {
-    if (lane == 0) sig[(long long)b * M + r] = kind < 0 ? INT_MIN : 0;
-    return;
+  double mx[4] = {0.0, 0.0, 0.0, 0.0}, ss[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k = lane; k < K; k += 128) {  // K % 16 == 0: four independent loads per lane
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double v = k + 32 * u < K ? __ldg(Ar + k + 32 * u) : 0.0;
+      mx[u] = fmax(mx[u], fabs(v));
+      ss[u] = fma(v, v, ss[u]);
+    }
   }
-  double ss = 0.0;
-  for (int k = lane; k < K; k += 32) {
-    const double v = ldexp(Ar[k], -em);
-    ss = fma(v, v, ss);
+  const double m = warp_max(fmax(fmax(mx[0], mx[1]), fmax(mx[2], mx[3])));
+  const double q = warp_sum((ss[0] + ss[1]) + (ss[2] + ss[3]));
+  int e = crt_exponent_1pass(m, q, P);
+  if (e == INT_MAX) {  // rescale by the maximum and sum again
+    int em;
+    frexp(m, &em);
+    double s2 = 0.0;
+    for (int k = lane; k < K; k += 32) {
+      const double v = ldexp(Ar[k], -em);
+      s2 = fma(v, v, s2);
+    }
+    e = crt_exponent_scaled(warp_sum(s2), em, P);
   }
-  ss = warp_sum(ss);
-  if (lane == 0) sig[(long long)b * M + r] = crt_exponent(ss, em, P);
+  if (lane == 0) sig[(long long)b * M + r] = e;
 }
 
+// 32 columns x 8 row slices per CTA (coalesced row reads), 4 rows in flight per thread
 __global__ void __launch_bounds__(256) k_crt_col_scale(const double* __restrict__ B, long long ldb, long long sB, int K,
                                                       int N, int P, int* __restrict__ tau) {
-  __shared__ double red[8][33];
-  __shared__ int ems[32];
+  __shared__ double red[2][8][33];
+  __shared__ int ex[32];
   const int b = blockIdx.y;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + tx;
   const double* Bb = B + (long long)b * sB + j;
-  double mx = 0.0;
+  double mx[4] = {0.0, 0.0, 0.0, 0.0}, ss[4] = {0.0, 0.0, 0.0, 0.0};
   if (j < N)
-    for (int k = ty; k < K; k += 8) mx = fmax(mx, fabs(Bb[(long long)k * ldb]));
-  red[ty][tx] = mx;
+    for (int k = ty; k < K; k += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double v = k + 8 * u < K ? __ldg(Bb + (long long)(k + 8 * u) * ldb) : 0.0;
+        mx[u] = fmax(mx[u], fabs(v));
+        ss[u] = fma(v, v, ss[u]);
+      }
+    }
+  red[0][ty][tx] = fmax(fmax(mx[0], mx[1]), fmax(mx[2], mx[3]));
+  red[1][ty][tx] = (ss[0] + ss[1]) + (ss[2] + ss[3]);
   __syncthreads();
   if (ty == 0) {
+    double m = red[0][0][tx], q = red[1][0][tx];
 #pragma unroll
-    for (int r = 1; r < 8; ++r) mx = fmax(mx, red[r][tx]);
-    int em = 0;
-    const int kind = crt_prescale(mx, em);
-    ems[tx] = kind > 0 ? em : (kind < 0 ? INT_MIN : 0x40000000);
+    for (int r = 1; r < 8; ++r) {
+      m = fmax(m, red[0][r][tx]);
+      q += red[1][r][tx];
+    }
+    ex[tx] = crt_exponent_1pass(m, q, P);
+    red[0][0][tx] = m;
   }
   __syncthreads();
-  const int em = ems[tx];
-  double ss = 0.0;
-  if (j < N && em != INT_MIN && em != 0x40000000)
+  if (ex[tx] == INT_MAX) {  // rare: rescale this column by its maximum and sum again
+    int em;
+    frexp(red[0][0][tx], &em);
+    double s2 = 0.0;
     for (int k = ty; k < K; k += 8) {
       const double v = ldexp(Bb[(long long)k * ldb], -em);
-      ss = fma(v, v, ss);
+      s2 = fma(v, v, s2);
     }
-  __syncthreads();
-  red[ty][tx] = ss;
+    red[1][ty][tx] = s2;
+  }
   __syncthreads();
   if (ty == 0 && j < N) {
+    int e = ex[tx];
+    if (e == INT_MAX) {
+      double q = 0.0;
 #pragma unroll
-    for (int r = 1; r < 8; ++r) ss += red[r][tx];
-    tau[(long long)b * N + j] = em == INT_MIN ? INT_MIN : em == 0x40000000 ? 0 : crt_exponent(ss, em, P);
+      for (int r = 0; r < 8; ++r) q += red[1][r][tx];
+      int em;
+      frexp(red[0][0][tx], &em);
+      e = crt_exponent_scaled(q, em, P);
+    }
+    tau[(long long)b * N + j] = e;
   }
 }
 
@@ -513,7 +552,7 @@ __global__ void __launch_bounds__(256) k_crt_split_rows(const double* __restrict
   const double* Ar = A + (long long)b * sA + (long long)r * lda + k4;
   double x[4];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) x[u] = sg == INT_MIN ? 0.0 : rint(ldexp(Ar[u], sg));  // exact scaling
+  for (int u = 0; u < 4; ++u) x[u] = sg == INT_MIN ? 0.0 : rint(crt_ldexp(Ar[u], sg));  // exact scaling
   const long long plane = (long long)batch * M * K;
   char4* o = reinterpret_cast<char4*>(out + ((long long)b * M + r) * K + k4);
 #pragma unroll
@@ -534,16 +573,22 @@ __global__ void __launch_bounds__(256) k_crt_split_cols(const double* __restrict
   const int b = blockIdx.z;
   const int k0 = blockIdx.y * 32, j0 = blockIdx.x * 64;
   const double* Bb = B + (long long)b * sB;
-  for (int idx = threadIdx.x; idx < 32 * 64; idx += blockDim.x) {
-    const int kk = idx / 64, jj = idx % 64;
-    const int k = k0 + kk, j = j0 + jj;
-    double x = 0.0;
-    if (k < K && j < N) {
-      const int tj = tau[(long long)b * N + j];
-      x = tj == INT_MIN ? 0.0 : rint(ldexp(Bb[(long long)k * ldb + j], tj));
-    }
+  // 8 elements per thread: all loads first, then the residues of the 8 interleaved
+  const int jj = threadIdx.x % 64, kq = threadIdx.x / 64;  // k = k0 + kq + 4 i
+  const int j = j0 + jj;
+  const int tj = j < N ? tau[(long long)b * N + j] : INT_MIN;
+  double x[8];
 #pragma unroll
-    for (int l = 0; l < NM; ++l) sd[l][jj][kk] = (signed char)crt_residue(x, c.m[l], c.inv_m[l], c.mi[l]);
+  for (int i = 0; i < 8; ++i) {
+    const int k = k0 + kq + 4 * i;
+    x[i] = (k < K && j < N && tj != INT_MIN) ? __ldg(Bb + (long long)k * ldb + j) : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = rint(crt_ldexp(x[i], tj == INT_MIN ? 0 : tj));
+#pragma unroll
+  for (int l = 0; l < NM; ++l) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sd[l][jj][kq + 4 * i] = (signed char)crt_residue(x[i], c.m[l], c.inv_m[l], c.mi[l]);
   }
   __syncthreads();
   const long long plane = (long long)batch * N * K;

@@ -329,3 +329,33 @@ def test_i8gemm_mod_rejects_bad_arguments():
     r = lib.hps_i8gemm_mod(_native.context(), _native.ptr(t), _native.ptr(t), _native.ptr(t), 16, 64, 48, 0, 32, 2, 1,
                            mods, 2, 0, _native.stream_ptr())  # nc % 32 != 0
     assert r == _native.HPS_ERR_ARG and "unsupported" in _native.last_error()
+
+
+def test_emulated_dgemm_extreme_scales():
+    """Modular emulation: rows / columns near the fp64 range edges (1e-300, 1e+300 and subnormal
+    entries) take the rescaled norm path and still give DGEMM-level relative errors."""
+    lib = _native.load()
+    rng = np.random.default_rng(7)
+    M, N, K = 64, 128, 256
+    A = rng.standard_normal((1, M, K))
+    Bm = rng.standard_normal((1, K, N))
+    A[0, 0] *= 1e-300
+    A[0, 1] *= 1e+290
+    A[0, 2, :8] = 5e-324  # subnormal entries
+    Bm[0, :, 3] *= 1e-200
+    Bm[0, :, 4] *= 1e+200
+    exact = np.einsum("bmk,bkn->bmn", A.astype(np.longdouble), Bm.astype(np.longdouble))
+    cx = _native.Context(0, emu_min_work=1, emu_min_k=16, emu_slices=0, emu_moduli=14)
+    try:
+        tA, tB = cuda(A), cuda(Bm)
+        tC = torch.zeros((1, M, N), dtype=torch.float64, device="cuda")
+        _native.check(lib.hps_dgemm_batched(cx, M, N, K, 1, 1.0, _native.ptr(tA), K, M * K, _native.ptr(tB), N, K * N,
+                                            None, 0, 0.0, _native.ptr(tC), N, M * N, _native.stream_ptr()), "gemm")
+        C = tC.cpu().numpy().astype(np.longdouble)
+    finally:
+        cx.close()
+    scale = np.abs(A).max(axis=2)[:, :, None].astype(np.longdouble) * np.abs(Bm).max(axis=1)[:, None, :] * K
+    ok = (scale > 1e-290) & (scale < 1e300)  # results representable in fp64 without underflow / overflow
+    err = np.abs(C - exact)[ok] / scale[ok]
+    assert np.isfinite(C[0, 1, :3]).all() and np.isfinite(C[0, 0]).all()
+    assert float(err.max()) <= 2.0 ** -50, float(err.max())
