@@ -73,6 +73,19 @@ static int launch_cfg64(const GemmParams& p, Ctx& cx, cudaStream_t stream) {
     split = (int)std::min<long long>((slots + tiles - 1) / tiles, p.K / (4 * BK));
     split = std::max(1, std::min(split, 16));
     while (split > 1 && (long long)split * p.batch > 65535) --split;
+  } else if (cx.opt[HPS_OPT_SPLITK] && p.Bidx && tiles < 4 * slots && p.K >= 16 * BK) {
+    // the batched solve's top depths (one to a few boxes, long K): a tile grid just over a wave
+    // (e.g. 512 tiles on 444 slots) leaves most SMs idle in its last wave; pick the split with the
+    // best wave fill, 3% per extra split for the partial sums' pass
+    double best = 0.0;
+    for (int s = 1; s <= 8 && (long long)s * 4 * BK <= p.K && (long long)s * p.batch <= 65535; ++s) {
+      const long long t = tiles * s, waves = (t + slots - 1) / slots;
+      const double eff = (double)t / (double)(waves * slots) - 0.03 * (s - 1);
+      if (eff > best + 1e-9) {
+        best = eff;
+        split = s;
+      }
+    }
   }
   GemmParams q = p;
   if (split > 1) {
@@ -135,6 +148,10 @@ int dgemm_launch(const GemmParams& p, Ctx& cx, cudaStream_t stream) {
   if (!p.Bidx && p.M <= 16 && p.N >= 64) return launch_cfg<16, 64, 16, 1, 2, 3>(p, cx, stream);
   if (!p.Bidx && p.M <= 32 && p.N >= 64) return launch_cfg<32, 64, 16, 1, 2, 3>(p, cx, stream);
   if (!p.Bidx && p.M == 96 && p.N == 96) return launch_cfg<48, 48, 16, 2, 2, 2>(p, cx, stream);
+  // row-gather GEMMs (the batched solve) with few rows (the bottom depths, n3 <= 32): 16 / 32-row
+  // tiles, as tall as the problem, instead of 64-row tiles that are mostly padding
+  if (p.Bidx && p.M <= 16) return launch_cfg<16, 64, 16, 1, 2, 3>(p, cx, stream);
+  if (p.Bidx && p.M <= 32) return launch_cfg<32, 64, 16, 1, 2, 3>(p, cx, stream);
   const bool narrow_gather = p.Bidx && p.N <= 64;
   if (!narrow_gather && p.K <= 32) return launch_cfg64<16, 2, 4>(p, cx, stream);
   if (!narrow_gather) return launch_cfg64<16, 3, 3>(p, cx, stream);

@@ -95,16 +95,14 @@ extern "C" int hps_solve_level(hps_ctx_t ctx, int nbatch, int n3, int ne, const 
   // GEMM: C = u rows [start0 + b*n3, +n3), A = S[b] (n3 x ne), B = u[Ie[b]] (ne x nrhs)
   GemmParams p{n3, nrhs, ne, nbatch, S, ne, (long long)n3 * ne, u, ldu, 0, Ie, ne,
                u + ii_start0 * ldu, ldu, (long long)n3 * ldu, 1.0, 0.0, nullptr};
-  // Gather B once into a plain (ne x nrhs) operand per box where that pays: (a) the bottom depths
-  // (n3 <= 32, many right-hand sides), which then run on the 16 / 32-row tiles instead of 64-row
-  // tiles that are mostly padding; (b) with HPS_OPT_EMU_SOLVE, large FP64-bound depths (K = ne >=
-  // the emulation threshold) through the FP64 emulation on the int8 tensor cores.
+  // With HPS_OPT_EMU_SOLVE, large FP64-bound depths (K = ne >= the emulation threshold) gather B
+  // once into a plain (ne x nrhs) operand per box and run through the FP64 emulation on the int8
+  // tensor cores (which takes no row gather).
   const bool emu_on = cx->opt[HPS_OPT_EMU_SOLVE] && cx->opt[HPS_OPT_EMU_MODULI] > 0;
   const double work = (double)n3 * nrhs * ne * nbatch;
   const bool emu_here = emu_on && nrhs >= 64 && ne >= cx->opt[HPS_OPT_EMU_MIN_K] &&
                         work >= (double)cx->opt[HPS_OPT_EMU_MIN_WORK] && n3 % 4 == 0 && nrhs % 4 == 0 && ne % 16 == 0;
-  const bool small_rows = n3 <= 32 && nrhs >= 64 && ne % 16 == 0 && nrhs % 2 == 0;
-  if (emu_here || small_rows) {
+  if (emu_here) {
     const long long rows = (long long)nbatch * ne;
     double* Bg = cx->gather_scratch((size_t)rows * nrhs, st);
     if (Bg) {
@@ -115,7 +113,7 @@ extern "C" int hps_solve_level(hps_ctx_t ctx, int nbatch, int n3, int ne, const 
       p.strideB = (long long)ne * nrhs;
       p.Bidx = nullptr;
       p.strideBidx = 0;
-      p.emu_ok = emu_here;
+      p.emu_ok = true;
     }
   }
   return dgemm_launch(p, *cx, st);

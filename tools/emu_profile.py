@@ -18,7 +18,7 @@ scratch = int(sys.argv[7]) if len(sys.argv) > 7 else 8192
 engine = int(sys.argv[8]) if len(sys.argv) > 8 else 0
 group = int(sys.argv[9]) if len(sys.argv) > 9 else 0
 cx = _native.Context(0, emu_moduli=moduli, emu_slices=slices, emu_scratch_mb=scratch, emu_engine=engine,
-                     emu_tile_group=group)
+                     emu_tile_group=group, emu_min_k=16)
 A = torch.randn(B, M, K, dtype=torch.float64, device="cuda")
 Bm = torch.randn(B, K, N, dtype=torch.float64, device="cuda")
 C = torch.empty(B, M, N, dtype=torch.float64, device="cuda")
