@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--emu-engine", type=int, default=None,
                     help="int8 products of the modular scheme: 0 = the library's tcgen05 kernel (default), 2 = its "
                          "CTA-pair variant, 1 = cuBLASLt")
-    ap.add_argument("--emu-min-k", type=int, default=None, help="emulate merge GEMMs with K >= this (default 1024)")
+    ap.add_argument("--emu-min-k", type=int, default=None, help="emulate merge GEMMs with K >= this (default 512)")
     ap.add_argument("--emu-solve", type=int, default=None, help="batched solve through the emulation too (default 0)")
     ap.add_argument("--validate-reference-model", action="store_true",
                     help="time whole oracle-port steps at configs 2 (L=6) and 3 (L=7) against the sampled model")

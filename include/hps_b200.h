@@ -55,7 +55,8 @@ typedef struct hps_ctx_s* hps_ctx_t;
                                        per operand, s (s + 1) / 2 int8 products (0 = off; used when
                                        HPS_OPT_EMU_MODULI is 0); the merges' S / T GEMMs and hps_dgemm_batched */
 #define HPS_OPT_EMU_MIN_WORK 7      /* emulate GEMMs with M N K batch >= this (2^32) */
-#define HPS_OPT_EMU_MIN_K 8         /* ... and K >= this (1024): below it the fp64 accumulation traffic wins */
+#define HPS_OPT_EMU_MIN_K 8         /* ... and K >= this (512): below it the residue and reconstruction passes
+                                       cost more than DMMA saves */
 #define HPS_OPT_EMU_MODULI 9        /* FP64 GEMM emulation, modular scheme: one int8 product per modulus
                                        (14, FP64-equivalent; 6..16; 0 = off) with Chinese-remainder
                                        reconstruction; takes precedence over HPS_OPT_EMU_SLICES */

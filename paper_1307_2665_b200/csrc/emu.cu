@@ -658,6 +658,51 @@ struct CrtIn<unsigned char> {  // the tcgen05 kernel's biased residues, 4 per wo
 // 4 columns per thread; all NM loads of a row are issued before the arithmetic (4 FP64 operations
 // per residue, no conversions).
 template <int NM, typename TIn>
+__device__ __forceinline__ void crt_row(const typename CrtIn<TIn>::V (&in)[NM], int sr, const int (&tj)[4], int b, int r,
+                                        int col0, const GemmParams& p, const CrtConst& c, bool& bad) {
+  double shi[4] = {0.0, 0.0, 0.0, 0.0}, slo[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int l = 0; l < NM; ++l) {
+    unsigned bb[4];
+    CrtIn<TIn>::biased(in[l], c, l, bb);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double rr = crt_unbias(bb[u]);
+      shi[u] = fma(rr, c.W[l], shi[u]);  // exact
+      slo[u] = fma(rr, c.wlo[l], slo[u]);
+    }
+  }
+  double v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const double q = rint(fma(shi[u], c.twoE_over_M, slo[u] * c.inv_M));
+    const double cp = fma(fma(-q, c.Mh, shi[u]), c.twoE, fma(-q, c.Mlo, slo[u]));
+    double w = (sr == INT_MIN || tj[u] == INT_MIN) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                    : crt_scale(cp, -(sr + tj[u]));
+    w *= p.alpha;
+    if (p.blk_j1a) w += blk_value(p, b, r, col0 + u);
+    v[u] = w;
+  }
+  double* dst = p.C + (long long)b * p.strideC + (long long)r * p.ldc + col0;
+  if (p.beta != 0.0) {  // C = alpha A B + beta C
+    const double2 o0 = *reinterpret_cast<const double2*>(dst), o1 = *reinterpret_cast<const double2*>(dst + 2);
+    v[0] = fma(p.beta, o0.x, v[0]);
+    v[1] = fma(p.beta, o0.y, v[1]);
+    v[2] = fma(p.beta, o1.x, v[2]);
+    v[3] = fma(p.beta, o1.y, v[3]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) bad |= !isfinite(v[u]);
+  *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
+  *reinterpret_cast<double2*>(dst + 2) = make_double2(v[2], v[3]);
+}
+
+// Reconstruction of the output columns [j0, j0 + nc) from the NM products of that panel
+// (Cl[l][b][i][0..nc): int32 products, or biased int8 residues), with the row / column scales,
+// alpha, the merge's block-diagonal addend and the non-finite flag. Rows on blockIdx.y (grid-stride,
+// two rows per step), 4 columns per thread; all 2 NM loads of a step are issued before the arithmetic
+// (4 FP64 operations per residue, no conversions).
+template <int NM, typename TIn>
 __global__ void __launch_bounds__(256) k_crt_accum(const TIn* __restrict__ Cl, int M, int nc, int j0, GemmParams p,
                                                   CrtConst c, const int* __restrict__ sig,
                                                   const int* __restrict__ tau) {
@@ -670,47 +715,21 @@ __global__ void __launch_bounds__(256) k_crt_accum(const TIn* __restrict__ Cl, i
     int tj[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) tj[u] = tau[(long long)b * p.N + j0 + c4 + u];
-    for (int r = blockIdx.y; r < M; r += gridDim.y) {
+    const int step = 2 * gridDim.y;
+    for (int r = blockIdx.y; r < M; r += step) {
+      const int r2 = r + gridDim.y;
+      const bool two = r2 < M;
       const TIn* src = Cl + ((long long)b * M + r) * nc + c4;
-      V4 in[NM];
+      const TIn* src2 = src + (long long)gridDim.y * nc;
+      V4 in[NM], in2[NM];
 #pragma unroll
       for (int l = 0; l < NM; ++l) in[l] = __ldcs(reinterpret_cast<const V4*>(src + l * plane));
-      const int sr = sig[(long long)b * M + r];
-      double shi[4] = {0.0, 0.0, 0.0, 0.0}, slo[4] = {0.0, 0.0, 0.0, 0.0};
+      if (two) {
 #pragma unroll
-      for (int l = 0; l < NM; ++l) {
-        unsigned bb[4];
-        CrtIn<TIn>::biased(in[l], c, l, bb);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double rr = crt_unbias(bb[u]);
-          shi[u] = fma(rr, c.W[l], shi[u]);  // exact
-          slo[u] = fma(rr, c.wlo[l], slo[u]);
-        }
+        for (int l = 0; l < NM; ++l) in2[l] = __ldcs(reinterpret_cast<const V4*>(src2 + l * plane));
       }
-      double v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double q = rint(fma(shi[u], c.twoE_over_M, slo[u] * c.inv_M));
-        const double cp = fma(fma(-q, c.Mh, shi[u]), c.twoE, fma(-q, c.Mlo, slo[u]));
-        double w = (sr == INT_MIN || tj[u] == INT_MIN) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                        : crt_scale(cp, -(sr + tj[u]));
-        w *= p.alpha;
-        if (p.blk_j1a) w += blk_value(p, b, r, j0 + c4 + u);
-        v[u] = w;
-      }
-      double* dst = p.C + (long long)b * p.strideC + (long long)r * p.ldc + j0 + c4;
-      if (p.beta != 0.0) {  // C = alpha A B + beta C
-        const double2 o0 = *reinterpret_cast<const double2*>(dst), o1 = *reinterpret_cast<const double2*>(dst + 2);
-        v[0] = fma(p.beta, o0.x, v[0]);
-        v[1] = fma(p.beta, o0.y, v[1]);
-        v[2] = fma(p.beta, o1.x, v[2]);
-        v[3] = fma(p.beta, o1.y, v[3]);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) bad |= !isfinite(v[u]);
-      *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
-      *reinterpret_cast<double2*>(dst + 2) = make_double2(v[2], v[3]);
+      crt_row<NM, TIn>(in, sig[(long long)b * M + r], tj, b, r, j0 + c4, p, c, bad);
+      if (two) crt_row<NM, TIn>(in2, sig[(long long)b * M + r2], tj, b, r2, j0 + c4, p, c, bad);
     }
   }
   if (p.nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicMax(p.nonfinite, b + p.batch_offset);

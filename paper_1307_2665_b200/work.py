@@ -70,7 +70,7 @@ def build_roofline_seconds(L, q, ngroups, f64_tflops, hbm_gbs):
     return t
 
 
-def emulated_gemms(L, q, d, min_k=1024, min_work=2 ** 32):
+def emulated_gemms(L, q, d, min_k=512, min_work=2 ** 32):
     """(M, N, K, batch) of the merge GEMMs of depth d that run as the FP64 emulation on int8
     (csrc/emu.cu: K >= min_k and M N K batch >= min_work): S = X^-1 R (n3 x ne x n3) and
     T = blk + C S (ne x ne x n3), 2^d merges."""
