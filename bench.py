@@ -487,9 +487,9 @@ def main():
     pin_F = torch.from_numpy(np.ascontiguousarray(F_host)).pin_memory()
     pipe = solver.Pipeline(tree, nodes, device=dev, reuse_graphs=not args.no_graph)
     st = U = None
-    # a stream of problems (about 2 s of device time, 4..20 problems): pipeline fill and drain are
+    # a stream of problems (about 3 s of device time, 5..20 problems): pipeline fill and drain are
     # inside the total; latency_s below is one problem alone
-    n_e2e = min(20, max(3, int(2.0 / max(t_step, 1e-6))))
+    n_e2e = min(20, max(5, int(3.0 / max(t_step, 1e-6))))
     for U, st in pipe.run([(co, pin_F)] * n_e2e):
         st = None
     st = U = None
