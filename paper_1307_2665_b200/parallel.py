@@ -326,6 +326,16 @@ def _merge_flags(d, pivoted):
         (_native.HPS_MERGE_PARENT_PIVOTED if d - 1 in pivoted else 0)
 
 
+def top_groups(s):
+    """The rank groups of the top merges (depths s-1 .. 0; group of parent k at depth d = ranks
+    [k 2^(s-d), (k+1) 2^(s-d))), in the order every rank creates them."""
+    out = []
+    for d in range(s - 1, -1, -1):
+        P = 1 << (s - d)
+        out.extend(tuple(range(k * P, (k + 1) * P)) for k in range(1 << d))
+    return out
+
+
 def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels", check=True, pivoted=()):
     """Subtree-parallel build. `comm` provides rank, world, send(tensor, dst), recv(tensor, src).
     `inputs` (from prepare_distributed) skips the host sampling/grouping. `top_mode` is "panels"
@@ -374,6 +384,8 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels
     # run on all ranks instead of one; the owner assembles T = blkdiag + panels and keeps S for the
     # solve. "owner": the owner merges alone (hps_merge_level). Same per-element arithmetic. ----
     cur = child_T
+    if top_mode == "panels" and hasattr(comm, "setup_groups"):  # every rank, same order: collective
+        comm.setup_groups(top_groups(s))
     for d in range(s - 1, -1, -1):
         P = 1 << (s - d)  # ranks in the parent's group
         k = rank >> (s - d)
@@ -402,19 +414,26 @@ def build_distributed(tree, coeffs, comm, backend, inputs=None, top_mode="panels
         n3, ne, w = dl.n3, dl.ne, dl.ne // P
         status = backend.status_word()
         st.statuses.append((d, k, status))
+        group = tuple(range(owner, owner + P))
         if rank == owner:
             children = backend.stack2(cur, other)
             Xf, perm, R, C = backend.merge_interface(d, children, status, pivoted=pivoted)
             for r in range(1, P):
-                comm.send(Xf, owner + r)
-                comm.send(perm, owner + r)
-                comm.send(C, owner + r)
                 comm.send(backend.col_panel(R, r * w, w), owner + r)
             Rp = backend.col_panel(R, 0, w)
         else:
             Xf, perm = backend.empty((1, n3, n3)), backend.empty_int((1, n3))
             C, Rp = backend.empty((1, ne, n3)), backend.empty((1, n3, w))
-            for t in (Xf, perm, C, Rp):
+            comm.recv(Rp, owner)
+        # the factored interface and C are the same for every rank of the group: one broadcast each
+        # (NCCL pipelines it; the owner no longer sends them P - 1 times)
+        for t in (Xf, perm, C):
+            if hasattr(comm, "bcast"):
+                comm.bcast(t, owner, group)
+            elif rank == owner:
+                for r in range(1, P):
+                    comm.send(t, owner + r)
+            else:
                 comm.recv(t, owner)
         Sp = backend.interface_solve(d, Xf, perm, Rp, status, pivoted=pivoted)
         Tp = backend.panel_gemm(C, Sp)
@@ -547,6 +566,30 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self._groups = {}
+
+    def setup_groups(self, groups):
+        """Create the process subgroups `groups` (tuples of ranks). Collective: every rank calls it
+        with the same list in the same order (torch.distributed.new_group's rule)."""
+        for g in groups:
+            g = tuple(g)
+            if g not in self._groups:
+                self._groups[g] = self.group if len(g) == self.world else self.dist.new_group(list(g))
+
+    def bcast(self, t, src, ranks):
+        """Broadcast t from rank src to `ranks` (a group set up by setup_groups): one NCCL
+        broadcast (pipelined over NVLink), so the source sends the data about once instead of once
+        per receiver."""
+        g = self._groups.get(tuple(ranks))
+        if g is None:
+            if self.rank == src:
+                for r in ranks:
+                    if r != src:
+                        self.send(t, r)
+            else:
+                self.recv(t, src)
+            return
+        self.dist.broadcast(t, src, group=g)
 
     def send(self, t, dst):
         self.dist.send(t.contiguous(), dst, group=self.group)
@@ -634,6 +677,17 @@ class LocalComm:
 
     def bcast_int(self, v):
         return int(self.allgather_obj(v)[0])
+
+    def setup_groups(self, groups):
+        pass
+
+    def bcast(self, t, src, ranks):
+        if self.rank == src:
+            for r in ranks:
+                if r != src:
+                    self.send(t, r)
+        else:
+            self.recv(t, src)
 
 
 def _cuda_backend_extras():
