@@ -354,6 +354,7 @@ struct CrtConst {
   double W[CRT_MAX], wlo[CRT_MAX];    // w_l = W_l 2^E + wlo_l, W_l integer, |wlo_l| <= 2^(E - 1)
   double Mh, Mlo;                     // Mod = Mh 2^E + Mlo
   double twoE_over_M, inv_M, twoE;
+  double gP[(CRT_MAX + 2) / 3], ginvP[(CRT_MAX + 2) / 3];  // residue groups: products of moduli 3g..3g+2 (< 2^24)
 };
 
 static const int kModuli[CRT_MAX] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
@@ -410,6 +411,12 @@ static bool crt_constants(int n, CrtConst& c) {
   c.twoE = ldexp(1.0, c.E);
   c.twoE_over_M = c.twoE / dMod;
   c.inv_M = 1.0 / dMod;
+  for (int g = 0; 3 * g < n; ++g) {
+    double P = 1.0;
+    for (int l = 3 * g; l < std::min(n, 3 * g + 3); ++l) P *= (double)kModuli[l];  // < 2^24, exact
+    c.gP[g] = P;
+    c.ginvP[g] = 1.0 / P;
+  }
   return true;
 }
 
@@ -529,15 +536,25 @@ __global__ void __launch_bounds__(256) k_crt_col_scale(const double* __restrict_
   }
 }
 
-// symmetric residue of the integer x (|x| <= 2^55, exact in fp64) modulo m, in [-128, 127]; the
-// quotient is rounded and the remainder read out through the 1.5 * 2^52 shift (no conversion unit).
-__device__ __forceinline__ int crt_residue(double x, double m, double inv_m, int mi) {
-  const double kShift = 6755399441055744.0;          // 1.5 * 2^52
-  const double q = (x * inv_m + kShift) - kShift;    // rint(x / m), |x / m| < 2^51
-  const double r = fma(-m, q, x);                    // exact: a small integer
-  int ri = __double2loint(r + kShift);               // r, two's complement in the low word
-  ri = ri > 127 ? ri - mi : ri;
-  return ri < -128 ? ri + mi : ri;
+// Residues of the integer x (|x| <= 2^55, exact in fp64) modulo every m_l, each in [-128, 128]
+// (+128 only for m = 256, whose byte wraps to the same class), as the low bytes of r[l]. Two levels,
+// all on the FP64 pipe and without range fixes: y = x mod P_g for the product P_g < 2^24 of three
+// moduli (the quotient rounded through the 1.5 * 2^52 shift may be one off, so |y| <= 1.5 P_g <
+// 2^25, exact), then y mod m_l with an exact quotient (y / m_l is far from the half-integers its
+// rounding could confuse), read out through the same shift.
+constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
+template <int NM>
+__device__ __forceinline__ void crt_residues(double x, const CrtConst& c, int (&r)[NM]) {
+#pragma unroll
+  for (int g = 0; g < (NM + 2) / 3; ++g) {
+    const double q = fma(x, c.ginvP[g], kShift) - kShift;
+    const double y = fma(-c.gP[g], q, x);
+#pragma unroll
+    for (int l = 3 * g; l < (3 * g + 3 < NM ? 3 * g + 3 : NM); ++l) {
+      const double ql = fma(y, c.inv_m[l], kShift) - kShift;
+      r[l] = __double2loint(fma(-c.m[l], ql, y) + kShift);
+    }
+  }
 }
 
 // residues of the scaled rows of A: out[l][b][i][k]; 4 k per thread
@@ -550,55 +567,52 @@ __global__ void __launch_bounds__(256) k_crt_split_rows(const double* __restrict
   if (k4 >= K) return;  // K % 16 == 0
   const int sg = sig[(long long)b * M + r];
   const double* Ar = A + (long long)b * sA + (long long)r * lda + k4;
-  double x[4];
+  int res[4][NM];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) x[u] = sg == INT_MIN ? 0.0 : rint(crt_ldexp(Ar[u], sg));  // exact scaling
+  for (int u = 0; u < 4; ++u) crt_residues<NM>(sg == INT_MIN ? 0.0 : rint(crt_ldexp(Ar[u], sg)), c, res[u]);
   const long long plane = (long long)batch * M * K;
-  char4* o = reinterpret_cast<char4*>(out + ((long long)b * M + r) * K + k4);
+  unsigned* o = reinterpret_cast<unsigned*>(out + ((long long)b * M + r) * K + k4);
 #pragma unroll
   for (int l = 0; l < NM; ++l)
-    o[l * (plane / 4)] = make_char4(crt_residue(x[0], c.m[l], c.inv_m[l], c.mi[l]),
-                                    crt_residue(x[1], c.m[l], c.inv_m[l], c.mi[l]),
-                                    crt_residue(x[2], c.m[l], c.inv_m[l], c.mi[l]),
-                                    crt_residue(x[3], c.m[l], c.inv_m[l], c.mi[l]));
+    o[l * (plane / 4)] = (res[0][l] & 0xFF) | ((res[1][l] & 0xFF) << 8) | ((res[2][l] & 0xFF) << 16) | (res[3][l] << 24);
 }
 
 // residues of the scaled columns of B, transposed: out[l][b][j][k]. Tile: 32 k x 64 j through
-// shared memory.
+// shared memory; each thread 8 consecutive k of one column (two packed words per modulus).
 template <int NM>
 __global__ void __launch_bounds__(256) k_crt_split_cols(const double* __restrict__ B, long long ldb, long long sB, int K,
                                                        int N, int batch, const int* __restrict__ tau, CrtConst c,
                                                        signed char* __restrict__ out) {
-  __shared__ signed char sd[NM][64][36];
+  __shared__ unsigned sd[NM][64][9];  // 32 k bytes per (l, j) + a padding word
   const int b = blockIdx.z;
   const int k0 = blockIdx.y * 32, j0 = blockIdx.x * 64;
   const double* Bb = B + (long long)b * sB;
-  // 8 elements per thread: all loads first, then the residues of the 8 interleaved
-  const int jj = threadIdx.x % 64, kq = threadIdx.x / 64;  // k = k0 + kq + 4 i
+  const int jj = threadIdx.x % 64, kq = threadIdx.x / 64;  // k = k0 + 8 kq + i
   const int j = j0 + jj;
   const int tj = j < N ? tau[(long long)b * N + j] : INT_MIN;
   double x[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int k = k0 + kq + 4 * i;
-    x[i] = (k < K && j < N && tj != INT_MIN) ? __ldg(Bb + (long long)k * ldb + j) : 0.0;
+    const int k = k0 + 8 * kq + i;
+    x[i] = (k < K && tj != INT_MIN) ? __ldg(Bb + (long long)k * ldb + j) : 0.0;
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] = rint(crt_ldexp(x[i], tj == INT_MIN ? 0 : tj));
+  for (int h = 0; h < 2; ++h) {
+    int res[4][NM];
 #pragma unroll
-  for (int l = 0; l < NM; ++l) {
+    for (int i = 0; i < 4; ++i) crt_residues<NM>(rint(crt_ldexp(x[4 * h + i], tj == INT_MIN ? 0 : tj)), c, res[i]);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sd[l][jj][kq + 4 * i] = (signed char)crt_residue(x[i], c.m[l], c.inv_m[l], c.mi[l]);
+    for (int l = 0; l < NM; ++l)
+      sd[l][jj][2 * kq + h] =
+          (res[0][l] & 0xFF) | ((res[1][l] & 0xFF) << 8) | ((res[2][l] & 0xFF) << 16) | (res[3][l] << 24);
   }
   __syncthreads();
   const long long plane = (long long)batch * N * K;
   signed char* ob = out + (long long)b * N * K;
   for (int idx = threadIdx.x; idx < NM * 64 * 8; idx += blockDim.x) {  // 4 bytes per store
-    const int k4 = (idx % 8) * 4, rest = idx / 8, jj = rest % 64, l = rest / 64;
-    const int k = k0 + k4, j = j0 + jj;
-    if (k < K && j < N)
-      *reinterpret_cast<char4*>(ob + l * plane + (long long)j * K + k) =
-          *reinterpret_cast<const char4*>(&sd[l][jj][k4]);
+    const int w = idx % 8, rest = idx / 8, jr = rest % 64, l = rest / 64;
+    const int k = k0 + 4 * w, jg = j0 + jr;
+    if (k < K && jg < N) *reinterpret_cast<unsigned*>(ob + l * plane + (long long)jg * K + k) = sd[l][jr][w];
   }
 }
 
