@@ -163,3 +163,53 @@ def test_interface_conditioning_report(cfg, L):
         cx, c11 = np.linalg.cond(Xd), np.linalg.cond(Xd[:h, :h])
         print(f"cfg{cfg} L{L} depth {d}: n3 {n3}, cond(X_d) {cx:.2e}, cond(A11) {c11:.2e}, LU growth {growth:.2f}")
         assert np.isfinite(cx) and cx < 1e10 and growth < 1e3  # cfg4 reaches 5e6 (its global problem is near-resonant)
+
+
+def test_crt_reconstruction_model():
+    """The modular FP64 emulation's reconstruction (csrc/emu.cu, crt_constants / k_crt_accum)
+    restated with Python integers and float64: for integers |C'| <= Mod / 8 given by their residues
+    modulo the 14 moduli, the exact high sum, the rounded quotient and the two-part correction
+    recover C' to within an ulp of the largest |C'|; the quotient never rounds the wrong way."""
+    import math
+
+    moduli = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199]
+    Mod = math.prod(moduli)
+    bits = Mod.bit_length()
+    E = bits - 42
+
+    def split(v):  # v = hi 2^E + lo, |lo| <= 2^(E-1)
+        unit = 1 << E
+        qv = (v + unit // 2) >> E if v >= 0 else -((-v + unit // 2) >> E)
+        return qv, v - qv * unit
+
+    W, wlo = [], []
+    for m in moduli:
+        Ml = Mod // m
+        y = pow(Ml % m, -1, m)
+        w = (Ml * y) % Mod
+        if w > Mod // 2:
+            w -= Mod
+        h, lo = split(w)
+        assert abs(h) < 2 ** 42 and abs(lo) <= 2 ** (E - 1)
+        W.append(float(h))
+        wlo.append(float(lo))
+    Mh, Mlo = split(Mod)
+    twoE, twoE_over_M, inv_M = 2.0 ** E, 2.0 ** E / float(Mod), 1.0 / float(Mod)
+    rng = np.random.default_rng(11)
+    bound = Mod // 8
+    vals = [int(x) for x in rng.integers(-2 ** 62, 2 ** 62, 200)]
+    vals = [v * (bound // 2 ** 62) + int(rng.integers(0, 2 ** 40)) for v in vals] + [bound, -bound, 0, 1, -1]
+    for C in vals:
+        r = [((C % m) + m // 2) % m - m // 2 for m in moduli]  # symmetric residues, |r| <= 128
+        shi = 0.0
+        slo = 0.0
+        for rr, Wl, wl in zip(r, W, wlo):
+            shi += rr * Wl  # exact: |shi| < 2^52
+            slo += rr * wl
+        assert abs(shi) < 2 ** 52
+        q = round(shi * twoE_over_M + slo * inv_M)
+        true_q = (sum(rr * (Wl * 2 ** E + wl) for rr, Wl, wl in zip(r, W, wlo)) - C) / Mod
+        assert abs(q - true_q) < 0.25 or q == round(true_q)
+        X = shi - q * float(Mh)  # exact
+        cp = X * twoE + (slo - q * float(Mlo))
+        assert abs(cp - C) <= 2.0 ** (bits - 4 - 52), (C, cp)
