@@ -718,7 +718,7 @@ __device__ __forceinline__ void crt_row(const typename CrtIn<TIn>::V (&in)[NM], 
 // per residue, no conversions). (Two rows per step, for more loads in flight, was slower: 8.2 vs
 // 6.3 ms on 64 x 4096 x 4096 outputs.)
 template <int NM, typename TIn>
-__global__ void __launch_bounds__(256) k_crt_accum(const TIn* __restrict__ Cl, int M, int nc, int j0, GemmParams p,
+__global__ void __launch_bounds__(256, 4) k_crt_accum(const TIn* __restrict__ Cl, int M, int nc, int j0, GemmParams p,
                                                   CrtConst c, const int* __restrict__ sig,
                                                   const int* __restrict__ tau) {
   typedef typename CrtIn<TIn>::V V4;
