@@ -549,10 +549,11 @@ __device__ __forceinline__ void crt_residues(double x, const CrtConst& c, int (&
   for (int g = 0; g < (NM + 2) / 3; ++g) {
     const double q = fma(x, c.ginvP[g], kShift) - kShift;
     const double y = fma(-c.gP[g], q, x);
+    const double ys = y + kShift;  // exact; then y - m ql + kShift in one exact fma
 #pragma unroll
     for (int l = 3 * g; l < (3 * g + 3 < NM ? 3 * g + 3 : NM); ++l) {
       const double ql = fma(y, c.inv_m[l], kShift) - kShift;
-      r[l] = __double2loint(fma(-c.m[l], ql, y) + kShift);
+      r[l] = __double2loint(fma(-c.m[l], ql, ys));
     }
   }
 }
