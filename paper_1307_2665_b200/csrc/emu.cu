@@ -353,6 +353,7 @@ struct CrtConst {
   int mi[CRT_MAX], minv[CRT_MAX];     // reduction of int32 products: minv = floor(2^32 / m)
   double W[CRT_MAX], wlo[CRT_MAX];    // w_l = W_l 2^E + wlo_l, W_l integer, |wlo_l| <= 2^(E - 1)
   double Mh, Mlo;                     // Mod = Mh 2^E + Mlo
+  double shi0, slo0;                  // -kCrtBias sum W_l (exact), -kCrtBias sum wlo_l: the sums start here
   double twoE_over_M, inv_M, twoE;
   double gP[(CRT_MAX + 2) / 3], ginvP[(CRT_MAX + 2) / 3];  // residue groups: products of moduli 3g..3g+2 (< 2^24)
 };
@@ -360,12 +361,21 @@ struct CrtConst {
 static const int kModuli[CRT_MAX] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
 
 // Reconstruction arithmetic (k_crt_accum), with r_l = C_l mod m_l in [-128, 127], n <= 16 and
-// E = bits - 42 (Mod < 2^bits), all in fp64:
-//   shi = sum r_l W_l                    exact: |W_l| <= 2^41 + 1, |shi| < 2^52
-//   slo = sum r_l wlo_l                  |slo| <= 2^(E + 10), rounding 2^(E - 43)
+// E = bits - 36 (Mod < 2^bits), all in fp64. The residue byte b_l = r_l + 128 enters as the double
+// d_l = 4096 + b_l = r_l + kCrtBias, built with ONE byte permute (the byte dropped into mantissa
+// bits 8..15 of the high word 0x40B00000; low word 0), so the sums run over d_l from a bias-
+// cancelling start value instead of converting and unbiasing every residue:
+//   shi = shi0 + sum d_l W_l = sum r_l W_l   exact: |W_l| <= 2^35 + 1, d_l < 2^12.1, every partial sum
+//                                            an integer below 2^51 (shi0 = -kCrtBias sum W_l, exact)
+//   slo = slo0 + sum d_l wlo_l = sum r_l wlo_l   exact as well: wlo_l is w_l's remainder rounded to a
+//                                            multiple of 2^(E - 34) (<= 34 significant bits), which
+//                                            shifts C' by at most 14 * 128 * 2^(E - 35) = 2^(bits - 60)
 //   q   = rint(shi 2^E / Mod + slo / Mod)   |C'| <= Mod / 8 leaves a 3/8 margin to the rounding edge
-//   C'  = (shi - q Mh) 2^E + (slo - q Mlo)  the first factor exact (an integer < 2^42)
-// so C' carries an absolute error ~2^(bits - 85), far below an fp64 ulp of the largest |C'| ~ 2^(bits - 4).
+//   C'  = (shi - q Mh) 2^E + (slo - q Mlo)  the first factor exact (an integer < 2^47)
+// so C' carries an absolute error ~2^(bits - 60): 1/16 ulp of the largest |C'| ~ 2^(bits - 4), and a
+// thousand times below the rounding of A' and B' themselves (~sqrt(K) 2^(PB - 1) >= 2^(bits / 2 + 3)).
+// Both sums being exact, zero residues give an exact zero and the result does not depend on order.
+constexpr double kCrtBias = 4224.0;  // 4096 (the permuted double's leading one) + 128 (the byte's bias)
 static bool crt_constants(int n, CrtConst& c) {
   if (n < 2 || n > CRT_MAX) return false;
   typedef unsigned __int128 u128;
@@ -379,18 +389,25 @@ static bool crt_constants(int n, CrtConst& c) {
   c.n = n;
   c.PA = (flo - 3) / 2;
   c.PB = flo - 3 - c.PA;
-  c.E = bits - 42;
+  c.E = bits - 36;
   auto to_double = [](i128 v) {
     const bool neg = v < 0;
     u128 u = neg ? (u128)(-v) : (u128)v;
     const double d = (double)(unsigned long long)(u >> 64) * 18446744073709551616.0 + (double)(unsigned long long)(u & ~0ULL);
     return neg ? -d : d;
   };
-  auto split = [&](i128 v, double& hi, double& lo) {  // v = hi 2^E + lo, hi integer, |lo| <= 2^(E - 1)
+  // v = hi 2^E + lo, hi integer, |lo| <= 2^(E - 1); keep > 0: lo rounded to a multiple of 2^(E - 34)
+  // (at most 34 significant bits, so that sums of d_l wlo_l are exact too)
+  auto split = [&](i128 v, double& hi, double& lo, bool keep33) {
     const i128 unit = (i128)1 << c.E;
     const i128 qv = v >= 0 ? (v + unit / 2) >> c.E : -((-v + unit / 2) >> c.E);
-    hi = to_double(qv);  // |qv| < 2^42: exact
-    lo = to_double(v - qv * unit);
+    hi = to_double(qv);  // |qv| < 2^37: exact
+    i128 rem = v - qv * unit;
+    if (keep33) {
+      const i128 u2 = (i128)1 << (c.E - 34);
+      rem = (rem >= 0 ? (rem + u2 / 2) / u2 : -((-rem + u2 / 2) / u2)) * u2;
+    }
+    lo = to_double(rem);
   };
   const double dMod = to_double((i128)Mod);
   for (int l = 0; l < n; ++l) {
@@ -405,9 +422,13 @@ static bool crt_constants(int n, CrtConst& c) {
     c.inv_m[l] = 1.0 / (double)m;
     c.mi[l] = (int)m;
     c.minv[l] = (int)((1ULL << 32) / (unsigned long long)m);
-    split(ws, c.W[l], c.wlo[l]);
+    split(ws, c.W[l], c.wlo[l], true);
   }
-  split((i128)Mod, c.Mh, c.Mlo);
+  split((i128)Mod, c.Mh, c.Mlo, false);
+  double sw = 0.0, swl = 0.0;  // integers (in units of 1 and 2^(E - 34)) below 2^40: both sums exact
+  for (int l = 0; l < n; ++l) { sw += c.W[l]; swl += c.wlo[l]; }
+  c.shi0 = -kCrtBias * sw;  // 13 x 40 bits: exact
+  c.slo0 = -kCrtBias * swl;
   c.twoE = ldexp(1.0, c.E);
   c.twoE_over_M = c.twoE / dMod;
   c.inv_M = 1.0 / dMod;
@@ -634,9 +655,15 @@ __device__ __forceinline__ unsigned crt_biased(int v, int m, int minv) {
   r = r > 127 ? r - m : r;
   return (unsigned)(r + 128);
 }
-// biased residue (0..255) -> exact double r - 128, without the conversion unit
-__device__ __forceinline__ double crt_unbias(unsigned b) {
-  return __hiloint2double(0x43300000, (int)b) - 4503599627370624.0;  // 2^52 + 128
+// biased residue byte K of the packed word x -> the exact double 4096 + b = r + kCrtBias: one byte
+// permute drops the byte into mantissa bits 8..15 of the high word 0x40B00000 (2^12). Only the high
+// word of d is rewritten (its low word stays the zero it was initialised with), so no move is spent
+// on the low half of every temporary.
+template <int K>
+__device__ __forceinline__ void crt_biased_double(double& d, unsigned x) {
+  asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %0;\n\tprmt.b32 hi, %1, 0x40B00000, %2;\n\tmov.b64 %0, {lo, hi};\n\t}"
+      : "+d"(d)
+      : "r"(x), "n"(0x7604 + (K << 4)));
 }
 // 2^e for |e| <= 1022 (exact scale of the outputs), else ldexp
 __device__ __forceinline__ double crt_scale(double x, int e) {
@@ -649,42 +676,41 @@ struct CrtIn;
 template <>
 struct CrtIn<int> {  // cuBLASLt int32 products: reduced here
   typedef int4 V;
-  static __device__ __forceinline__ void biased(const V& x, const CrtConst& c, int l, unsigned (&b)[4]) {
-    b[0] = crt_biased(x.x, c.mi[l], c.minv[l]);
-    b[1] = crt_biased(x.y, c.mi[l], c.minv[l]);
-    b[2] = crt_biased(x.z, c.mi[l], c.minv[l]);
-    b[3] = crt_biased(x.w, c.mi[l], c.minv[l]);
+  static __device__ __forceinline__ void biased(const V& x, const CrtConst& c, int l, double (&d)[4]) {
+    crt_biased_double<0>(d[0], crt_biased(x.x, c.mi[l], c.minv[l]));
+    crt_biased_double<0>(d[1], crt_biased(x.y, c.mi[l], c.minv[l]));
+    crt_biased_double<0>(d[2], crt_biased(x.z, c.mi[l], c.minv[l]));
+    crt_biased_double<0>(d[3], crt_biased(x.w, c.mi[l], c.minv[l]));
   }
 };
 template <>
 struct CrtIn<unsigned char> {  // the tcgen05 kernel's biased residues, 4 per word
   typedef unsigned V;
-  static __device__ __forceinline__ void biased(const V& x, const CrtConst&, int, unsigned (&b)[4]) {
-    b[0] = x & 0xFFu;
-    b[1] = (x >> 8) & 0xFFu;
-    b[2] = (x >> 16) & 0xFFu;
-    b[3] = x >> 24;
+  static __device__ __forceinline__ void biased(const V& x, const CrtConst&, int, double (&d)[4]) {
+    crt_biased_double<0>(d[0], x);
+    crt_biased_double<1>(d[1], x);
+    crt_biased_double<2>(d[2], x);
+    crt_biased_double<3>(d[3], x);
   }
 };
 
 // Reconstruction of the output columns [j0, j0 + nc) from the NM products of that panel
 // (Cl[l][b][i][0..nc): int32 products, or biased int8 residues), with the row / column scales,
 // alpha, the merge's block-diagonal addend and the non-finite flag. Rows on blockIdx.y (grid-stride),
-// 4 columns per thread; all NM loads of a row are issued before the arithmetic (4 FP64 operations
+// 4 columns per thread; all NM loads of a row are issued before the arithmetic (one byte permute and two fma
 // per residue, no conversions).
 template <int NM, typename TIn>
 __device__ __forceinline__ void crt_row(const typename CrtIn<TIn>::V (&in)[NM], int sr, const int (&tj)[4], int b, int r,
                                         int col0, const GemmParams& p, const CrtConst& c, bool& bad) {
-  double shi[4] = {0.0, 0.0, 0.0, 0.0}, slo[4] = {0.0, 0.0, 0.0, 0.0};
+  double shi[4] = {c.shi0, c.shi0, c.shi0, c.shi0}, slo[4] = {c.slo0, c.slo0, c.slo0, c.slo0};
+  double d[4] = {0.0, 0.0, 0.0, 0.0};  // r + kCrtBias (high words rewritten per modulus)
 #pragma unroll
   for (int l = 0; l < NM; ++l) {
-    unsigned bb[4];
-    CrtIn<TIn>::biased(in[l], c, l, bb);
+    CrtIn<TIn>::biased(in[l], c, l, d);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double rr = crt_unbias(bb[u]);
-      shi[u] = fma(rr, c.W[l], shi[u]);  // exact
-      slo[u] = fma(rr, c.wlo[l], slo[u]);
+      shi[u] = fma(d[u], c.W[l], shi[u]);  // exact
+      slo[u] = fma(d[u], c.wlo[l], slo[u]);
     }
   }
   double v[4];
@@ -715,7 +741,7 @@ __device__ __forceinline__ void crt_row(const typename CrtIn<TIn>::V (&in)[NM], 
 // Reconstruction of the output columns [j0, j0 + nc) from the NM products of that panel
 // (Cl[l][b][i][0..nc): int32 products, or biased int8 residues), with the row / column scales,
 // alpha, the merge's block-diagonal addend and the non-finite flag. Rows on blockIdx.y (grid-stride),
-// 4 columns per thread; all NM loads of a row are issued before the arithmetic (4 FP64 operations
+// 4 columns per thread; all NM loads of a row are issued before the arithmetic (one byte permute and two fma
 // per residue, no conversions). (Two rows per step, for more loads in flight, was slower: 8.2 vs
 // 6.3 ms on 64 x 4096 x 4096 outputs.)
 template <int NM, typename TIn>

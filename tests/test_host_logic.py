@@ -168,19 +168,26 @@ def test_interface_conditioning_report(cfg, L):
 def test_crt_reconstruction_model():
     """The modular FP64 emulation's reconstruction (csrc/emu.cu, crt_constants / k_crt_accum)
     restated with Python integers and float64: for integers |C'| <= Mod / 8 given by their residues
-    modulo the 14 moduli, the exact high sum, the rounded quotient and the two-part correction
-    recover C' to within an ulp of the largest |C'|; the quotient never rounds the wrong way."""
+    modulo the 14 moduli, the exact high sum (run over the biased doubles d = r + 4224 from a
+    bias-cancelling start value, as the kernel does), the rounded quotient and the two-part
+    correction recover C' to within an ulp of the largest |C'|; the quotient never rounds the
+    wrong way and every partial high sum stays an exact integer."""
     import math
 
     moduli = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199]
     Mod = math.prod(moduli)
     bits = Mod.bit_length()
-    E = bits - 42
+    E = bits - 36
+    bias = 4224.0  # 4096 (the byte-permuted double's leading one) + 128 (the byte's bias)
 
-    def split(v):  # v = hi 2^E + lo, |lo| <= 2^(E-1)
+    def split(v, keep33=False):  # v = hi 2^E + lo, |lo| <= 2^(E-1); keep33: lo to a multiple of 2^(E-34)
         unit = 1 << E
         qv = (v + unit // 2) >> E if v >= 0 else -((-v + unit // 2) >> E)
-        return qv, v - qv * unit
+        rem = v - qv * unit
+        if keep33:
+            u2 = 1 << (E - 34)
+            rem = ((rem + u2 // 2) // u2 if rem >= 0 else -((-rem + u2 // 2) // u2)) * u2
+        return qv, rem
 
     W, wlo = [], []
     for m in moduli:
@@ -189,26 +196,32 @@ def test_crt_reconstruction_model():
         w = (Ml * y) % Mod
         if w > Mod // 2:
             w -= Mod
-        h, lo = split(w)
-        assert abs(h) < 2 ** 42 and abs(lo) <= 2 ** (E - 1)
+        h, lo = split(w, True)
+        assert abs(h) <= 2 ** 35 + 1 and abs(lo) <= 2 ** (E - 1)
         W.append(float(h))
         wlo.append(float(lo))
     Mh, Mlo = split(Mod)
     twoE, twoE_over_M, inv_M = 2.0 ** E, 2.0 ** E / float(Mod), 1.0 / float(Mod)
+    shi0, slo0 = -bias * sum(W), -bias * sum(wlo)
+    assert shi0 == -int(bias) * sum(int(w) for w in W)  # exact
     rng = np.random.default_rng(11)
     bound = Mod // 8
     vals = [int(x) for x in rng.integers(-2 ** 62, 2 ** 62, 200)]
     vals = [v * (bound // 2 ** 62) + int(rng.integers(0, 2 ** 40)) for v in vals] + [bound, -bound, 0, 1, -1]
     for C in vals:
         r = [((C % m) + m // 2) % m - m // 2 for m in moduli]  # symmetric residues, |r| <= 128
-        shi = 0.0
-        slo = 0.0
+        shi, slo = shi0, slo0
+        exact = int(shi0)
         for rr, Wl, wl in zip(r, W, wlo):
-            shi += rr * Wl  # exact: |shi| < 2^52
-            slo += rr * wl
-        assert abs(shi) < 2 ** 52
+            d = float(rr) + bias  # 4096 + (r + 128)
+            shi = shi + d * Wl  # the product (13 x 36 bits) and the sum are exact, as the kernel's fma
+            exact += (rr + int(bias)) * int(Wl)
+            assert abs(exact) < 2 ** 53 and shi == float(exact)  # every partial sum exact
+            slo += d * wl
+        assert shi == float(sum(rr * int(Wl) for rr, Wl in zip(r, W)))
+        assert slo == float(sum(rr * int(wl) for rr, wl in zip(r, wlo)))  # the low sum is exact too
         q = round(shi * twoE_over_M + slo * inv_M)
-        true_q = (sum(rr * (Wl * 2 ** E + wl) for rr, Wl, wl in zip(r, W, wlo)) - C) / Mod
+        true_q = (sum(rr * (int(Wl) * 2 ** E + int(wl)) for rr, Wl, wl in zip(r, W, wlo)) - C) / Mod
         assert abs(q - true_q) < 0.25 or q == round(true_q)
         X = shi - q * float(Mh)  # exact
         cp = X * twoE + (slo - q * float(Mlo))
