@@ -697,10 +697,24 @@ struct CrtIn<unsigned char> {  // the tcgen05 kernel's biased residues, 4 per wo
 // Reconstruction of the output columns [j0, j0 + nc) from the NM products of that panel
 // (Cl[l][b][i][0..nc): int32 products, or biased int8 residues), with the row / column scales,
 // alpha, the merge's block-diagonal addend and the non-finite flag. Rows on blockIdx.y (grid-stride),
-// 4 columns per thread; all NM loads of a row are issued before the arithmetic (one byte permute and two fma
-// per residue, no conversions).
+// 4 columns per thread; all NM loads of a row are issued before the arithmetic (one byte permute and
+// two fma per residue, no conversions). Everything that depends on the columns only is set up
+// before the row loop: the column scales as doubles (times alpha), their block-diagonal map entries;
+// per row the scale is one product of two powers of two (rows or columns whose exponents leave the
+// normal range take crt_scale instead), and the residue planes are walked with one pointer.
+// (Two rows per step, for more loads in flight, was slower: 8.2 vs 6.3 ms on 64 x 4096 x 4096 outputs.)
+struct CrtCols {
+  int tj[4];
+  double csa[4];   // alpha 2^-tj (fast path)
+  bool fast;       // every tj finite and within the fast range, alpha's exponent small
+  int tjmin, tjmax;
+  int cm[4];       // block-diagonal addend: column map entries
+  bool ctop[4];    //   and the half each column lies in
+};
+constexpr int kCrtFastExp = 960;  // |sig|, |tau|, |sig + tau| up to here: 2^-e built and multiplied directly
+
 template <int NM, typename TIn>
-__device__ __forceinline__ void crt_row(const typename CrtIn<TIn>::V (&in)[NM], int sr, const int (&tj)[4], int b, int r,
+__device__ __forceinline__ void crt_row(const typename CrtIn<TIn>::V (&in)[NM], int sr, const CrtCols& cc, int b, int r,
                                         int col0, const GemmParams& p, const CrtConst& c, bool& bad) {
   double shi[4] = {c.shi0, c.shi0, c.shi0, c.shi0}, slo[4] = {c.slo0, c.slo0, c.slo0, c.slo0};
   double d[4] = {0.0, 0.0, 0.0, 0.0};  // r + kCrtBias (high words rewritten per modulus)
@@ -710,19 +724,34 @@ __device__ __forceinline__ void crt_row(const typename CrtIn<TIn>::V (&in)[NM], 
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       shi[u] = fma(d[u], c.W[l], shi[u]);  // exact
-      slo[u] = fma(d[u], c.wlo[l], slo[u]);
+      slo[u] = fma(d[u], c.wlo[l], slo[u]);  // exact
     }
   }
   double v[4];
+  const bool fast = cc.fast && (unsigned)(sr + kCrtFastExp) <= 2u * kCrtFastExp &&
+                    (unsigned)(sr + cc.tjmin + kCrtFastExp) <= 2u * kCrtFastExp &&
+                    (unsigned)(sr + cc.tjmax + kCrtFastExp) <= 2u * kCrtFastExp;
+  const double rs = __hiloint2double((int)((unsigned)(1023 - sr) << 20), 0);  // 2^-sr (used on the fast path only)
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const double q = rint(fma(shi[u], c.twoE_over_M, slo[u] * c.inv_M));
     const double cp = fma(fma(-q, c.Mh, shi[u]), c.twoE, fma(-q, c.Mlo, slo[u]));
-    double w = (sr == INT_MIN || tj[u] == INT_MIN) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                    : crt_scale(cp, -(sr + tj[u]));
-    w *= p.alpha;
-    if (p.blk_j1a) w += blk_value(p, b, r, col0 + u);
-    v[u] = w;
+    if (fast) {
+      v[u] = cp * (rs * cc.csa[u]);  // rs csa: an exact power-of-two scaling of alpha; one rounding
+    } else {
+      const double w = (sr == INT_MIN || cc.tj[u] == INT_MIN) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                               : crt_scale(cp, -(sr + cc.tj[u]));
+      v[u] = w * p.alpha;
+    }
+  }
+  if (p.blk_j1a) {  // T = blkdiag(Ta11, Tb22) + C S: the addend of this row's half
+    const int n1 = p.M >> 1;
+    const bool top = r < n1;
+    const int gb = b + p.batch_offset;
+    const double* src = (top ? p.blk.a(gb) : p.blk.bb(gb)) + (long long)(top ? p.blk_j1a[r] : p.blk_j2b[r - n1]) * p.blk.m;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (cc.ctop[u] == top) v[u] += src[cc.cm[u]];
   }
   double* dst = p.C + (long long)b * p.strideC + (long long)r * p.ldc + col0;
   if (p.beta != 0.0) {  // C = alpha A B + beta C
@@ -738,12 +767,6 @@ __device__ __forceinline__ void crt_row(const typename CrtIn<TIn>::V (&in)[NM], 
   *reinterpret_cast<double2*>(dst + 2) = make_double2(v[2], v[3]);
 }
 
-// Reconstruction of the output columns [j0, j0 + nc) from the NM products of that panel
-// (Cl[l][b][i][0..nc): int32 products, or biased int8 residues), with the row / column scales,
-// alpha, the merge's block-diagonal addend and the non-finite flag. Rows on blockIdx.y (grid-stride),
-// 4 columns per thread; all NM loads of a row are issued before the arithmetic (one byte permute and two fma
-// per residue, no conversions). (Two rows per step, for more loads in flight, was slower: 8.2 vs
-// 6.3 ms on 64 x 4096 x 4096 outputs.)
 template <int NM, typename TIn>
 __global__ void __launch_bounds__(256, 4) k_crt_accum(const TIn* __restrict__ Cl, int M, int nc, int j0, GemmParams p,
                                                   CrtConst c, const int* __restrict__ sig,
@@ -754,15 +777,35 @@ __global__ void __launch_bounds__(256, 4) k_crt_accum(const TIn* __restrict__ Cl
   const long long plane = (long long)p.batch * M * nc;
   bool bad = false;
   if (c4 < nc) {
-    int tj[4];
+    CrtCols cc;
+    int ea;
+    frexp(p.alpha, &ea);
+    cc.fast = p.alpha != 0.0 && isfinite(p.alpha) && ea >= -30 && ea <= 30;
+    cc.tjmin = INT_MAX;
+    cc.tjmax = INT_MIN;
+    const int n1 = p.M >> 1;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) tj[u] = tau[(long long)b * p.N + j0 + c4 + u];
+    for (int u = 0; u < 4; ++u) {
+      const int col = j0 + c4 + u;
+      const int t = tau[(long long)b * p.N + col];
+      cc.tj[u] = t;
+      cc.fast = cc.fast && (unsigned)(t + kCrtFastExp) <= 2u * kCrtFastExp;
+      cc.tjmin = min(cc.tjmin, t);
+      cc.tjmax = max(cc.tjmax, t);
+      cc.csa[u] = __hiloint2double((int)((unsigned)(1023 - (cc.fast ? t : 0)) << 20), 0) * p.alpha;
+      cc.ctop[u] = col < n1;
+      cc.cm[u] = p.blk_j1a ? (cc.ctop[u] ? p.blk_j1a[col] : p.blk_j2b[col - n1]) : 0;
+    }
+    const TIn* src0 = Cl + (long long)b * M * nc + c4;
     for (int r = blockIdx.y; r < M; r += gridDim.y) {
-      const TIn* src = Cl + ((long long)b * M + r) * nc + c4;
+      const TIn* src = src0 + (long long)r * nc;
       V4 in[NM];
 #pragma unroll
-      for (int l = 0; l < NM; ++l) in[l] = __ldcs(reinterpret_cast<const V4*>(src + l * plane));
-      crt_row<NM, TIn>(in, sig[(long long)b * M + r], tj, b, r, j0 + c4, p, c, bad);
+      for (int l = 0; l < NM; ++l) {
+        in[l] = __ldcs(reinterpret_cast<const V4*>(src));
+        src += plane;
+      }
+      crt_row<NM, TIn>(in, sig[(long long)b * M + r], cc, b, r, j0 + c4, p, c, bad);
     }
   }
   if (p.nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicMax(p.nonfinite, b + p.batch_offset);
