@@ -67,7 +67,9 @@ typedef struct hps_ctx_s* hps_ctx_t;
 #define HPS_OPT_EMU_TILE_GROUP 12   /* tile rows per group of the tcgen05 kernel's tile order (0: ~32 MB of A) */
 #define HPS_OPT_EMU_SOLVE 13        /* batched solve (b >= 64) through the emulation too (0: DMMA; measured slower
                                        at b = 256: S is read once, its residues cost about what DMMA saves) */
-#define HPS_OPT_COUNT 14
+#define HPS_OPT_EMU_SPLIT 14        /* operand residues of the modular scheme: integer pipes + a small int8 MMA per
+                                       element pair (1) or the FP64 pipe (0) */
+#define HPS_OPT_COUNT 15
 int hps_ctx_create(int device, hps_ctx_t* out);
 int hps_ctx_destroy(hps_ctx_t ctx);
 int hps_ctx_set_option(hps_ctx_t ctx, int option, long long value);

@@ -45,6 +45,7 @@ HPS_OPT_EMU_SCRATCH_MB = 10
 HPS_OPT_EMU_ENGINE = 11
 HPS_OPT_EMU_TILE_GROUP = 12
 HPS_OPT_EMU_SOLVE = 13
+HPS_OPT_EMU_SPLIT = 14
 
 HPS_MERGE_PIVOTED = 1
 HPS_MERGE_PARENT_PIVOTED = 2

@@ -21,7 +21,7 @@ struct Ctx {
   // emulation for K >= 512 and >= 2^32 multiply-adds: the modular scheme with 14 moduli
   // (FP64-equivalent accuracy; the 8-slice scheme when moduli = 0), <= 8 GB of products, int8
   // products on this library's tcgen05 kernel
-  long long opt[HPS_OPT_COUNT] = {1, 16, 1, 2, 0, 0, 8, 1LL << 32, 512, 14, 8192, 0, 0, 0};
+  long long opt[HPS_OPT_COUNT] = {1, 16, 1, 2, 0, 0, 8, 1LL << 32, 512, 14, 8192, 0, 0, 0, 1};
   // side streams: 1 = fork (recursive inverse), 2/3 = look-ahead inverse pair (highest priority)
   cudaStream_t side = nullptr, ahead = nullptr, ahead_side = nullptr;
   bool streams_ok = false;

@@ -638,6 +638,250 @@ __global__ void __launch_bounds__(256) k_crt_split_cols(const double* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Residues on the integer pipes (HPS_OPT_EMU_SPLIT 1, the default): the FP64-pipe version above
+// spends ~63 FP64 operations per element and is bound by that pipe. Here the scaled integer y (|y| <=
+// 2^61) is converted once (cvt.rni.s64.f64) and shifted to v = y + S > 0, S a multiple of every
+// modulus of a group (the first eight moduli; the rest), so v = y modulo each of them. The eight
+// bytes d_i of v feed a small int8 tensor-core product (legacy mma.sync m16n8k32, u8 x s8):
+//   c_l = sum_i d_i (256^i mod m_l)     (symmetric constants: |c_l| < 2^18) is congruent to y.
+// A lane holds two elements (MMA rows g and g + 8); an MMA row is four consecutive elements (one per
+// lane of a quad), and the B fragment is block-diagonal over those four slots, so one MMA yields 2
+// moduli x 4 slots for 16 + 16 elements and 7 MMAs cover 14 moduli. Then
+//   q = floor((c + h) / m) = (c minv + h minv + 2^20) >> 32   (exact for |c| < 2^18: minv = floor(2^32 /
+//                                        m) + 1, the 2^20 outweighs minv's excess times a negative c)
+//   r = c - q m in [-h, m - 1 - h], h = floor(m / 2): a signed byte congruent to y,
+// two integer multiply-adds per residue; the four slots of a row are packed into one word with byte
+// permutes and one quad shuffle. ~65 instructions per element instead of ~167.
+struct ResTab {
+  unsigned clo[CRT_MAX], chi[CRT_MAX];  // 256^i mod m as signed bytes, i = 0..3 and 4..7
+  unsigned minv[CRT_MAX], kq[CRT_MAX];  // floor(2^32 / m) + 1, and h * minv + 2^20 (< 2^32)
+  int m[CRT_MAX];
+  unsigned long long shift[2];          // S of the moduli 0..7 and of the moduli 8..
+};
+static bool res_tab(int n, ResTab& t) {
+  typedef unsigned __int128 u128;
+  for (int grp = 0; grp < 2; ++grp) {
+    u128 P = 1;
+    for (int l = 8 * grp; l < std::min(n, 8 * grp + 8); ++l) P *= (u128)kModuli[l];
+    const u128 lo = (u128)1 << 61, hi = ((u128)1 << 64) - ((u128)1 << 61);  // v = y + S in (0, 2^64) for |y| <= 2^61
+    u128 S = P * std::max<u128>(1, ((u128)1 << 62) / P);
+    if (S < lo || S > hi) return false;
+    t.shift[grp] = (unsigned long long)S;
+  }
+  for (int l = 0; l < CRT_MAX; ++l) {
+    const int m = kModuli[l < n ? l : 0];
+    unsigned lo = 0, hi = 0;
+    long long pw = 1;
+    for (int i = 0; i < 8; ++i) {
+      int c = (int)(pw % m);
+      if (c >= (m + 1) / 2) c -= m;  // [-128, 127]
+      (i < 4 ? lo : hi) |= (unsigned)(c & 0xFF) << (8 * (i & 3));
+      pw = (pw * 256) % m;
+    }
+    t.clo[l] = lo;
+    t.chi[l] = hi;
+    t.minv[l] = (unsigned)((1ULL << 32) / (unsigned long long)m) + 1u;
+    t.kq[l] = (unsigned)(m / 2) * t.minv[l] + (1u << 20);
+    t.m[l] = m;
+  }
+  return true;
+}
+
+// keeps a per-lane constant in its register: ptxas otherwise re-reads the parameter bank (an indexed
+// LDC through the address-divergence unit) at every use, which then bounds the kernel. A shuffle
+// from the own lane is opaque to it.
+__device__ __forceinline__ void res_pin(unsigned& x) {
+  asm volatile("{\n\t.reg .u32 l;\n\tmov.u32 l, %%laneid;\n\tshfl.sync.idx.b32 %0, %0, l, 31, 0xffffffff;\n\t}" : "+r"(x));
+}
+__device__ __forceinline__ void res_pin(int& x) {
+  asm volatile("{\n\t.reg .u32 l;\n\tmov.u32 l, %%laneid;\n\tshfl.sync.idx.b32 %0, %0, l, 31, 0xffffffff;\n\t}" : "+r"(x));
+}
+
+template <int NM>
+struct ResFrag {  // a lane's constants: B fragments of the NJ MMAs and the reduction constants of its moduli
+  static constexpr int NJ = (NM + 1) / 2;
+  unsigned b0[NJ], b1[NJ];
+  int minv[NJ], negm[NJ];
+  long long kq[NJ];
+  __device__ __forceinline__ void init(const ResTab& t, int lane) {
+    const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int lb = 2 * j + (g >> 2);  // B column g: modulus lb, element slot g & 3
+      const bool on = tq == (g & 3) && lb < NM;
+      b0[j] = on ? t.clo[lb < NM ? lb : 0] : 0u;
+      b1[j] = on ? t.chi[lb < NM ? lb : 0] : 0u;
+      const int lc = 2 * j + (tq >> 1) < NM ? 2 * j + (tq >> 1) : 0;  // C columns 2 tq, 2 tq + 1: modulus lc
+      negm[j] = -t.m[lc];
+      minv[j] = (int)t.minv[lc];
+      unsigned k = t.kq[lc];
+      res_pin(b0[j]);
+      res_pin(b1[j]);
+      res_pin(negm[j]);
+      res_pin(minv[j]);
+      res_pin(k);
+      kq[j] = (long long)k;
+    }
+  }
+};
+
+// w[j]: the residues modulo m_(2j + (tq >> 1)) of four consecutive elements as one word of signed
+// bytes. y0 is this lane's element of the first 32 (element index = lane), y1 of the second 32. Even
+// lanes receive the word of elements 4g .. 4g + 3, odd lanes that of elements 32 + 4g .. 32 + 4g + 3.
+template <int NM>
+__device__ __forceinline__ void res_words(long long y0, long long y1, const ResFrag<NM>& f, const ResTab& t, int lane,
+                                          unsigned (&w)[ResFrag<NM>::NJ]) {
+  const bool odd = lane & 1;
+#pragma unroll
+  for (int j = 0; j < ResFrag<NM>::NJ; ++j) {
+    const unsigned long long S = t.shift[j >= 4 ? 1 : 0];  // MMA j: moduli 2j, 2j + 1
+    const unsigned long long v0 = (unsigned long long)y0 + S, v1 = (unsigned long long)y1 + S;
+    int c0, c1, c2, c3;
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, {%10, %10, %10, %10};"
+                 : "=r"(c0), "=r"(c1), "=r"(c2), "=r"(c3)
+                 : "r"((unsigned)v0), "r"((unsigned)v1), "r"((unsigned)(v0 >> 32)), "r"((unsigned)(v1 >> 32)), "r"(f.b0[j]),
+                   "r"(f.b1[j]), "r"(0));
+    auto red = [&](int c) {  // c - m floor((c + h) / m)
+      const int q = (int)(((long long)c * (long long)f.minv[j] + f.kq[j]) >> 32);
+      return (unsigned)(q * f.negm[j] + c);
+    };
+    const unsigned pg = __byte_perm(red(c0), red(c1), 0x0040), pg8 = __byte_perm(red(c2), red(c3), 0x0040);
+    const unsigned recv = __shfl_xor_sync(0xffffffffu, odd ? pg : pg8, 1);
+    w[j] = __byte_perm(odd ? recv : pg, odd ? pg8 : recv, 0x5410);
+  }
+}
+
+// x 2^e rounded to an integer (ties to even, as rint), e fixed per row / column: one multiply when 2^e
+// is a normal number
+__device__ __forceinline__ long long res_scaled(double x, int e, double pw, bool direct) {
+  return __double2ll_rn(direct ? x * pw : ldexp(x, e));
+}
+
+// residues of the scaled rows of A: out[l][b][i][k]; a warp takes 256 consecutive k of a row in 4
+// steps of 64 (the 8 loads of a lane issued first); 128 threads, 5 CTAs per SM (96 registers)
+template <int NM>
+__global__ void __launch_bounds__(128, 5) k_crt_split_rows_mma(const double* __restrict__ A, long long lda, long long sA,
+                                                              int M, int K, int batch, const int* __restrict__ sig,
+                                                              ResTab t, signed char* __restrict__ out) {
+  constexpr int NJ = ResFrag<NM>::NJ;
+  const int b = blockIdx.z, r = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kbeg = (blockIdx.x * 4 + warp) * 256;
+  if (kbeg >= K) return;
+  ResFrag<NM> f;
+  f.init(t, lane);
+  const int sg = sig[(long long)b * M + r];
+  const bool direct = sg >= -1022 && sg <= 1023;
+  const double pw = __longlong_as_double((long long)((direct ? sg : 0) + 1023) << 52);
+  const double* Ar = A + (long long)b * sA + (long long)r * lda;
+  double x[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = kbeg + 32 * s + lane;
+    x[s] = (k < K && sg != INT_MIN) ? __ldg(Ar + k) : 0.0;
+  }
+  const long long plane = (long long)batch * M * K;
+  const int g = lane >> 2, tq = lane & 3;
+  const int lmine = tq >> 1, koff = (lane & 1) * 32 + 4 * g;
+  // this lane's word of modulus 2j + lmine at step s: obase + 2 j plane + 64 s
+  signed char* obase = out + ((long long)b * M + r) * K + lmine * plane + kbeg + koff;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int k0 = kbeg + 64 * s;
+    if (k0 >= K) break;
+    unsigned w[NJ];
+    res_words<NM>(res_scaled(x[2 * s], sg, pw, direct), res_scaled(x[2 * s + 1], sg, pw, direct), f, t, lane, w);
+    if (k0 + koff < K) {
+      signed char* o = obase + 64 * s;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        if (2 * j + lmine < NM) *reinterpret_cast<unsigned*>(o) = w[j];
+        o += 2 * plane;
+      }
+    }
+  }
+}
+
+// residues of the scaled columns of B, transposed: out[l][b][j][k]. CTA tile 32 k x 64 j in three
+// phases through shared memory: (1) coalesced row reads, each element scaled by its column's power of
+// two and converted to an integer; (2) warp w takes columns 16w .. 16w + 15: per step a lane holds
+// the integers of (k = 4s + tq, j = g) and (k = 4s + tq, j = 8 + g), so a quad = four consecutive k
+// of one column = one output word, staged at [l][j][s]; (3) the 32 bytes of every (l, j) leave as
+// full sectors (8 lanes x 4 bytes).
+template <int NM>
+struct ResColsSmem {
+  static constexpr int SY = 68;           // integer tile row stride (64-bit words; == 4 mod 16: phase 2's quad reads are conflict-free)
+  static constexpr int SL = 64 * 9 + 16;  // words per modulus: 64 columns x (8 words + 1 pad), + 16 so that a lane pair's two moduli take different banks
+  static constexpr int kBytes = 32 * SY * 8 + NM * SL * 4;
+};
+template <int NM>
+__global__ void __launch_bounds__(128, 4) k_crt_split_cols_mma(const double* __restrict__ B, long long ldb, long long sB,
+                                                              int K, int N, int batch, const int* __restrict__ tau,
+                                                              ResTab t, signed char* __restrict__ out) {
+  constexpr int NJ = ResFrag<NM>::NJ;
+  constexpr int SY = ResColsSmem<NM>::SY, SL = ResColsSmem<NM>::SL;
+  extern __shared__ __align__(16) unsigned char res_smem[];
+  long long* sy = reinterpret_cast<long long*>(res_smem);               // 32 x SY integers
+  unsigned* so = reinterpret_cast<unsigned*>(res_smem + 32 * SY * 8);  // [l][j][s]: NM x SL words
+  const int b = blockIdx.z, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int j0 = blockIdx.x * 64, k0 = blockIdx.y * 32;
+  {  // phase 1: thread -> column pair 2 (tid % 32), rows tid / 32 + 4 i
+    const int jc = j0 + 2 * lane;
+    const int t0 = jc < N ? tau[(long long)b * N + jc] : INT_MIN, t1 = jc + 1 < N ? tau[(long long)b * N + jc + 1] : INT_MIN;
+    const int e0 = t0 == INT_MIN ? 0 : t0, e1 = t1 == INT_MIN ? 0 : t1;
+    const bool d0 = e0 >= -1022 && e0 <= 1023, d1 = e1 >= -1022 && e1 <= 1023;
+    const double p0 = __longlong_as_double((long long)((d0 ? e0 : 0) + 1023) << 52);
+    const double p1 = __longlong_as_double((long long)((d1 ? e1 : 0) + 1023) << 52);
+    const double* Bb = B + (long long)b * sB + jc;
+    const bool vec = jc + 1 < N && !(ldb & 1) && !(reinterpret_cast<uintptr_t>(B) & 15) && !(sB & 1);
+    double2 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int k = k0 + warp + 4 * i;
+      x[i] = make_double2(0.0, 0.0);
+      if (k < K) {
+        if (vec) {
+          x[i] = __ldg(reinterpret_cast<const double2*>(Bb + (long long)k * ldb));
+        } else {
+          if (jc < N) x[i].x = __ldg(Bb + (long long)k * ldb);
+          if (jc + 1 < N) x[i].y = __ldg(Bb + (long long)k * ldb + 1);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int kr = warp + 4 * i;
+      const long long y0 = t0 == INT_MIN ? 0 : res_scaled(x[i].x, e0, p0, d0);
+      const long long y1 = t1 == INT_MIN ? 0 : res_scaled(x[i].y, e1, p1, d1);
+      *reinterpret_cast<longlong2*>(&sy[kr * SY + 2 * lane]) = make_longlong2(y0, y1);
+    }
+  }
+  ResFrag<NM> f;
+  f.init(t, lane);
+  __syncthreads();
+  {  // phase 2
+    const int jl = 16 * warp + g;  // local columns jl and jl + 8
+    const int jm = (lane & 1) ? jl + 8 : jl, lmine = tq >> 1;
+#pragma unroll 2
+    for (int s = 0; s < 8; ++s) {
+      unsigned w[NJ];
+      res_words<NM>(sy[(4 * s + tq) * SY + jl], sy[(4 * s + tq) * SY + jl + 8], f, t, lane, w);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (2 * j + lmine < NM) so[(2 * j + lmine) * SL + jm * 9 + s] = w[j];
+    }
+  }
+  __syncthreads();
+  const long long plane = (long long)batch * N * K;
+  signed char* ob = out + (long long)b * N * K;
+  for (int idx = tid; idx < NM * 64 * 8; idx += 128) {  // 4 bytes per store
+    const int wq = idx % 8, rest = idx / 8, jr = rest % 64, l = rest / 64;
+    const int k = k0 + 4 * wq, jg = j0 + jr;
+    if (k < K && jg < N) *reinterpret_cast<unsigned*>(ob + l * plane + (long long)jg * K + k) = so[l * SL + jr * 9 + wq];
+  }
+}
+
 #define HPS_CRT_SWITCH(n, CALL)                                                                            \
   switch (n) {                                                                                             \
     case 2: CALL(2); break; case 3: CALL(3); break; case 4: CALL(4); break; case 5: CALL(5); break;        \
@@ -916,18 +1160,41 @@ static int emu_gemm_crt(const GemmParams& p, Ctx& cx, cudaStream_t st) {
   HPS_LAUNCH_CHECK();
   k_crt_col_scale<<<dim3((p.N + 31) / 32, p.batch), 256, 0, st>>>(p.B, p.ldb, p.strideB, p.K, p.N, c.PB, tau);
   HPS_LAUNCH_CHECK();
+  // the operands' residue bytes: A rows and B columns (transposed), K-contiguous; 16-byte stores need
+  // K % 16 == 0 (emu_eligible) and 256-byte aligned planes (align above)
+  if (cx.opt[HPS_OPT_EMU_SPLIT] != 0) {  // integer pipes + int8 MMA (default)
+    ResTab rt;
+    if (!res_tab(n, rt)) return 1;
+#define HPS_SPLIT_ROWS(NM)                                                                                          \
+  k_crt_split_rows_mma<NM><<<dim3((p.K + 1023) / 1024, p.M, p.batch), 128, 0, st>>>(p.A, p.lda, p.strideA, p.M, p.K, \
+                                                                                    p.batch, sig, rt, Ar)
+    HPS_CRT_SWITCH(n, HPS_SPLIT_ROWS)
+#undef HPS_SPLIT_ROWS
+    HPS_LAUNCH_CHECK();
+#define HPS_SPLIT_COLS(NM)                                                                                      \
+  {                                                                                                             \
+    const int as = ensure_smem_attr((const void*)k_crt_split_cols_mma<NM>, cx.device, ResColsSmem<NM>::kBytes); \
+    if (as != HPS_OK) return as;                                                                                \
+    k_crt_split_cols_mma<NM><<<dim3((p.N + 63) / 64, (p.K + 31) / 32, p.batch), 128, ResColsSmem<NM>::kBytes, st>>>( \
+        p.B, p.ldb, p.strideB, p.K, p.N, p.batch, tau, rt, Br);                                                 \
+  }
+    HPS_CRT_SWITCH(n, HPS_SPLIT_COLS)
+#undef HPS_SPLIT_COLS
+    HPS_LAUNCH_CHECK();
+  } else {  // FP64 pipe
 #define HPS_SPLIT_ROWS(NM)                                                                                   \
   k_crt_split_rows<NM><<<dim3((p.K / 4 + 255) / 256, p.M, p.batch), 256, 0, st>>>(p.A, p.lda, p.strideA, p.M, p.K, \
                                                                                  p.batch, sig, c, Ar)
-  HPS_CRT_SWITCH(n, HPS_SPLIT_ROWS)
+    HPS_CRT_SWITCH(n, HPS_SPLIT_ROWS)
 #undef HPS_SPLIT_ROWS
-  HPS_LAUNCH_CHECK();
+    HPS_LAUNCH_CHECK();
 #define HPS_SPLIT_COLS(NM)                                                                                        \
   k_crt_split_cols<NM><<<dim3((p.N + 63) / 64, (p.K + 31) / 32, p.batch), 256, 0, st>>>(p.B, p.ldb, p.strideB, p.K, \
                                                                                       p.N, p.batch, tau, c, Br)
-  HPS_CRT_SWITCH(n, HPS_SPLIT_COLS)
+    HPS_CRT_SWITCH(n, HPS_SPLIT_COLS)
 #undef HPS_SPLIT_COLS
-  HPS_LAUNCH_CHECK();
+    HPS_LAUNCH_CHECK();
+  }
   const int one = 1, zero = 0;
   for (int j0 = 0; j0 < p.N; j0 += nc) {
     const int w = std::min(nc, p.N - j0);

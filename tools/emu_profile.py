@@ -1,6 +1,6 @@
 """Per-kernel device times of one emulated (or DMMA) merge-shaped GEMM through hps_dgemm_batched,
 from torch.profiler (CUPTI): which of scales / residues / int8 products / reconstruction dominate
-(dev tool). Usage: python tools/emu_profile.py M N K batch [moduli slices scratch_mb engine tile_group]"""
+(dev tool). Usage: python tools/emu_profile.py M N K batch [moduli slices scratch_mb engine tile_group split]"""
 import sys
 from collections import defaultdict
 
@@ -17,8 +17,9 @@ slices = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 scratch = int(sys.argv[7]) if len(sys.argv) > 7 else 8192
 engine = int(sys.argv[8]) if len(sys.argv) > 8 else 0
 group = int(sys.argv[9]) if len(sys.argv) > 9 else 0
+split = int(sys.argv[10]) if len(sys.argv) > 10 else 1
 cx = _native.Context(0, emu_moduli=moduli, emu_slices=slices, emu_scratch_mb=scratch, emu_engine=engine,
-                     emu_tile_group=group, emu_min_k=16)
+                     emu_tile_group=group, emu_min_k=16, emu_split=split)
 A = torch.randn(B, M, K, dtype=torch.float64, device="cuda")
 Bm = torch.randn(B, K, N, dtype=torch.float64, device="cuda")
 C = torch.empty(B, M, N, dtype=torch.float64, device="cuda")
