@@ -435,6 +435,10 @@ static bool crt_constants(int n, CrtConst& c) {
   for (int g = 0; 3 * g < n; ++g) {
     double P = 1.0;
     for (int l = 3 * g; l < std::min(n, 3 * g + 3); ++l) P *= (double)kModuli[l];  // < 2^24, exact
+    // a short last group (n % 3 != 0): a power-of-two multiple of the product reduces just as well
+    // (every modulus of the group divides it) and keeps the first quotient x / P below 2^51 for
+    // |x| up to 2^61 (16 moduli; with P = 193 alone the 1.5 * 2^52 shift no longer rounded it)
+    while (P < 0x1p20) P *= 2.0;
     c.gP[g] = P;
     c.ginvP[g] = 1.0 / P;
   }
@@ -557,7 +561,7 @@ __global__ void __launch_bounds__(256) k_crt_col_scale(const double* __restrict_
   }
 }
 
-// Residues of the integer x (|x| <= 2^55, exact in fp64) modulo every m_l, each in [-128, 128]
+// Residues of the integer x (|x| <= 2^61, exact in fp64) modulo every m_l, each in [-128, 128]
 // (+128 only for m = 256, whose byte wraps to the same class), as the low bytes of r[l]. Two levels,
 // all on the FP64 pipe and without range fixes: y = x mod P_g for the product P_g < 2^24 of three
 // moduli (the quotient rounded through the 1.5 * 2^52 shift may be one off, so |y| <= 1.5 P_g <

@@ -222,7 +222,7 @@ def test_emulated_dgemm_accuracy(M, N, K, B, scheme, count):
         assert errs["emu"] <= 2.0 ** -40, errs
 
 
-@pytest.mark.parametrize("moduli", [14, 16])
+@pytest.mark.parametrize("moduli", [13, 14, 15, 16])
 def test_emulated_dgemm_nonfinite_and_panels(moduli):
     """Modular emulation: output column panels (a small scratch cap forces several), the merge's
     alpha, a non-finite row (NaN row of the output, flagged like the DMMA path) and zero rows."""
@@ -329,6 +329,37 @@ def test_i8gemm_mod_rejects_bad_arguments():
     r = lib.hps_i8gemm_mod(_native.context(), _native.ptr(t), _native.ptr(t), _native.ptr(t), 16, 64, 48, 0, 32, 2, 1,
                            mods, 2, 0, _native.stream_ptr())  # nc % 32 != 0
     assert r == _native.HPS_ERR_ARG and "unsupported" in _native.last_error()
+
+
+@pytest.mark.parametrize("moduli", [6, 13, 14, 15, 16])
+@pytest.mark.parametrize("M,N,K,B", [(200, 544, 272, 2), (132, 100, 1040, 3), (512, 512, 4096, 1)])
+def test_emulated_dgemm_split_paths_bitwise(M, N, K, B, moduli):
+    """Modular emulation: the operand residues computed on the integer pipes (int64 conversion, a
+    small int8 MMA per element pair, integer reduction; HPS_OPT_EMU_SPLIT 1) are the same signed
+    bytes as the FP64-pipe ones (0), so the products are bitwise equal; partial tiles in M, N and K,
+    every leftover count of moduli (NM % 4), scales spread over 40 binades."""
+    lib = _native.load()
+    rng = np.random.default_rng(M + moduli)
+    A = rng.standard_normal((B, M, K)) * np.exp2(rng.integers(-20, 20, (B, M, 1)))
+    Bm = rng.standard_normal((B, K, N)) * np.exp2(rng.integers(-20, 20, (B, 1, N)))
+    A[0, 3, :] = 0.0
+    outs = []
+    for split in (0, 1):
+        cx = _native.Context(0, emu_min_work=1, emu_min_k=16, emu_slices=0, emu_moduli=moduli, emu_split=split)
+        try:
+            tA, tB = cuda(A), cuda(Bm)
+            tC = torch.zeros((B, M, N), dtype=torch.float64, device="cuda")
+            _native.check(lib.hps_dgemm_batched(cx, M, N, K, B, 1.0, _native.ptr(tA), K, M * K, _native.ptr(tB), N,
+                                                K * N, None, 0, 0.0, _native.ptr(tC), N, M * N, _native.stream_ptr()),
+                          "gemm")
+            outs.append(tC.cpu().numpy())
+        finally:
+            cx.close()
+    assert np.array_equal(outs[0], outs[1])
+    ref = np.einsum("bmk,bkn->bmn", A, Bm)
+    scale = np.abs(A).max(axis=2)[:, :, None] * np.abs(Bm).max(axis=1)[:, None, :] * K
+    scale[0, 3] = 1.0
+    assert float((np.abs(outs[1] - ref) / scale).max()) <= (2.0 ** -50 if moduli >= 13 else 2.0 ** -10)
 
 
 def test_emulated_dgemm_extreme_scales():
