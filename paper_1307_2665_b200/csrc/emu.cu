@@ -503,7 +503,7 @@ __global__ void k_crt_row_scale(const double* __restrict__ A, long long lda, lon
   if (lane == 0) sig[(long long)b * M + r] = e;
 }
 
-// 32 columns x 8 row slices per CTA (coalesced row reads), 4 rows in flight per thread
+// 32 columns x 8 row slices per CTA (coalesced row reads), 8 rows in flight per thread
 __global__ void __launch_bounds__(256) k_crt_col_scale(const double* __restrict__ B, long long ldb, long long sB, int K,
                                                       int N, int P, int* __restrict__ tau) {
   __shared__ double red[2][8][33];
@@ -514,12 +514,14 @@ __global__ void __launch_bounds__(256) k_crt_col_scale(const double* __restrict_
   const double* Bb = B + (long long)b * sB + j;
   double mx[4] = {0.0, 0.0, 0.0, 0.0}, ss[4] = {0.0, 0.0, 0.0, 0.0};
   if (j < N)
-    for (int k = ty; k < K; k += 32) {
+    for (int k = ty; k < K; k += 64) {  // 8 loads in flight per thread
+      double v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double v = k + 8 * u < K ? __ldg(Bb + (long long)(k + 8 * u) * ldb) : 0.0;
-        mx[u] = fmax(mx[u], fabs(v));
-        ss[u] = fma(v, v, ss[u]);
+      for (int u = 0; u < 8; ++u) v[u] = k + 8 * u < K ? __ldg(Bb + (long long)(k + 8 * u) * ldb) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        mx[u & 3] = fmax(mx[u & 3], fabs(v[u]));
+        ss[u & 3] = fma(v[u], v[u], ss[u & 3]);
       }
     }
   red[0][ty][tx] = fmax(fmax(mx[0], mx[1]), fmax(mx[2], mx[3]));
