@@ -226,3 +226,47 @@ def test_crt_reconstruction_model():
         X = shi - q * float(Mh)  # exact
         cp = X * twoE + (slo - q * float(Mlo))
         assert abs(cp - C) <= 2.0 ** (bits - 4 - 52), (C, cp)
+
+
+def test_residue_reduction_model():
+    """The integer-pipe operand residues of the modular emulation (csrc/emu.cu, res_tab / res_words)
+    restated with numpy integers: the group shift S is a multiple of every modulus of its group and
+    keeps v = y + S inside (0, 2^64) for |y| <= 2^61; the byte sums c = sum d_i (256^i mod m) (the
+    int8 MMA) are congruent to v and below 2^18 in magnitude; over that whole range the multiply-high
+    quotient with the 2^20 bias equals floor((c + h) / m) and r = c - q m is a signed byte congruent
+    to y."""
+    import math
+
+    moduli = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193]
+    rng = np.random.default_rng(5)
+    for n in (6, 13, 14, 15, 16):
+        for grp in (moduli[:min(n, 8)], moduli[8:n]):
+            if not grp:
+                continue
+            P = math.prod(grp)
+            S = P * max(1, (1 << 62) // P)
+            assert (1 << 61) <= S <= (1 << 64) - (1 << 61)
+            assert all(S % m == 0 for m in grp)
+            ys = [int(v) for v in rng.integers(-(1 << 61), 1 << 61, 64)] + [-(1 << 61), 1 << 61, 0, -1, 1]
+            for m in grp:
+                consts = []
+                pw = 1
+                for _ in range(8):
+                    cc = pw % m
+                    consts.append(cc - m if cc >= (m + 1) // 2 else cc)
+                    pw = pw * 256 % m
+                assert all(-128 <= cc <= 127 for cc in consts)
+                for y in ys:
+                    v = y + S
+                    assert 0 < v < 1 << 64
+                    c = sum(((v >> (8 * i)) & 0xFF) * consts[i] for i in range(8))
+                    assert abs(c) < 1 << 18 and (c - y) % m == 0
+    c = np.arange(-(1 << 18), 1 << 18, dtype=np.int64)
+    for m in moduli:
+        h, minv = m // 2, (1 << 32) // m + 1
+        kq = h * minv + (1 << 20)
+        assert kq < 1 << 32
+        q = (c * minv + kq) >> 32  # arithmetic shift: floor
+        assert np.array_equal(q, (c + h) // m)
+        r = c - q * m
+        assert r.min() >= -h and r.max() <= m - 1 - h and -128 <= r.min() and r.max() <= 127
