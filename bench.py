@@ -67,6 +67,8 @@ def parse():
                          "CTA-pair variant, 1 = cuBLASLt")
     ap.add_argument("--emu-min-k", type=int, default=None, help="emulate merge GEMMs with K >= this (default 512)")
     ap.add_argument("--emu-solve", type=int, default=None, help="batched solve through the emulation too (default 0)")
+    ap.add_argument("--emu-split", type=int, default=None,
+                    help="operand residues on the integer pipes + int8 MMA (1, default) or the FP64 pipe (0)")
     ap.add_argument("--validate-reference-model", action="store_true",
                     help="time whole oracle-port steps at configs 2 (L=6) and 3 (L=7) against the sampled model")
     ap.add_argument("--full-reference", action="store_true",
@@ -166,7 +168,7 @@ def configure_emulation(args):
     """Apply the --emu-* options to every context slot; return the scheme that runs (csrc/emu.cu)."""
     from paper_1307_2665_b200 import _native
 
-    for name in ("emu_slices", "emu_moduli", "emu_engine", "emu_min_k", "emu_solve"):
+    for name in ("emu_slices", "emu_moduli", "emu_engine", "emu_min_k", "emu_solve", "emu_split"):
         v = getattr(args, name)
         if v is not None:
             for slot in range(4):
