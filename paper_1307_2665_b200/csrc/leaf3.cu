@@ -481,10 +481,14 @@ __global__ void __launch_bounds__(l3::THREADS, 2) k_leaf16v3(LeafArgs a) {
 #undef act0
 #undef act1
     // rank-kb update of M[act rows][c0 + [cbeg, cend)] by the update warps (uw = 0..3). Work item:
-    // 8 rows x CW columns whose C loads are all issued before the DMMAs (one L2 round trip).
+    // 8 rows x CW columns whose C loads are all issued before the DMMAs (one L2 round trip); CW = 64
+    // keeps a warp's DMMA burst at 32, so the panel warps' FP64 operations queue behind less.
     // uw >= 0: static round-robin over 4 update warps; uw < 0: pull items from s_next (any warp).
     auto update = [&](int k, int cbeg, int cend, int uw) {
-      constexpr int CW = 128, NJ = CW / 8;
+#ifndef HPS_LEAF_CW
+#define HPS_LEAF_CW 64  // 128: 4-5% slower once the panel warps have issue priority (longer DMMA bursts ahead of their FP64 ops); 32: the same as 64
+#endif
+      constexpr int CW = HPS_LEAF_CW, NJ = CW / 8;
       const int k0 = 16 * k, kb = min(16, NI - k0), c0 = k0 + kb, nT = LDM - c0;
       const int buf = k & 1;
       const int nact = s_nact[buf];
