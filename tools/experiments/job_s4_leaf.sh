@@ -1,4 +1,8 @@
 set -u
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_baseline_sizes.py tests/test_gpu_spec.py -m gpu -x -q > gpurun_out/s4_leaf_tests.log 2>&1; tail -2 gpurun_out/s4_leaf_tests.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_spec.py -m gpu -x -q > gpurun_out/s4_leaf_tests.log 2>&1; tail -2 gpurun_out/s4_leaf_tests.log
+run() { timeout 300 python bench.py --config $1 --no-cpu-baseline > gpurun_out/s4_ab.json 2> gpurun_out/s4_ab.err; python -c "
+import json,sys; d=json.loads(open('gpurun_out/s4_ab.json').read().strip().splitlines()[-1]); st=d['stages']; print('$2', $1, round(d['ms_per_step'],3), round(st['build_ms'],3), round(d['roofline']['achieved'],2))"; }
+run 2 new
+run 2 new
+run 4 new
