@@ -135,16 +135,22 @@ __device__ __forceinline__ void tile_coords(long long t, int tm, int tn, int G, 
   ni = rr / gs;
 }
 
-// (v mod m) + 128 in [0, 255] for |v| < 2^30: v + m ceil(2^30 / m) is in [0, 2^31), its
-// multiply-high quotient (minv = floor(2^32 / m)) is the floor or one less, so the remainder is in
-// [0, 2m); one correction, then the symmetric representative, biased.
+// The biased symmetric residue ((v mod m) in [128 - m, 127]) + 128 of |v| < 2^30, in six integer
+// operations. With off = m (floor(2^30 / m) + 1) + (m - 128), t = v + off is in [0, 2^31 + 2m) and
+// congruent to v - 128, and for r' = t mod m the result is r' + (256 - m) whichever half v mod m lies
+// in (v mod m = r' + 128 - m <= 127 if r' + 128 >= m, else r' + 128 > 127 and the representative is
+// r' + 128 - m: both give r' + 256 - m), so no centring test. The multiply-high quotient (minv =
+// floor(2^32 / m)) is the floor or one less, so t - q m is in [0, 2m): one unsigned-min correction.
 __device__ __forceinline__ uint32_t mod_byte(uint32_t u, int m, int minv, int off) {
-  const unsigned v = (unsigned)((int)u + off);
-  const int q = (int)__umulhi(v, (unsigned)minv);
-  int r = (int)v - q * m;
-  r = r >= m ? r - m : r;
-  r = r > 127 ? r - m : r;
-  return (uint32_t)(r + 128);
+  const unsigned t = u + (unsigned)off;
+  const unsigned r = t - __umulhi(t, (unsigned)minv) * (unsigned)m;
+  return min(r, r - (unsigned)m) + (unsigned)(256 - m);
+}
+// pack four of them into a word of bytes
+__device__ __forceinline__ uint32_t mod_bytes4(const uint32_t* v, int m, int minv, int off) {
+  const uint32_t lo = __byte_perm(mod_byte(v[0], m, minv, off), mod_byte(v[1], m, minv, off), 0x0040);
+  const uint32_t hi = __byte_perm(mod_byte(v[2], m, minv, off), mod_byte(v[3], m, minv, off), 0x0040);
+  return __byte_perm(lo, hi, 0x5410);
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row = mi * BM + q * 32 + lane;
       const int l = z / batch;
       const int m = mt.m[l];
-      const int minv = mt.minv[l], off = m * ((1 << 30) / m + 1);
+      const int minv = mt.minv[l], off = m * ((1 << 30) / m + 1) + (m - 128);
       unsigned char* dst = R + ((long long)z * M + row) * nc + ni * BN;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
 #pragma unroll 1
@@ -264,8 +270,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint32_t w[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            w[i] = mod_byte(v[4 * i], m, minv, off) | (mod_byte(v[4 * i + 1], m, minv, off) << 8) |
-                   (mod_byte(v[4 * i + 2], m, minv, off) << 16) | (mod_byte(v[4 * i + 3], m, minv, off) << 24);
+            w[i] = mod_bytes4(v + 4 * i, m, minv, off);
           uint4* o = reinterpret_cast<uint4*>(dst + c * 32);
           o[0] = make_uint4(w[0], w[1], w[2], w[3]);
           o[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -450,7 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int row = mi * pair::BM + (int)rank * 128 + q * 32 + lane;
       const int l = z / batch;
       const int m = mt.m[l];
-      const int minv = mt.minv[l], off = m * ((1 << 30) / m + 1);
+      const int minv = mt.minv[l], off = m * ((1 << 30) / m + 1) + (m - 128);
       unsigned char* dst = R + ((long long)z * M + row) * nc + ni * pair::BN;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * pair::BN;
 #pragma unroll 1
@@ -461,8 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           uint32_t w[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            w[i] = mod_byte(v[4 * i], m, minv, off) | (mod_byte(v[4 * i + 1], m, minv, off) << 8) |
-                   (mod_byte(v[4 * i + 2], m, minv, off) << 16) | (mod_byte(v[4 * i + 3], m, minv, off) << 24);
+            w[i] = mod_bytes4(v + 4 * i, m, minv, off);
           uint4* o = reinterpret_cast<uint4*>(dst + c * 32);
           o[0] = make_uint4(w[0], w[1], w[2], w[3]);
           o[1] = make_uint4(w[4], w[5], w[6], w[7]);
