@@ -135,22 +135,23 @@ __device__ __forceinline__ void tile_coords(long long t, int tm, int tn, int G, 
   ni = rr / gs;
 }
 
-// The biased symmetric residue ((v mod m) in [128 - m, 127]) + 128 of |v| < 2^30, in six integer
+// The biased symmetric residue ((v mod m) in [128 - m, 127]) + 128 of |v| < 2^30, in five integer
 // operations. With off = m (floor(2^30 / m) + 1) + (m - 128), t = v + off is in [0, 2^31 + 2m) and
 // congruent to v - 128, and for r' = t mod m the result is r' + (256 - m) whichever half v mod m lies
 // in (v mod m = r' + 128 - m <= 127 if r' + 128 >= m, else r' + 128 > 127 and the representative is
 // r' + 128 - m: both give r' + 256 - m), so no centring test. The multiply-high quotient (minv =
 // floor(2^32 / m)) is the floor or one less, so t - q m is in [0, 2m): one unsigned-min correction.
-__device__ __forceinline__ uint32_t mod_byte(uint32_t u, int m, int minv, int off) {
+__device__ __forceinline__ uint32_t mod_raw(uint32_t u, int m, int minv, int off) {  // r' = (v + off) mod m
   const unsigned t = u + (unsigned)off;
   const unsigned r = t - __umulhi(t, (unsigned)minv) * (unsigned)m;
-  return min(r, r - (unsigned)m) + (unsigned)(256 - m);
+  return min(r, r - (unsigned)m);
 }
-// pack four of them into a word of bytes
+// four of them as a word of bytes; the + (256 - m) is added to all four at once (r' + 256 - m <= 255:
+// no carry between the bytes)
 __device__ __forceinline__ uint32_t mod_bytes4(const uint32_t* v, int m, int minv, int off) {
-  const uint32_t lo = __byte_perm(mod_byte(v[0], m, minv, off), mod_byte(v[1], m, minv, off), 0x0040);
-  const uint32_t hi = __byte_perm(mod_byte(v[2], m, minv, off), mod_byte(v[3], m, minv, off), 0x0040);
-  return __byte_perm(lo, hi, 0x5410);
+  const uint32_t lo = __byte_perm(mod_raw(v[0], m, minv, off), mod_raw(v[1], m, minv, off), 0x0040);
+  const uint32_t hi = __byte_perm(mod_raw(v[2], m, minv, off), mod_raw(v[3], m, minv, off), 0x0040);
+  return __byte_perm(lo, hi, 0x5410) + (uint32_t)(256 - m) * 0x01010101u;
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
