@@ -1046,14 +1046,18 @@ __global__ void __launch_bounds__(256, 4) k_crt_accum(const TIn* __restrict__ Cl
       cc.ctop[u] = col < n1;
       cc.cm[u] = p.blk_j1a ? (cc.ctop[u] ? p.blk_j1a[col] : p.blk_j2b[col - n1]) : 0;
     }
-    const TIn* src0 = Cl + (long long)b * M * nc + c4;
+    // 32-bit indices in units of V4 (four elements): n planes hold < 2^32 of them under the scratch
+    // cap (<= 8 GB, emu_gemm_crt), so a load costs one index add and one wide multiply-add
+    const V4* base = reinterpret_cast<const V4*>(Cl);
+    const unsigned planeV = (unsigned)(plane >> 2), ncV = (unsigned)nc >> 2;
+    const unsigned idx0 = (unsigned)b * (unsigned)M * ncV + ((unsigned)c4 >> 2);
     for (int r = blockIdx.y; r < M; r += gridDim.y) {
-      const TIn* src = src0 + (long long)r * nc;
+      unsigned idx = idx0 + (unsigned)r * ncV;
       V4 in[NM];
 #pragma unroll
       for (int l = 0; l < NM; ++l) {
-        in[l] = __ldcs(reinterpret_cast<const V4*>(src));
-        src += plane;
+        in[l] = __ldcs(base + idx);
+        idx += planeV;
       }
       crt_row<NM, TIn>(in, sig[(long long)b * M + r], cc, b, r, j0 + c4, p, c, bad);
     }
@@ -1127,7 +1131,8 @@ static int emu_gemm_crt(const GemmParams& p, Ctx& cx, cudaStream_t st) {
   // of 256 (the kernel's tile width) where the cap allows
   const bool own = cx.opt[HPS_OPT_EMU_ENGINE] != 1;  // 0: tcgen05 single CTAs, 2: CTA pairs, 1: cuBLASLt
   const size_t elt = own ? 1 : sizeof(int);  // the tcgen05 kernel stores residues, cuBLASLt int32 sums
-  const size_t cap = (size_t)std::max<long long>(1, cx.opt[HPS_OPT_EMU_SCRATCH_MB]) << 20;
+  // at most 8 GB of products: k_crt_accum indexes them with 32 bits (in units of four elements)
+  const size_t cap = (size_t)std::min<long long>(8192, std::max<long long>(1, cx.opt[HPS_OPT_EMU_SCRATCH_MB])) << 20;
   const size_t per_col = (size_t)n * p.batch * p.M * elt;
   const size_t maxc = std::max<size_t>(32, cap / per_col);
   int nc;
