@@ -738,11 +738,16 @@ def solve_device(state, F, out=None, ctx=None):
     b = F.shape[1]
     ldu = rhs_ld(b)
     N = lay.N
+    # Every row of U is written: the boundary rows [0, n_gamma) by the scatter of F (root.I_e is a
+    # permutation of them) and every interface range by its depth's solve (TreeLayout.depth_off), so
+    # only the padding columns of a batch that is not a multiple of 8 need zeros (the GEMM path
+    # reads them as right-hand sides).
     if out is None:
-        U = torch.zeros((N, ldu), dtype=torch.float64, device=state.device)
+        U = (torch.empty if ldu == b else torch.zeros)((N, ldu), dtype=torch.float64, device=state.device)
     else:
         U = out
-        U.zero_()
+        if ldu != b:
+            U.zero_()
     U[:, :b].index_copy_(0, state.root_Ie_dev, F.to(torch.float64))
     stream = _native.stream_ptr()
     for d in range(2 * lay.L):
